@@ -1,0 +1,140 @@
+/*
+ * dbp_b200.h -- C ABI of the B200-native overlap-save digital-backpropagation
+ * library (libdbp_b200.so).
+ *
+ * This is the drop-in boundary for the reference's DBP hot path
+ * (pkg/src/fiberdbp/dbp.py:160 ``backpropagate`` driving
+ * pkg/src/fiberdbp/spectral.py:87 ``overlap_save_run``).  Plain pointers and
+ * sizes only; no torch, numpy or C++ types cross it.  Every function returns
+ * DBP_OK (0) or a negative error code and never throws; the message of the
+ * last failure on the calling thread is available from dbp_last_error().
+ *
+ * Sample layout everywhere: complex64 (interleaved float re, im), batch-major
+ * rows ``[item][polarisation x|y][sample]``, i.e. each item is the reference's
+ * DualPolSignal.stack() (sigkit.py:73-75) in single precision.
+ *
+ * Threading: a plan belongs to one device; calls on one plan must be
+ * serialised by the caller.  Plans on different devices may be driven
+ * concurrently from different threads.
+ */
+#ifndef DBP_B200_H
+#define DBP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DBP_OK 0
+#define DBP_EINVAL (-1)   /* invalid argument  (reference: ValueError)  */
+#define DBP_ECUDA (-2)    /* CUDA runtime failure / no device           */
+#define DBP_ENOMEM (-3)   /* device or pinned-host allocation failed   */
+#define DBP_ESTATE (-4)   /* plan not configured (set_linear/set_steps) */
+
+/* algorithms: dbp.py:25 ALGORITHMS = ("ffe", "ssfm", "essfm"); 3 = rotation
+ * only (the nonlinear sub-step alone, dbp.py:49 / channel.py:61)           */
+#define DBP_ALG_FFE 0
+#define DBP_ALG_SSFM 1
+#define DBP_ALG_ESSFM 2
+#define DBP_ALG_ROTATE 3
+
+/* arrangements: dbp.py:32 ARRANGEMENTS                                      */
+#define DBP_ARR_SYMMETRIC 0
+#define DBP_ARR_LINEAR_FIRST 1
+#define DBP_ARR_NONLINEAR_FIRST 2
+
+#define DBP_MAX_SIDE_COEFFS 64   /* EssfmCoefficients.n_coeffs supported   */
+#define DBP_MIN_BLOCK_LEN 16     /* OverlapPlan.block_len range on the GPU */
+#define DBP_MAX_BLOCK_LEN 8192
+
+typedef struct dbp_plan dbp_plan;
+
+/* Message of the last failure on this thread ("" if none). */
+const char* dbp_last_error(void);
+
+/* ABI version (major * 100 + minor). */
+int dbp_version(void);
+
+/* Number of visible CUDA devices (0 when none). */
+int dbp_device_count(int* count);
+
+/* Plan for OverlapPlan(block_len, overlap) on ``device``
+ * (replaces the geometry checks of spectral.py:63-81).                      */
+int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap);
+int dbp_plan_destroy(dbp_plan* plan);
+
+/* Linear sub-step filters, natural FFT bin order, interleaved (re, im)
+ * float64, length 2*block_len each, exactly as the reference builds them
+ * (dbp.py:186 for FFE; dbp.py:196-197 ``kernel`` / ``half_kernel``).  The
+ * library folds numpy's 1/N inverse normalisation in and rounds to
+ * complex64.  ``half_kernel`` may be NULL unless the symmetric arrangement
+ * of a split-step program is used.                                          */
+int dbp_plan_set_linear(dbp_plan* plan, const double* kernel, const double* half_kernel);
+
+/* Step program (dbp.py:193-233).  ``weights``/``gains`` hold the reverse
+ * schedule's per-step nonlinear weight and amplitude gain in processing
+ * order (dbp.py:112-157), ``gamma`` the value the reference passes to the
+ * sub-step (i.e. -link.gamma, dbp.py:203/207); each rotation is
+ * exp(-j * gamma * weight_j * F).  ``coeffs`` = c_0..c_{n_coeffs} for
+ * ESSFM (sigkit.py:152-183), ignored otherwise.  FFE ignores everything
+ * but ``algorithm``.                                                         */
+int dbp_plan_set_steps(dbp_plan* plan, int algorithm, int arrangement, int num_steps,
+                       const double* weights, const double* gains, double gamma,
+                       const double* coeffs, int n_coeffs);
+
+/* Number of overlap-save blocks ceil(n_total / (N - M)) (spectral.py:126). */
+int dbp_num_blocks(const dbp_plan* plan, int64_t n_total, int64_t* out);
+
+/* Whole-signal run on device buffers (the GPU replacement of
+ * overlap_save_run(sig, plan, process), spectral.py:87-145): ``d_in`` and
+ * ``d_out`` are [batch][2][n_total] complex64; blocks
+ * [block_begin, block_end) of every item are processed with the circular
+ * extension of the whole signal and their kept centres written to the
+ * matching output samples.  Asynchronous on ``stream`` (cudaStream_t, NULL =
+ * legacy default stream).                                                    */
+int dbp_run(dbp_plan* plan, const void* d_in, void* d_out, int64_t n_total, int batch,
+            int64_t block_begin, int64_t block_end, void* stream);
+
+/* Chunk run for sharding a long stream: ``d_in`` is [batch][2][in_len]
+ * holding global samples [block_begin*step - M/2, ...) already extended
+ * cyclically by the caller (in_len >= (block_end-block_begin)*step + M);
+ * ``d_out`` is [batch][2][out_len] receiving global samples
+ * [block_begin*step, min(block_end*step, n_total)).                          */
+int dbp_run_chunk(dbp_plan* plan, const void* d_in, void* d_out, int64_t n_total, int batch,
+                  int64_t block_begin, int64_t block_end, int64_t in_len, int64_t out_len,
+                  void* stream);
+
+/* Host-buffer run: h_in/h_out are [batch][2][n_total] complex64 in host
+ * memory (pinned for full PCIe speed, pageable accepted).  Copies in,
+ * processes blocks [block_begin, block_end) and copies the kept samples
+ * out, pipelined over two streams; returns after completion (the
+ * reference's synchronous semantics).                                        */
+int dbp_run_host(dbp_plan* plan, const void* h_in, void* h_out, int64_t n_total, int batch,
+                 int64_t block_begin, int64_t block_end);
+
+/* Device staging budget (bytes) used by dbp_run_host (default 1 GiB).       */
+int dbp_plan_set_staging(dbp_plan* plan, size_t bytes);
+
+/* Unit seam: apply the configured per-block operator (the reference's
+ * ``process`` closure, dbp.py:212-233) to n_blocks full (2, N) blocks,
+ * [n_blocks][2][N] complex64 -> same shape, every sample kept.              */
+int dbp_process_blocks(dbp_plan* plan, const void* d_blocks, void* d_out, int64_t n_blocks,
+                       void* stream);
+
+/* Wait for all work the plan queued on its internal streams. */
+int dbp_plan_synchronize(dbp_plan* plan);
+
+/* Pinned host memory helpers (cudaHostAlloc / cudaFreeHost). */
+int dbp_host_alloc(void** ptr, size_t bytes);
+int dbp_host_free(void* ptr);
+
+/* Kernel launches issued by this process so far (evidence counter). */
+int64_t dbp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DBP_B200_H */

@@ -1,0 +1,46 @@
+"""B200-native drop-in for the digital-backpropagation hot path of arXiv 1507.00921.
+
+Mirrors the reference package's (``fiberdbp``) DBP API -- ``backpropagate``,
+``DbpConfig``, ``OverlapPlan`` and the signal / link value types -- and runs
+the overlap-save block engine with the SSFM / ESSFM / FFE operators as one
+fused sm_100a CUDA kernel behind the C ABI in ``include/dbp_b200.h``
+(``libdbp_b200.so``, loaded through ctypes).  There is no CPU fallback.
+"""
+
+from .params import (
+    DualPolSignal,
+    EssfmCoefficients,
+    FiberParams,
+    LinkConfig,
+    alpha_from_db_per_km,
+    dbm_to_watts,
+    effective_length,
+    scale_to_power,
+    signal_power,
+    watts_to_dbm,
+)
+from .framing import OverlapPlan, fft_frequencies, is_power_of_two, next_power_of_two, shard_blocks
+from .backprop import (
+    ALGORITHMS,
+    ARRANGEMENTS,
+    DbpConfig,
+    DbpEngine,
+    backpropagate,
+    backpropagate_batch,
+    channel_memory_samples,
+    estimate_channel_memory,
+    get_engine,
+    nonlinear_substep_essfm,
+    nonlinear_substep_ssfm,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "DualPolSignal", "EssfmCoefficients", "FiberParams", "LinkConfig", "alpha_from_db_per_km",
+    "dbm_to_watts", "effective_length", "scale_to_power", "signal_power", "watts_to_dbm",
+    "OverlapPlan", "fft_frequencies", "is_power_of_two", "next_power_of_two", "shard_blocks",
+    "ALGORITHMS", "ARRANGEMENTS", "DbpConfig", "DbpEngine", "backpropagate", "backpropagate_batch",
+    "channel_memory_samples", "estimate_channel_memory", "get_engine", "nonlinear_substep_essfm",
+    "nonlinear_substep_ssfm", "__version__",
+]

@@ -1,0 +1,207 @@
+"""ctypes binding of libdbp_b200.so (the C ABI in include/dbp_b200.h).
+
+There is no CPU fallback: if the shared library is missing or no CUDA
+device is visible, every entry point raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from pathlib import Path
+
+import numpy as np
+
+LIB_PATH = Path(__file__).resolve().parent / "libdbp_b200.so"
+
+DBP_OK, DBP_EINVAL, DBP_ECUDA, DBP_ENOMEM, DBP_ESTATE = 0, -1, -2, -3, -4
+ALG_CODES = {"ffe": 0, "ssfm": 1, "essfm": 2, "rotate": 3}
+ARR_CODES = {"symmetric": 0, "linear-first": 1, "nonlinear-first": 2}
+MIN_BLOCK_LEN, MAX_BLOCK_LEN, MAX_SIDE_COEFFS = 16, 8192, 64
+
+# every symbol include/dbp_b200.h declares, with (restype, argtypes)
+_c_int, _c_void_p, _c_int64, _c_double_p = ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)
+SIGNATURES = {
+    "dbp_last_error": (ctypes.c_char_p, []),
+    "dbp_version": (_c_int, []),
+    "dbp_device_count": (_c_int, [ctypes.POINTER(_c_int)]),
+    "dbp_plan_create": (_c_int, [ctypes.POINTER(_c_void_p), _c_int, _c_int, _c_int]),
+    "dbp_plan_destroy": (_c_int, [_c_void_p]),
+    "dbp_plan_set_linear": (_c_int, [_c_void_p, _c_double_p, _c_double_p]),
+    "dbp_plan_set_steps": (_c_int, [_c_void_p, _c_int, _c_int, _c_int, _c_double_p, _c_double_p,
+                                    ctypes.c_double, _c_double_p, _c_int]),
+    "dbp_num_blocks": (_c_int, [_c_void_p, _c_int64, ctypes.POINTER(_c_int64)]),
+    "dbp_run": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int, _c_int64, _c_int64, _c_void_p]),
+    "dbp_run_chunk": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int, _c_int64, _c_int64,
+                               _c_int64, _c_int64, _c_void_p]),
+    "dbp_run_host": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int, _c_int64, _c_int64]),
+    "dbp_plan_set_staging": (_c_int, [_c_void_p, ctypes.c_size_t]),
+    "dbp_process_blocks": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_void_p]),
+    "dbp_plan_synchronize": (_c_int, [_c_void_p]),
+    "dbp_host_alloc": (_c_int, [ctypes.POINTER(_c_void_p), ctypes.c_size_t]),
+    "dbp_host_free": (_c_int, [_c_void_p]),
+    "dbp_launch_count": (_c_int64, []),
+}
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load_library(path: str | os.PathLike | None = None):
+    """Load (once) and type the C ABI.  Raises RuntimeError when absent."""
+    global _lib
+    with _lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path is not None else LIB_PATH
+        if not p.exists():
+            raise RuntimeError(
+                f"{p} is missing: build the CUDA library first "
+                "(python -m paper_1507_00921_b200.build); there is no CPU fallback")
+        lib = ctypes.CDLL(str(p))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def _check(rc: int, what: str):
+    if rc == DBP_OK:
+        return
+    msg = load_library().dbp_last_error().decode(errors="replace")
+    if rc == DBP_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    raise RuntimeError(f"{what} failed ({rc}): {msg}")
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    _check(load_library().dbp_device_count(ctypes.byref(n)), "dbp_device_count")
+    return n.value
+
+
+def launch_count() -> int:
+    return int(load_library().dbp_launch_count())
+
+
+def _dptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+class NativePlan:
+    """Owner of one ``dbp_plan`` (device tables + staging) on one device."""
+
+    def __init__(self, device: int, block_len: int, overlap: int):
+        lib = load_library()
+        if device_count() == 0:
+            raise RuntimeError("no CUDA device visible: the B200 DBP path has no CPU fallback")
+        h = ctypes.c_void_p()
+        _check(lib.dbp_plan_create(ctypes.byref(h), int(device), int(block_len), int(overlap)),
+               "dbp_plan_create")
+        self._h = h
+        self._lib = lib
+        self.device = int(device)
+        self.block_len = int(block_len)
+        self.overlap = int(overlap)
+        self.lock = threading.Lock()
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.dbp_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def set_linear(self, kernel: np.ndarray, half_kernel: np.ndarray | None):
+        k = np.ascontiguousarray(np.asarray(kernel, dtype=np.complex128)).view(np.float64)
+        hk = None if half_kernel is None else np.ascontiguousarray(
+            np.asarray(half_kernel, dtype=np.complex128)).view(np.float64)
+        _check(self._lib.dbp_plan_set_linear(self._h, _dptr(k), None if hk is None else _dptr(hk)),
+               "dbp_plan_set_linear")
+
+    def set_steps(self, algorithm: str, arrangement: str, weights, gains, gamma: float, coeffs=None):
+        w = np.ascontiguousarray(np.asarray(weights, dtype=np.float64))
+        g = np.ascontiguousarray(np.asarray(gains, dtype=np.float64))
+        c = np.ascontiguousarray(np.asarray([1.0] if coeffs is None else coeffs, dtype=np.float64))
+        _check(self._lib.dbp_plan_set_steps(self._h, ALG_CODES[algorithm], ARR_CODES[arrangement],
+                                            int(w.size), _dptr(w), _dptr(g), float(gamma), _dptr(c),
+                                            int(c.size - 1)), "dbp_plan_set_steps")
+
+    def set_staging(self, nbytes: int):
+        _check(self._lib.dbp_plan_set_staging(self._h, int(nbytes)), "dbp_plan_set_staging")
+
+    def num_blocks(self, n_total: int) -> int:
+        out = ctypes.c_int64()
+        _check(self._lib.dbp_num_blocks(self._h, int(n_total), ctypes.byref(out)), "dbp_num_blocks")
+        return out.value
+
+    def run_host(self, h_in: np.ndarray, h_out: np.ndarray, n_total: int, batch: int,
+                 block_begin: int, block_end: int):
+        """h_in / h_out: C-contiguous complex64 arrays of shape (batch, 2, n_total)."""
+        for a in (h_in, h_out):
+            if a.dtype != np.complex64 or not a.flags.c_contiguous or a.size != batch * 2 * n_total:
+                raise ValueError("host buffers must be C-contiguous complex64 (batch, 2, n)")
+        _check(self._lib.dbp_run_host(self._h, h_in.ctypes.data, h_out.ctypes.data, int(n_total),
+                                      int(batch), int(block_begin), int(block_end)), "dbp_run_host")
+
+    def run_host_ptr(self, p_in: int, p_out: int, n_total: int, batch: int, block_begin: int,
+                     block_end: int):
+        _check(self._lib.dbp_run_host(self._h, p_in, p_out, int(n_total), int(batch),
+                                      int(block_begin), int(block_end)), "dbp_run_host")
+
+    def run_device(self, d_in: int, d_out: int, n_total: int, batch: int, block_begin: int,
+                   block_end: int, stream: int = 0):
+        _check(self._lib.dbp_run(self._h, d_in, d_out, int(n_total), int(batch), int(block_begin),
+                                 int(block_end), stream or None), "dbp_run")
+
+    def run_chunk(self, d_in: int, d_out: int, n_total: int, batch: int, block_begin: int,
+                  block_end: int, in_len: int, out_len: int, stream: int = 0):
+        _check(self._lib.dbp_run_chunk(self._h, d_in, d_out, int(n_total), int(batch),
+                                       int(block_begin), int(block_end), int(in_len), int(out_len),
+                                       stream or None), "dbp_run_chunk")
+
+    def process_blocks(self, d_in: int, d_out: int, n_blocks: int, stream: int = 0):
+        _check(self._lib.dbp_process_blocks(self._h, d_in, d_out, int(n_blocks), stream or None),
+               "dbp_process_blocks")
+
+    def synchronize(self):
+        _check(self._lib.dbp_plan_synchronize(self._h), "dbp_plan_synchronize")
+
+
+class PinnedBuffer:
+    """Page-locked host buffer viewed as a numpy array (cudaHostAlloc)."""
+
+    def __init__(self, shape, dtype=np.complex64):
+        lib = load_library()
+        dt = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dt.itemsize
+        p = ctypes.c_void_p()
+        _check(lib.dbp_host_alloc(ctypes.byref(p), max(nbytes, 1)), "dbp_host_alloc")
+        self._p = p
+        self._lib = lib
+        buf = (ctypes.c_byte * max(nbytes, 1)).from_address(p.value)
+        self.array = np.frombuffer(buf, dtype=dt, count=int(np.prod(shape))).reshape(shape)
+
+    def free(self):
+        if self._p is not None and self._p.value:
+            self.array = None
+            self._lib.dbp_host_free(self._p)
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

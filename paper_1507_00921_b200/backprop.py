@@ -1,0 +1,322 @@
+"""Drop-in ``backpropagate`` for the reference's DBP API, executed on B200.
+
+Same public names, argument meaning, validation errors and warnings as
+``fiberdbp.dbp`` (pkg/src/fiberdbp/dbp.py): ``ALGORITHMS``,
+``ARRANGEMENTS``, ``channel_memory_samples``, ``estimate_channel_memory``,
+``DbpConfig``, ``backpropagate(sig, cfg, jobs=1)``.  The host side keeps
+everything that is float64 scalar work in the reference -- validation, the
+short-overlap warning (dbp.py:175-181), the reverse step schedule
+(dbp.py:112-157) and the dispersion filters (dbp.py:186, 196-197) -- and
+hands the per-sample work to the fused CUDA kernel through the C ABI
+(include/dbp_b200.h).  Samples cross the boundary as complex64; the result
+is returned as the reference's complex128 ``DualPolSignal``.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+import warnings
+from collections import OrderedDict
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from . import _native
+from .framing import OverlapPlan, fft_frequencies, next_power_of_two, shard_blocks
+from .params import DualPolSignal, EssfmCoefficients, LinkConfig
+
+ALGORITHMS = ("ffe", "ssfm", "essfm")
+ARRANGEMENTS = ("symmetric", "linear-first", "nonlinear-first")
+
+
+def channel_memory_samples(beta2: float, length_km: float, bandwidth_hz: float) -> float:
+    """Dispersive memory 2 pi |beta2| L B^2 in samples (dbp.py:35-41)."""
+    if length_km <= 0.0:
+        raise ValueError("length must be positive")
+    if bandwidth_hz <= 0.0:
+        raise ValueError("bandwidth must be positive")
+    return 2.0 * math.pi * abs(beta2) * 1e-24 * length_km * bandwidth_hz ** 2
+
+
+def estimate_channel_memory(beta2: float, length_km: float, bandwidth_hz: float) -> int:
+    """Channel memory rounded up to a power of two (dbp.py:44-46)."""
+    return next_power_of_two(channel_memory_samples(beta2, length_km, bandwidth_hz))
+
+
+@dataclass(frozen=True)
+class DbpConfig:
+    """Block-wise channel-inverter configuration (dbp.py:78-109)."""
+
+    algorithm: str
+    plan: OverlapPlan
+    link: LinkConfig
+    num_steps: int = 1
+    coeffs: EssfmCoefficients | None = None
+    arrangement: str = "symmetric"
+
+    def __post_init__(self):
+        if self.algorithm not in ALGORITHMS:
+            raise ValueError(f"algorithm must be one of {ALGORITHMS}, got {self.algorithm!r}")
+        if self.arrangement not in ARRANGEMENTS:
+            raise ValueError(f"arrangement must be one of {ARRANGEMENTS}, got {self.arrangement!r}")
+        if self.num_steps < 1:
+            raise ValueError("num_steps must be >= 1")
+        if self.algorithm == "essfm":
+            if self.coeffs is None:
+                raise ValueError("essfm requires a coefficient set")
+            if self.plan.block_len <= 2 * self.coeffs.n_coeffs:
+                raise ValueError("block length too short for the coefficient memory")
+
+
+def _reverse_step_schedule(link, num_steps: int) -> list[tuple[float, float, float]]:
+    """(dz_km, weight_km, gain) per reverse step, last physical segment first.
+
+    Restates dbp.py:112-157 exactly (exact rational step boundaries in span
+    units; forward power profile 1 at amplifier outputs, exp(-alpha z)
+    inside a span; weight = profile integral over the segment / profile at
+    its far end; gain = sqrt(profile(a) / profile(b))).
+    """
+    alpha = link.span.alpha
+    span_len = link.span.length
+    n_spans = link.num_spans
+    dz = link.total_length / num_steps
+
+    def level(z: Fraction) -> float:
+        if z.denominator == 1:
+            return 1.0
+        local = float(z - math.floor(z)) * span_len
+        return math.exp(-alpha * local)
+
+    def area(a: Fraction, b: Fraction) -> float:
+        s, acc = math.floor(a), 0.0
+        while s < b:
+            t0 = float(max(a, Fraction(s)) - s) * span_len
+            t1 = float(min(b, Fraction(s + 1)) - s) * span_len
+            acc += (math.exp(-alpha * t0) - math.exp(-alpha * t1)) / alpha if alpha > 0.0 else t1 - t0
+            s += 1
+        return acc
+
+    out = []
+    for j in range(num_steps, 0, -1):
+        a = Fraction((j - 1) * n_spans, num_steps)
+        b = Fraction(j * n_spans, num_steps)
+        lb = level(b)
+        out.append((dz, area(a, b) / lb, math.sqrt(level(a) / lb)))
+    return out
+
+
+def _dispersion(freqs: np.ndarray, beta2: float, length: float) -> np.ndarray:
+    # same float64 expression as dbp.py:186 / 196-197
+    return np.exp(1j * 2.0 * np.pi ** 2 * (beta2 * 1e-24) * freqs ** 2 * length)
+
+
+class DbpEngine:
+    """One DBP configuration compiled onto one device (tables resident in HBM)."""
+
+    def __init__(self, cfg: DbpConfig, sample_rate: float, device: int = 0):
+        self.cfg = cfg
+        self.sample_rate = float(sample_rate)
+        self.device = int(device)
+        plan = cfg.plan
+        n = plan.block_len
+        if not (_native.MIN_BLOCK_LEN <= n <= _native.MAX_BLOCK_LEN):
+            raise ValueError(f"block_len {n} outside the GPU-supported range "
+                             f"[{_native.MIN_BLOCK_LEN}, {_native.MAX_BLOCK_LEN}]")
+        self.native = _native.NativePlan(self.device, n, plan.overlap)
+        link = cfg.link
+        freqs = fft_frequencies(n, self.sample_rate)
+        beta2 = link.span.beta2
+        if cfg.algorithm == "ffe":
+            self.native.set_linear(_dispersion(freqs, beta2, link.total_length), None)
+            self.native.set_steps("ffe", cfg.arrangement, [0.0], [1.0], 0.0)
+            self.schedule = []
+        else:
+            sched = _reverse_step_schedule(link, cfg.num_steps)
+            dz = sched[0][0]
+            self.native.set_linear(_dispersion(freqs, beta2, dz), _dispersion(freqs, beta2, 0.5 * dz))
+            if cfg.algorithm == "ssfm" and cfg.coeffs is None:
+                coeffs = None
+            else:
+                coeffs = cfg.coeffs.c if cfg.coeffs is not None else None
+            self.native.set_steps(cfg.algorithm, cfg.arrangement, [w for _, w, _ in sched],
+                                  [g for _, _, g in sched], -link.span.gamma,
+                                  None if cfg.algorithm == "ssfm" else coeffs)
+            self.schedule = sched
+
+    def num_blocks(self, n_total: int) -> int:
+        return self.cfg.plan.num_blocks(n_total)
+
+    def run_host(self, samples: np.ndarray, out: np.ndarray | None = None,
+                 block_range: tuple[int, int] | None = None) -> np.ndarray:
+        """(B, 2, n) complex -> (B, 2, n) complex64 through host buffers."""
+        x = np.ascontiguousarray(samples, dtype=np.complex64)
+        if x.ndim == 2:
+            x = x[None]
+        if x.ndim != 3 or x.shape[1] != 2:
+            raise ValueError("expected (batch, 2, n) or (2, n) samples")
+        b, _, n = x.shape
+        if out is None:
+            out = np.zeros_like(x)
+        b0, b1 = block_range if block_range is not None else (0, self.num_blocks(n))
+        with self.native.lock:
+            self.native.run_host(x, out, n, b, b0, b1)
+        return out
+
+    def close(self):
+        self.native.close()
+
+
+_ENGINES: "OrderedDict[tuple, DbpEngine]" = OrderedDict()
+_ENGINES_LOCK = threading.Lock()
+_MAX_ENGINES = 16
+
+
+def _cfg_key(cfg: DbpConfig, sample_rate: float, device: int) -> tuple:
+    sp = cfg.link.span
+    c = None if cfg.coeffs is None else cfg.coeffs.c.tobytes()
+    return (device, cfg.algorithm, cfg.plan.block_len, cfg.plan.overlap, cfg.num_steps,
+            cfg.arrangement, float(sample_rate), sp.beta2, sp.gamma, sp.alpha_db_per_km, sp.length,
+            cfg.link.num_spans, c)
+
+
+def get_engine(cfg: DbpConfig, sample_rate: float, device: int = 0) -> DbpEngine:
+    """Cached engine for (config, sample rate, device)."""
+    key = _cfg_key(cfg, sample_rate, device)
+    with _ENGINES_LOCK:
+        eng = _ENGINES.get(key)
+        if eng is not None:
+            _ENGINES.move_to_end(key)
+            return eng
+    eng = DbpEngine(cfg, sample_rate, device)
+    with _ENGINES_LOCK:
+        _ENGINES[key] = eng
+        while len(_ENGINES) > _MAX_ENGINES:
+            _, old = _ENGINES.popitem(last=False)
+            old.close()
+    return eng
+
+
+def _warn_short_overlap(cfg: DbpConfig, sample_rate: float, stacklevel: int):
+    span = cfg.link.span
+    memory = (channel_memory_samples(span.beta2, cfg.link.total_length, sample_rate)
+              if span.beta2 != 0.0 else 0.0)
+    if cfg.plan.overlap < memory:
+        warnings.warn(
+            f"overlap {cfg.plan.overlap} below estimated channel memory "
+            f"{memory:.0f} samples; block edges may leak interblock interference",
+            stacklevel=stacklevel + 1,
+        )
+
+
+def _resolve_devices(device, devices) -> list[int]:
+    if devices is not None:
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise ValueError("devices must not be empty")
+        return devs
+    return [0 if device is None else int(device)]
+
+
+def backpropagate_batch(samples: np.ndarray, sample_rate: float, cfg: DbpConfig, *,
+                        device: int | None = None, devices=None) -> np.ndarray:
+    """Batched DBP: (B, 2, n) complex waveforms -> (B, 2, n) complex64.
+
+    With several ``devices`` the work is split across them -- by whole
+    waveforms when B >= #devices, else by contiguous overlap-save block
+    ranges -- with no exchange; results are bitwise equal to one device.
+    """
+    x = np.ascontiguousarray(samples, dtype=np.complex64)
+    if x.ndim == 2:
+        x = x[None]
+    if x.ndim != 3 or x.shape[1] != 2 or x.shape[2] < 1:
+        raise ValueError("expected (batch, 2, n) samples with n >= 1")
+    _warn_short_overlap(cfg, sample_rate, stacklevel=2)
+    devs = _resolve_devices(device, devices)
+    out = np.zeros_like(x)
+    if len(devs) == 1:
+        return get_engine(cfg, sample_rate, devs[0]).run_host(x, out)
+    b, _, n = x.shape
+    engines = [get_engine(cfg, sample_rate, d) for d in devs]
+    jobs = []
+    if b >= len(devs):
+        for (i0, i1), eng in zip(shard_blocks(b, len(devs)), engines):
+            if i1 > i0:
+                jobs.append((eng, x[i0:i1], out[i0:i1], None))
+    else:
+        for (b0, b1), eng in zip(shard_blocks(cfg.plan.num_blocks(n), len(devs)), engines):
+            if b1 > b0:
+                jobs.append((eng, x, None, (b0, b1)))
+    results = []
+    with ThreadPoolExecutor(max_workers=len(jobs)) as pool:
+        futs = [pool.submit(lambda j: j[0].run_host(j[1], j[2], j[3]), j) for j in jobs]
+        results = [f.result() for f in futs]
+    for (eng, _, dst, rng), res in zip(jobs, results):
+        if rng is not None:
+            lo, hi = cfg.plan.output_span(rng[0], rng[1], n)
+            out[..., lo:hi] = res[..., lo:hi]
+    return out
+
+
+def backpropagate(sig: DualPolSignal, cfg: DbpConfig, jobs: int = 1, *,
+                  device: int | None = None, devices=None) -> DualPolSignal:
+    """Invert the configured link on a received waveform (dbp.py:160-235).
+
+    ``jobs`` is validated like the reference (spectral.py:119-120) and
+    otherwise ignored: the GPU result does not depend on it.  ``device`` /
+    ``devices`` select the GPU(s).
+    """
+    _warn_short_overlap(cfg, sig.sample_rate, stacklevel=2)
+    if jobs < 1:
+        raise ValueError("jobs must be >= 1")
+    x = np.empty((1, 2, len(sig)), dtype=np.complex64)
+    x[0, 0] = sig.x
+    x[0, 1] = sig.y
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        out = backpropagate_batch(x, sig.sample_rate, cfg, device=device, devices=devices)
+    return DualPolSignal(out[0, 0], out[0, 1], sig.sample_rate)
+
+
+# ---------------------------------------------------------------------------
+# sub-step mirrors (dbp.py:49-75, channel.py:61-71) on the GPU
+# ---------------------------------------------------------------------------
+
+_ROT_PLANS: dict = {}
+
+
+def _rotate_blocks(block: np.ndarray, gamma: float, dz_eff: float, c: np.ndarray,
+                   device: int = 0) -> np.ndarray:
+    blk = np.asarray(block)
+    if blk.ndim != 2 or blk.shape[0] != 2:
+        raise ValueError("expected a (2, n) dual-polarization block")
+    n = blk.shape[1]
+    if n <= 2 * (c.size - 1):
+        raise ValueError(f"block length {n} too short for {c.size - 1} side coefficients")
+    if not (_native.MIN_BLOCK_LEN <= n <= _native.MAX_BLOCK_LEN) or (n & (n - 1)):
+        raise ValueError(f"GPU sub-step needs a power-of-two block in "
+                         f"[{_native.MIN_BLOCK_LEN}, {_native.MAX_BLOCK_LEN}], got {n}")
+    key = (device, n)
+    plan = _ROT_PLANS.get(key)
+    if plan is None:
+        plan = _native.NativePlan(device, n, 0)
+        _ROT_PLANS[key] = plan
+    with plan.lock:
+        plan.set_steps("rotate", "symmetric", [dz_eff], [1.0], gamma, c)
+        x = np.ascontiguousarray(blk.astype(np.complex64))[None]
+        out = np.zeros_like(x)
+        plan.run_host(x, out, n, 1, 0, 1)
+    return out[0].astype(np.complex128)
+
+
+def nonlinear_substep_essfm(block, gamma: float, dz_eff: float, coeffs: EssfmCoefficients,
+                            *, device: int = 0) -> np.ndarray:
+    """GPU ESSFM rotation of one (2, n) block, cyclic FIR inside the block (dbp.py:49-75)."""
+    return _rotate_blocks(block, gamma, dz_eff, np.asarray(coeffs.c, dtype=np.float64), device)
+
+
+def nonlinear_substep_ssfm(block, gamma: float, dz_eff: float, *, device: int = 0) -> np.ndarray:
+    """GPU plain rotation exp(-j gamma dz_eff (|x|^2 + |y|^2)) (channel.py:61-71)."""
+    return _rotate_blocks(block, gamma, dz_eff, np.array([1.0]), device)

@@ -1,0 +1,585 @@
+// C ABI of libdbp_b200.so (declared in include/dbp_b200.h).
+//
+// The plan owns the device-resident tables of one DBP configuration
+// (dispersion filters, FFT twiddles, step program, ESSFM coefficients) and
+// the staging buffers of the host-buffer entry point.  Nothing here throws
+// across the ABI: failures return a negative code and leave a message in a
+// thread-local string (dbp_last_error).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/dbp_b200.h"
+#include "launch.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<long long> g_launches{0};
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(DBP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define DBP_CUDA(call, what)                      \
+  do {                                            \
+    cudaError_t e_ = (call);                      \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+int ilog2_exact(int n) {
+  if (n <= 0 || (n & (n - 1)) != 0) return -1;
+  int l = 0;
+  while ((1 << l) < n) ++l;
+  return l;
+}
+
+int fir_phys(int u) { return u + ((u >> 4) << 2); }
+
+// RAII device switch
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+using LaunchFn = cudaError_t (*)(const dbp::KernelParams&, long long, size_t, cudaStream_t);
+using ShapeFn = dbp::LaunchShape (*)();
+
+template <int L>
+void fill_tables(LaunchFn* lf, ShapeFn* sf) {
+  lf[L] = &dbp::launch_block_kernel<L>;
+  sf[L] = &dbp::launch_shape<L>;
+  if constexpr (L < dbp::kMaxLogN) fill_tables<L + 1>(lf, sf);
+}
+
+struct Dispatch {
+  LaunchFn launch[dbp::kMaxLogN + 1] = {};
+  ShapeFn shape[dbp::kMaxLogN + 1] = {};
+  Dispatch() { fill_tables<dbp::kMinLogN>(launch, shape); }
+};
+
+const Dispatch& dispatch() {
+  static Dispatch d;
+  return d;
+}
+
+}  // namespace
+
+struct dbp_plan {
+  int device = 0;
+  int N = 0, M = 0, logn = 0, step = 0, lead = 0;
+  float2* d_full = nullptr;
+  float2* d_half = nullptr;
+  float2* d_tw = nullptr;
+  float2* d_steps = nullptr;
+  int steps_cap = 0;
+  float* d_coeff = nullptr;
+  bool have_full = false, have_half = false, have_steps = false;
+  int program = dbp::kFFE, arrangement = dbp::kSymmetric, n_steps = 0, nc = 0;
+  float c[dbp::kMaxSideCoeffs + 4] = {};
+  // host-run staging
+  size_t staging_budget = size_t(1) << 30;
+  cudaStream_t streams[2] = {nullptr, nullptr};
+  void* d_stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][in/out]
+  size_t stage_bytes = 0;
+};
+
+namespace {
+
+// Twiddles W_{16 S_p}^{ns k} for every pass p < NP-1, layout [p][k-1][ns], float64 -> float32.
+std::vector<float2> make_twiddles(int logn) {
+  const int np = (logn + 3) / 4;
+  std::vector<float2> tw;
+  for (int p = 0; p < np - 1; ++p) {
+    const int ls = logn - 4 * (p + 1);
+    const long long S = 1LL << ls;
+    const long long period = 16 * S;
+    for (int k = 1; k < 16; ++k) {
+      for (long long ns = 0; ns < S; ++ns) {
+        const long long m = (ns * k) % period;
+        const double ang = -2.0 * M_PI * (double)m / (double)period;
+        tw.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
+      }
+    }
+  }
+  return tw;
+}
+
+int upload(float2** dst, const std::vector<float2>& src) {
+  if (*dst == nullptr) {
+    DBP_CUDA(cudaMalloc(dst, src.size() * sizeof(float2)), "cudaMalloc(table)");
+  }
+  DBP_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(float2), cudaMemcpyHostToDevice),
+           "cudaMemcpy(table)");
+  return DBP_OK;
+}
+
+int slice_floats(int N, int pw) {
+  int fir = fir_phys(N + 2 * pw) + 4 + fir_phys(N);
+  int v = 4 * N > fir ? 4 * N : fir;
+  return (v + 3) & ~3;
+}
+
+int check_ready(const dbp_plan* p) {
+  if (!p) return fail(DBP_EINVAL, "null plan");
+  if (!p->have_steps) return fail(DBP_ESTATE, "dbp_plan_set_steps has not been called");
+  if (p->program != dbp::kRotateOnly && !p->have_full)
+    return fail(DBP_ESTATE, "dbp_plan_set_linear has not been called");
+  if (p->program != dbp::kFFE && p->program != dbp::kRotateOnly &&
+      p->arrangement == dbp::kSymmetric && !p->have_half)
+    return fail(DBP_ESTATE, "symmetric arrangement needs the half-step kernel");
+  return DBP_OK;
+}
+
+// Fill the parameters shared by every launch mode.
+void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
+  std::memset(&kp, 0, sizeof(kp));
+  kp.program = p->program;
+  kp.arrangement = p->arrangement;
+  kp.n_steps = p->n_steps;
+  kp.nc = p->nc;
+  kp.fir_pad = (p->nc + 3) & ~3;
+  kp.slice_floats = slice_floats(p->N, kp.fir_pad);
+  kp.tab_full = p->d_full;
+  kp.tab_half = p->d_half ? p->d_half : p->d_full;
+  kp.twiddle = p->d_tw;
+  kp.steps = p->d_steps;
+  kp.coeff = p->d_coeff;
+  std::memcpy(kp.c, p->c, sizeof(kp.c));
+}
+
+int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
+  if (kp.total_blocks <= 0) return DBP_OK;
+  const Dispatch& d = dispatch();
+  const dbp::LaunchShape sh = d.shape[p->logn]();
+  const long long ctas = (kp.total_blocks + sh.slices - 1) / sh.slices;
+  if (ctas > 0x7fffffffLL) return fail(DBP_EINVAL, "too many blocks for one launch");
+  const size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices;
+  cudaError_t e = d.launch[p->logn](kp, ctas, smem, s);
+  if (e != cudaSuccess) return cuda_fail(e, "dbp_block_kernel launch");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return DBP_OK;
+}
+
+int check_range(const dbp_plan* p, int64_t n_total, int batch, int64_t b0, int64_t b1) {
+  if (n_total < 1) return fail(DBP_EINVAL, "signal must contain at least one sample");
+  if (batch < 0) return fail(DBP_EINVAL, "batch must be >= 0");
+  const int64_t nb = (n_total + p->step - 1) / p->step;
+  if (b0 < 0 || b1 < b0 || b1 > nb)
+    return fail(DBP_EINVAL, "block range outside [0, ceil(n_total / (N - M))]");
+  return DBP_OK;
+}
+
+int ensure_staging(dbp_plan* p, size_t bytes) {
+  if (p->stage_bytes >= bytes) return DBP_OK;
+  for (int s = 0; s < 2; ++s)
+    for (int k = 0; k < 2; ++k) {
+      if (p->d_stage[s][k]) cudaFree(p->d_stage[s][k]);
+      p->d_stage[s][k] = nullptr;
+    }
+  p->stage_bytes = 0;
+  for (int s = 0; s < 2; ++s)
+    for (int k = 0; k < 2; ++k) {
+      cudaError_t e = cudaMalloc(&p->d_stage[s][k], bytes);
+      if (e != cudaSuccess) return fail(DBP_ENOMEM, std::string("staging cudaMalloc: ") + cudaGetErrorString(e));
+    }
+  p->stage_bytes = bytes;
+  for (int s = 0; s < 2; ++s)
+    if (!p->streams[s]) DBP_CUDA(cudaStreamCreateWithFlags(&p->streams[s], cudaStreamNonBlocking), "cudaStreamCreate");
+  return DBP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dbp_last_error(void) { return g_last_error.c_str(); }
+
+int dbp_version(void) { return 100; }
+
+int64_t dbp_launch_count(void) { return g_launches.load(); }
+
+int dbp_device_count(int* count) {
+  if (!count) return fail(DBP_EINVAL, "null count");
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    *count = 0;
+    cudaGetLastError();
+    return DBP_OK;
+  }
+  *count = n;
+  return DBP_OK;
+}
+
+int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
+  if (!out) return fail(DBP_EINVAL, "null output pointer");
+  *out = nullptr;
+  const int logn = ilog2_exact(block_len);
+  if (logn < 0) return fail(DBP_EINVAL, "block_len must be a power of two, got " + std::to_string(block_len));
+  if (!(0 <= overlap && overlap < block_len)) return fail(DBP_EINVAL, "overlap must satisfy 0 <= overlap < block_len");
+  if (logn < dbp::kMinLogN || logn > dbp::kMaxLogN)
+    return fail(DBP_EINVAL, "block_len " + std::to_string(block_len) + " outside the GPU range [16, 8192]");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(DBP_ECUDA, "no CUDA device available");
+  }
+  if (device < 0 || device >= ndev) return fail(DBP_EINVAL, "device index out of range");
+  DeviceGuard g(device);
+  if (!g.ok) return fail(DBP_ECUDA, "cudaSetDevice failed");
+  dbp_plan* p = new (std::nothrow) dbp_plan();
+  if (!p) return fail(DBP_ENOMEM, "host allocation failed");
+  p->device = device;
+  p->N = block_len;
+  p->M = overlap;
+  p->logn = logn;
+  p->step = block_len - overlap;
+  p->lead = overlap / 2;
+  std::vector<float2> tw = make_twiddles(logn);
+  if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
+  int rc = upload(&p->d_tw, tw);
+  if (rc != DBP_OK) {
+    dbp_plan_destroy(p);
+    return rc;
+  }
+  *out = p;
+  return DBP_OK;
+}
+
+int dbp_plan_destroy(dbp_plan* p) {
+  if (!p) return DBP_OK;
+  DeviceGuard g(p->device);
+  for (int s = 0; s < 2; ++s) {
+    if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
+    for (int k = 0; k < 2; ++k)
+      if (p->d_stage[s][k]) cudaFree(p->d_stage[s][k]);
+    if (p->streams[s]) cudaStreamDestroy(p->streams[s]);
+  }
+  cudaFree(p->d_full);
+  cudaFree(p->d_half);
+  cudaFree(p->d_tw);
+  cudaFree(p->d_steps);
+  cudaFree(p->d_coeff);
+  delete p;
+  return DBP_OK;
+}
+
+int dbp_plan_set_staging(dbp_plan* p, size_t bytes) {
+  if (!p) return fail(DBP_EINVAL, "null plan");
+  if (bytes < (size_t(1) << 20)) return fail(DBP_EINVAL, "staging budget must be >= 1 MiB");
+  p->staging_budget = bytes;
+  return DBP_OK;
+}
+
+int dbp_plan_set_linear(dbp_plan* p, const double* kernel, const double* half_kernel) {
+  if (!p) return fail(DBP_EINVAL, "null plan");
+  if (!kernel) return fail(DBP_EINVAL, "null kernel");
+  DeviceGuard g(p->device);
+  const double inv_n = 1.0 / (double)p->N;
+  std::vector<float2> h(p->N);
+  for (int k = 0; k < p->N; ++k) {
+    const double re = kernel[2 * k], im = kernel[2 * k + 1];
+    if (!std::isfinite(re) || !std::isfinite(im)) return fail(DBP_EINVAL, "kernel must be finite");
+    h[k] = make_float2((float)(re * inv_n), (float)(im * inv_n));
+  }
+  int rc = upload(&p->d_full, h);
+  if (rc != DBP_OK) return rc;
+  p->have_full = true;
+  if (half_kernel) {
+    for (int k = 0; k < p->N; ++k) {
+      const double re = half_kernel[2 * k], im = half_kernel[2 * k + 1];
+      if (!std::isfinite(re) || !std::isfinite(im)) return fail(DBP_EINVAL, "half kernel must be finite");
+      h[k] = make_float2((float)(re * inv_n), (float)(im * inv_n));
+    }
+    rc = upload(&p->d_half, h);
+    if (rc != DBP_OK) return rc;
+    p->have_half = true;
+  } else {
+    p->have_half = false;
+  }
+  return DBP_OK;
+}
+
+int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_steps,
+                       const double* weights, const double* gains, double gamma,
+                       const double* coeffs, int n_coeffs) {
+  if (!p) return fail(DBP_EINVAL, "null plan");
+  if (algorithm < DBP_ALG_FFE || algorithm > DBP_ALG_ROTATE)
+    return fail(DBP_EINVAL, "unknown algorithm code " + std::to_string(algorithm));
+  if (arrangement < DBP_ARR_SYMMETRIC || arrangement > DBP_ARR_NONLINEAR_FIRST)
+    return fail(DBP_EINVAL, "unknown arrangement code " + std::to_string(arrangement));
+  DeviceGuard g(p->device);
+  p->program = algorithm;
+  p->arrangement = arrangement;
+  std::memset(p->c, 0, sizeof(p->c));
+  p->c[0] = 1.0f;
+  p->nc = 0;
+  if (algorithm == DBP_ALG_FFE) {
+    p->n_steps = 0;
+    p->have_steps = true;
+    return DBP_OK;
+  }
+  if (num_steps < 1) return fail(DBP_EINVAL, "num_steps must be >= 1");
+  if (!weights || !gains) return fail(DBP_EINVAL, "null weights or gains");
+  if (!std::isfinite(gamma)) return fail(DBP_EINVAL, "gamma must be finite");
+  if (algorithm == DBP_ALG_ESSFM || algorithm == DBP_ALG_ROTATE) {
+    if (!coeffs) return fail(DBP_EINVAL, "essfm requires a coefficient set");
+    if (n_coeffs < 0 || n_coeffs > DBP_MAX_SIDE_COEFFS)
+      return fail(DBP_EINVAL, "n_coeffs must be in [0, " + std::to_string(DBP_MAX_SIDE_COEFFS) + "]");
+    if (p->N <= 2 * n_coeffs) return fail(DBP_EINVAL, "block length too short for the coefficient memory");
+    int nc = n_coeffs;
+    for (int i = 0; i <= n_coeffs; ++i)
+      if (!std::isfinite(coeffs[i])) return fail(DBP_EINVAL, "coefficients must be finite");
+    // trailing zero side taps contribute fma(0, s, acc) == acc: drop them (bit-identical)
+    while (nc > 0 && (float)coeffs[nc] == 0.0f) --nc;
+    for (int i = 0; i <= nc; ++i) p->c[i] = (float)coeffs[i];
+    p->nc = nc;
+  }
+  std::vector<float2> st(num_steps);
+  for (int j = 0; j < num_steps; ++j) {
+    if (!std::isfinite(weights[j]) || !std::isfinite(gains[j])) return fail(DBP_EINVAL, "schedule must be finite");
+    // reference rotation exp(-j * gamma * w * F)  ==  exp(+j * a * F), a = -gamma * w
+    st[j] = make_float2((float)(-gamma * weights[j]), (float)gains[j]);
+  }
+  if (num_steps > p->steps_cap) {
+    cudaFree(p->d_steps);
+    p->d_steps = nullptr;
+    DBP_CUDA(cudaMalloc(&p->d_steps, num_steps * sizeof(float2)), "cudaMalloc(steps)");
+    p->steps_cap = num_steps;
+  }
+  DBP_CUDA(cudaMemcpy(p->d_steps, st.data(), num_steps * sizeof(float2), cudaMemcpyHostToDevice), "cudaMemcpy(steps)");
+  if (!p->d_coeff) DBP_CUDA(cudaMalloc(&p->d_coeff, sizeof(p->c)), "cudaMalloc(coeff)");
+  DBP_CUDA(cudaMemcpy(p->d_coeff, p->c, sizeof(p->c), cudaMemcpyHostToDevice), "cudaMemcpy(coeff)");
+  p->n_steps = num_steps;
+  p->have_steps = true;
+  return DBP_OK;
+}
+
+int dbp_num_blocks(const dbp_plan* p, int64_t n_total, int64_t* out) {
+  if (!p || !out) return fail(DBP_EINVAL, "null argument");
+  if (n_total < 0) return fail(DBP_EINVAL, "n_total must be >= 0");
+  *out = (n_total + p->step - 1) / p->step;
+  return DBP_OK;
+}
+
+int dbp_run(dbp_plan* p, const void* d_in, void* d_out, int64_t n_total, int batch,
+            int64_t block_begin, int64_t block_end, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  rc = check_range(p, n_total, batch, block_begin, block_end);
+  if (rc) return rc;
+  if (!d_in || !d_out) return fail(DBP_EINVAL, "null device buffer");
+  DeviceGuard g(p->device);
+  dbp::KernelParams kp;
+  base_params(p, kp);
+  kp.in = static_cast<const float2*>(d_in);
+  kp.out = static_cast<float2*>(d_out);
+  kp.n_total = n_total;
+  kp.in_pol_stride = n_total;
+  kp.in_item_stride = 2 * n_total;
+  kp.out_pol_stride = n_total;
+  kp.out_item_stride = 2 * n_total;
+  kp.in_origin = 0;
+  kp.out_origin = 0;
+  kp.block_begin = block_begin;
+  kp.blocks_per_item = block_end - block_begin;
+  kp.total_blocks = kp.blocks_per_item * batch;
+  kp.cyclic = 1;
+  kp.step = p->step;
+  kp.lead = p->lead;
+  return launch(p, kp, static_cast<cudaStream_t>(stream));
+}
+
+int dbp_run_chunk(dbp_plan* p, const void* d_in, void* d_out, int64_t n_total, int batch,
+                  int64_t block_begin, int64_t block_end, int64_t in_len, int64_t out_len,
+                  void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  rc = check_range(p, n_total, batch, block_begin, block_end);
+  if (rc) return rc;
+  if (!d_in || !d_out) return fail(DBP_EINVAL, "null device buffer");
+  const int64_t need_in = (block_end - block_begin) * p->step + p->M;
+  int64_t end = block_end * p->step;
+  if (end > n_total) end = n_total;
+  const int64_t need_out = end - block_begin * p->step;
+  if (in_len < need_in) return fail(DBP_EINVAL, "in_len shorter than (blocks * step + M)");
+  if (out_len < need_out) return fail(DBP_EINVAL, "out_len shorter than the kept samples");
+  DeviceGuard g(p->device);
+  dbp::KernelParams kp;
+  base_params(p, kp);
+  kp.in = static_cast<const float2*>(d_in);
+  kp.out = static_cast<float2*>(d_out);
+  kp.n_total = n_total;
+  kp.in_pol_stride = in_len;
+  kp.in_item_stride = 2 * in_len;
+  kp.out_pol_stride = out_len;
+  kp.out_item_stride = 2 * out_len;
+  kp.in_origin = block_begin * p->step - p->lead;
+  kp.out_origin = block_begin * p->step;
+  kp.block_begin = block_begin;
+  kp.blocks_per_item = block_end - block_begin;
+  kp.total_blocks = kp.blocks_per_item * batch;
+  kp.cyclic = 0;
+  kp.step = p->step;
+  kp.lead = p->lead;
+  return launch(p, kp, static_cast<cudaStream_t>(stream));
+}
+
+int dbp_process_blocks(dbp_plan* p, const void* d_blocks, void* d_out, int64_t n_blocks, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (n_blocks < 0) return fail(DBP_EINVAL, "n_blocks must be >= 0");
+  if (!d_blocks || !d_out) return fail(DBP_EINVAL, "null device buffer");
+  DeviceGuard g(p->device);
+  dbp::KernelParams kp;
+  base_params(p, kp);
+  kp.in = static_cast<const float2*>(d_blocks);
+  kp.out = static_cast<float2*>(d_out);
+  kp.n_total = p->N;
+  kp.in_pol_stride = p->N;
+  kp.in_item_stride = 2LL * p->N;
+  kp.out_pol_stride = p->N;
+  kp.out_item_stride = 2LL * p->N;
+  kp.block_begin = 0;
+  kp.blocks_per_item = 1;
+  kp.total_blocks = n_blocks;
+  kp.cyclic = 1;
+  kp.step = p->N;
+  kp.lead = 0;
+  return launch(p, kp, static_cast<cudaStream_t>(stream));
+}
+
+int dbp_plan_synchronize(dbp_plan* p) {
+  if (!p) return fail(DBP_EINVAL, "null plan");
+  DeviceGuard g(p->device);
+  for (int s = 0; s < 2; ++s)
+    if (p->streams[s]) DBP_CUDA(cudaStreamSynchronize(p->streams[s]), "cudaStreamSynchronize");
+  return DBP_OK;
+}
+
+int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, int batch,
+                 int64_t block_begin, int64_t block_end) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  rc = check_range(p, n_total, batch, block_begin, block_end);
+  if (rc) return rc;
+  if (!h_in || !h_out) return fail(DBP_EINVAL, "null host buffer");
+  if (batch == 0 || block_end == block_begin) return DBP_OK;
+  DeviceGuard g(p->device);
+  const size_t row = (size_t)n_total * sizeof(float2);    // one polarisation
+  const size_t item = 2 * row;
+  const size_t slot_budget = p->staging_budget / 4;       // per in/out buffer per slot
+  const int64_t nb = (n_total + p->step - 1) / p->step;
+  const bool full_range = block_begin == 0 && block_end == nb;
+  const int64_t out_lo = block_begin * p->step;
+  int64_t out_hi = block_end * p->step;
+  if (out_hi > n_total) out_hi = n_total;
+  const char* src = static_cast<const char*>(h_in);
+  char* dst = static_cast<char*>(h_out);
+
+  if (item <= slot_budget) {
+    // whole items per chunk, cyclic mode, two streams ping-pong
+    const int per = (int)std::min<size_t>((size_t)batch, slot_budget / item);
+    rc = ensure_staging(p, per * item);
+    if (rc) return rc;
+    int slot = 0;
+    for (int i0 = 0; i0 < batch; i0 += per, slot ^= 1) {
+      const int cnt = std::min(per, batch - i0);
+      cudaStream_t s = p->streams[slot];
+      void* din = p->d_stage[slot][0];
+      void* dout = p->d_stage[slot][1];
+      DBP_CUDA(cudaMemcpyAsync(din, src + (size_t)i0 * item, cnt * item, cudaMemcpyHostToDevice, s), "H2D");
+      rc = dbp_run(p, din, dout, n_total, cnt, block_begin, block_end, s);
+      if (rc) return rc;
+      if (full_range) {
+        DBP_CUDA(cudaMemcpyAsync(dst + (size_t)i0 * item, dout, cnt * item, cudaMemcpyDeviceToHost, s), "D2H");
+      } else {
+        for (int it = 0; it < cnt; ++it)
+          for (int pol = 0; pol < 2; ++pol) {
+            const size_t off = (size_t)it * item + pol * row + out_lo * sizeof(float2);
+            DBP_CUDA(cudaMemcpyAsync(dst + (size_t)i0 * item + off, static_cast<char*>(dout) + off,
+                                     (out_hi - out_lo) * sizeof(float2), cudaMemcpyDeviceToHost, s), "D2H");
+          }
+      }
+    }
+  } else {
+    // one item larger than a staging slot: block-range chunks with halos
+    const int64_t span_budget = (int64_t)(slot_budget / (2 * sizeof(float2)));
+    int64_t per_blocks = (span_budget - p->M) / p->step;
+    if (per_blocks < 1) return fail(DBP_EINVAL, "staging budget too small for one block");
+    rc = ensure_staging(p, slot_budget);
+    if (rc) return rc;
+    int slot = 0;
+    for (int it = 0; it < batch; ++it) {
+      for (int64_t b0 = block_begin; b0 < block_end; b0 += per_blocks, slot ^= 1) {
+        const int64_t b1 = std::min(block_end, b0 + per_blocks);
+        cudaStream_t s = p->streams[slot];
+        char* din = static_cast<char*>(p->d_stage[slot][0]);
+        char* dout = static_cast<char*>(p->d_stage[slot][1]);
+        const int64_t span = (b1 - b0) * p->step + p->M;
+        const int64_t g0 = b0 * p->step - p->lead;
+        if (span > n_total) return fail(DBP_EINVAL, "chunk span exceeds the signal length");
+        int64_t o1 = b1 * p->step;
+        if (o1 > n_total) o1 = n_total;
+        const int64_t olen = o1 - b0 * p->step;
+        for (int pol = 0; pol < 2; ++pol) {
+          const char* srow = src + (size_t)it * item + pol * row;
+          char* drow = din + (size_t)pol * span * sizeof(float2);
+          // pieces of [g0, g0 + span) modulo n_total (wraps at most once each side)
+          int64_t done = 0;
+          while (done < span) {
+            int64_t gi = (g0 + done) % n_total;
+            if (gi < 0) gi += n_total;
+            const int64_t len = std::min(span - done, n_total - gi);
+            DBP_CUDA(cudaMemcpyAsync(drow + done * sizeof(float2), srow + gi * sizeof(float2),
+                                     len * sizeof(float2), cudaMemcpyHostToDevice, s), "H2D");
+            done += len;
+          }
+        }
+        rc = dbp_run_chunk(p, din, dout, n_total, 1, b0, b1, span, olen, s);
+        if (rc) return rc;
+        for (int pol = 0; pol < 2; ++pol)
+          DBP_CUDA(cudaMemcpyAsync(dst + (size_t)it * item + pol * row + b0 * p->step * sizeof(float2),
+                                   dout + (size_t)pol * olen * sizeof(float2), olen * sizeof(float2),
+                                   cudaMemcpyDeviceToHost, s), "D2H");
+      }
+    }
+  }
+  for (int s = 0; s < 2; ++s) DBP_CUDA(cudaStreamSynchronize(p->streams[s]), "cudaStreamSynchronize");
+  return DBP_OK;
+}
+
+int dbp_host_alloc(void** ptr, size_t bytes) {
+  if (!ptr) return fail(DBP_EINVAL, "null pointer");
+  *ptr = nullptr;
+  cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) return fail(DBP_ENOMEM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+  return DBP_OK;
+}
+
+int dbp_host_free(void* ptr) {
+  if (!ptr) return DBP_OK;
+  DBP_CUDA(cudaFreeHost(ptr), "cudaFreeHost");
+  return DBP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,20 @@
+// Instantiation of the fused DBP block kernel for N = 2^9.
+#include "launch.h"
+
+namespace dbp {
+
+template <>
+cudaError_t launch_block_kernel<9>(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
+                                    cudaStream_t stream) {
+  using G = Geo<9>;
+  if (smem_bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(dbp_block_kernel<9>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+  }
+  dbp_block_kernel<9><<<dim3((unsigned)n_ctas), dim3(G::T, G::BPC), smem_bytes, stream>>>(kp);
+  return cudaGetLastError();
+}
+
+}  // namespace dbp

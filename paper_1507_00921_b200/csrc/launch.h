@@ -1,0 +1,27 @@
+// Per-block-length launchers of the fused kernel (one translation unit per
+// log2 N so the big unrolled kernels compile in parallel).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dbp_block_kernel.cuh"
+
+namespace dbp {
+
+constexpr int kMinLogN = 4;   // N = 16
+constexpr int kMaxLogN = 13;  // N = 8192
+
+struct LaunchShape {
+  int threads_x;  // T = N / 16
+  int slices;     // block slices per CTA
+};
+
+template <int LOGN>
+cudaError_t launch_block_kernel(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
+                                cudaStream_t stream);
+
+template <int LOGN>
+LaunchShape launch_shape() {
+  return LaunchShape{Geo<LOGN>::T, Geo<LOGN>::BPC};
+}
+
+}  // namespace dbp

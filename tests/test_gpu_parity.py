@@ -1,0 +1,262 @@
+"""GPU parity: the fused CUDA path (through the C ABI) against the reference.
+
+Tolerance (BASELINE north_star): relative L2 error <= 1e-5 per kept
+overlap-save block against the float64 reference / oracle; identical QPSK
+decisions; |dQ| <= 0.02 dB.  Bit-exact where the reference's own tests
+demand exactness (identity coefficients == plain SSFM, jobs invariance) and
+where the GPU design guarantees it (batching, block-range sharding).
+"""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1507_00921_b200 as pb
+from paper_1507_00921_b200 import _native
+from oracle import dbp_port, waveforms
+
+from .helpers import case_config, port_config, quiet_link, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+TOL_BLOCK = 1e-5   # per-block relative L2, north_star
+STD = pb.FiberParams(beta2=-21.0, gamma=1.3, alpha_db_per_km=0.2, length=40.0)
+
+
+def _run(x, case_or_cfg, rate=56e9, **kw):
+    cfg = case_or_cfg
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return pb.backpropagate_batch(x, rate, cfg, **kw)
+
+
+def _case_inputs(golden, case):
+    name = case["name"]
+    if case["signal"] == "white":
+        x = golden[f"bp_{name}_in"]
+        c = golden.get(f"bp_{name}_c")
+        want = golden[f"bp_{name}_out"]
+    else:
+        x = golden["link_rx"]
+        c = golden["link_c17"] if case["algorithm"] == "essfm" else None
+        want = golden[f"link_{name}_out"]
+    return x, c, want
+
+
+def test_library_sees_a_device():
+    assert _native.device_count() >= 1
+
+
+def test_golden_cases_match_reference_per_block(golden, manifest):
+    before = _native.launch_count()
+    worst = {}
+    for case in manifest["cases"]:
+        x, c, want = _case_inputs(golden, case)
+        cfg = case_config(case, c)
+        got = _run(x, cfg)[0]
+        errs = dbp_port.per_block_rel_l2(got, want, case["block_len"], case["overlap"])
+        worst[case["name"]] = float(errs.max())
+        assert errs.max() <= TOL_BLOCK, (case["name"], errs.max())
+        # and against the oracle port on the same inputs
+        port = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(cfg))
+        assert dbp_port.per_block_rel_l2(got, port, case["block_len"], case["overlap"]).max() <= TOL_BLOCK
+    assert _native.launch_count() > before  # the CUDA kernel ran
+    print("worst per-block rel-L2:", worst)
+
+
+@pytest.mark.parametrize("arrangement", pb.ARRANGEMENTS)
+@pytest.mark.parametrize("steps,spans,side", [(1, 1, 16), (3, 2, 5), (5, 3, 32), (2, 1, 0)])
+def test_identity_coefficients_bit_equal_plain(rng, arrangement, steps, spans, side):
+    # test_dbp.py:90-114 / test_acceptance.py:207-234: worst == 0.0
+    x = (rng.normal(size=(2, 1024)) + 1j * rng.normal(size=(2, 1024))).astype(np.complex64)
+    plan = pb.OverlapPlan(512, 128)
+    link = quiet_link(spans, STD)
+    plain = _run(x, pb.DbpConfig("ssfm", plan, link, num_steps=steps, arrangement=arrangement))
+    ident = _run(x, pb.DbpConfig("essfm", plan, link, num_steps=steps,
+                                 coeffs=pb.EssfmCoefficients.identity(side), arrangement=arrangement))
+    np.testing.assert_array_equal(plain, ident)
+
+
+def test_ffe_is_linear(rng):
+    # test_dbp.py:117-128
+    plan = pb.OverlapPlan(1024, 256)
+    cfg = pb.DbpConfig("ffe", plan, quiet_link(4, STD))
+    a = (rng.normal(size=(2, 4096)) + 1j * rng.normal(size=(2, 4096))).astype(np.complex64)
+    b = (rng.normal(size=(2, 4096)) + 1j * rng.normal(size=(2, 4096))).astype(np.complex64)
+    mix = (2.0 * a - 0.5j * b).astype(np.complex64)
+    oa, ob, om = _run(a, cfg)[0], _run(b, cfg)[0], _run(mix, cfg)[0]
+    err = np.max(np.abs(om - (2.0 * oa - 0.5j * ob)))
+    assert err < 1e-5 * np.max(np.abs(om))  # float32 arithmetic (reference: 1e-10 in float64)
+
+
+@pytest.mark.parametrize("nc", [0, 1, 2, 4])
+def test_substep_matches_reference(golden, nc):
+    # test_dbp.py:47-57 geometry (N = 16); float32 so rel 2e-6 instead of 1e-14
+    blk, c = golden[f"sub{nc}_in"], golden[f"sub{nc}_c"]
+    got = pb.nonlinear_substep_essfm(blk, 1.7, 0.25, pb.EssfmCoefficients(c))
+    want = golden[f"sub{nc}_out"]
+    np.testing.assert_allclose(got, want, rtol=0, atol=2e-6 * np.max(np.abs(want)))
+
+
+def test_substep_ssfm_equals_identity_essfm(rng):
+    blk = rng.normal(size=(2, 64)) + 1j * rng.normal(size=(2, 64))
+    a = pb.nonlinear_substep_essfm(blk, 1.3, 18.2, pb.EssfmCoefficients.identity(6))
+    b = pb.nonlinear_substep_ssfm(blk, 1.3, 18.2)
+    np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("nc", [1, 3, 9, 17, 24, 32, 33, 64])
+def test_fir_paths_match_oracle(rng, nc):
+    n = 256 if nc <= 64 else 512
+    blk = 0.03 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))
+    c = rng.normal(size=nc + 1) * 0.1
+    c[0] = 1.0
+    got = pb.nonlinear_substep_essfm(blk, -1.3, 800.0, pb.EssfmCoefficients(c))
+    want = dbp_port.rotate_essfm(blk.astype(np.complex64).astype(np.complex128), -1.3, 800.0, c)
+    assert rel_l2(got, want) < 2e-6
+
+
+def test_process_blocks_matches_captured_closure(golden, manifest):
+    torch = pytest.importorskip("torch")
+    for case in manifest["cases"]:
+        if case["signal"] != "link":
+            continue
+        name = case["name"]
+        c = golden["link_c17"] if case["algorithm"] == "essfm" else None
+        cfg = case_config(case, c)
+        eng = pb.get_engine(cfg, 56e9, 0)
+        blocks = np.ascontiguousarray(golden[f"link_{name}_blk_in"].astype(np.complex64))
+        d_in = torch.from_numpy(blocks.view(np.float32)).cuda()
+        d_out = torch.empty_like(d_in)
+        eng.native.process_blocks(d_in.data_ptr(), d_out.data_ptr(), blocks.shape[0])
+        torch.cuda.synchronize()
+        got = d_out.cpu().numpy().view(np.complex64)
+        want = golden[f"link_{name}_blk_out"]
+        for b in range(blocks.shape[0]):
+            assert rel_l2(got[b], want[b]) <= TOL_BLOCK, (name, b, rel_l2(got[b], want[b]))
+
+
+def test_batch_items_bit_equal_single(rng):
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(4, STD),
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    x = (0.03 * (rng.normal(size=(5, 2, 20000)) + 1j * rng.normal(size=(5, 2, 20000)))).astype(np.complex64)
+    batch = _run(x, cfg)
+    for i in range(5):
+        np.testing.assert_array_equal(batch[i], _run(x[i], cfg)[0])
+
+
+@pytest.mark.parametrize("parts", [2, 3, 8])
+def test_block_range_shards_bit_equal_whole(rng, parts):
+    # multi-GPU contract: chunks on multiples of N - M are bitwise equal
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, STD),
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    x = (0.03 * (rng.normal(size=(1, 2, 100000)) + 1j * rng.normal(size=(1, 2, 100000)))).astype(np.complex64)
+    whole = _run(x, cfg)
+    eng = pb.get_engine(cfg, 56e9, 0)
+    out = np.zeros_like(x)
+    for b0, b1 in pb.shard_blocks(eng.num_blocks(x.shape[-1]), parts):
+        part = eng.run_host(x, block_range=(b0, b1))
+        lo, hi = cfg.plan.output_span(b0, b1, x.shape[-1])
+        out[..., lo:hi] = part[..., lo:hi]
+    np.testing.assert_array_equal(out, whole)
+
+
+def test_chunk_mode_bit_equal_whole(rng):
+    torch = pytest.importorskip("torch")
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, STD),
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(9)), arrangement="linear-first")
+    n = 50000
+    x = (0.03 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))).astype(np.complex64)
+    whole = _run(x, cfg)[0]
+    eng = pb.get_engine(cfg, 56e9, 0)
+    nb = eng.num_blocks(n)
+    for b0, b1 in [(0, 5), (5, 17), (17, nb)]:
+        lo, hi = cfg.plan.input_span(b0, b1)
+        span = np.ascontiguousarray(pb.framing.gather_span(x, lo, hi))
+        olo, ohi = cfg.plan.output_span(b0, b1, n)
+        d_in = torch.from_numpy(span.view(np.float32)).cuda()
+        d_out = torch.zeros((2, (ohi - olo) * 2), dtype=torch.float32, device="cuda")
+        eng.native.run_chunk(d_in.data_ptr(), d_out.data_ptr(), n, 1, b0, b1, hi - lo, ohi - olo)
+        torch.cuda.synchronize()
+        got = d_out.cpu().numpy().view(np.complex64)
+        np.testing.assert_array_equal(got, whole[:, olo:ohi])
+
+
+def test_large_item_host_chunking_bit_equal(rng):
+    # item larger than a staging slot -> dbp_run_host's halo'd block-range path
+    cfg = pb.DbpConfig("ssfm", pb.OverlapPlan(1024, 256), quiet_link(8, STD), num_steps=3)
+    n = 300000
+    x = (0.03 * (rng.normal(size=(1, 2, n)) + 1j * rng.normal(size=(1, 2, n)))).astype(np.complex64)
+    whole = _run(x, cfg)
+    eng = pb.DbpEngine(cfg, 56e9, 0)
+    eng.native.set_staging(1 << 20)   # 256 KiB per slot buffer < 4.8 MB item
+    chunked = eng.run_host(x)
+    eng.close()
+    np.testing.assert_array_equal(chunked, whole)
+
+
+def test_jobs_bit_identical(rng):
+    x = (rng.normal(size=8192) + 1j * rng.normal(size=8192))
+    sig = pb.DualPolSignal(x, x[::-1], 56e9)
+    cfg = pb.DbpConfig("ssfm", pb.OverlapPlan(2048, 512), quiet_link(2, STD), num_steps=4)
+    a = pb.backpropagate(sig, cfg, jobs=1)
+    b = pb.backpropagate(sig, cfg, jobs=3)
+    np.testing.assert_array_equal(a.stack(), b.stack())
+    assert a.x.dtype == np.complex128 and len(a) == len(sig) and a.sample_rate == sig.sample_rate
+    with pytest.raises(ValueError):
+        pb.backpropagate(sig, cfg, jobs=0)
+
+
+def test_warns_on_short_overlap(rng):
+    # test_dbp.py:203-214
+    x = rng.normal(size=4096) + 0j
+    sig = pb.DualPolSignal(x, x, 56e9)
+    with pytest.warns(UserWarning, match="channel memory"):
+        pb.backpropagate(sig, pb.DbpConfig("ffe", pb.OverlapPlan(1024, 256), quiet_link(80, STD)))
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        pb.backpropagate(sig, pb.DbpConfig("ffe", pb.OverlapPlan(2048, 512), quiet_link(1, STD)))
+
+
+@pytest.mark.parametrize("n_total", [1, 5, 1536, 1537, 4096, 5000])
+def test_ffe_identity_filter_edge_lengths(rng, n_total):
+    # zero dispersion: the block engine must reproduce any input length (test_spectral.py:72-77)
+    span = pb.FiberParams(beta2=0.0, gamma=1.3, alpha_db_per_km=0.2, length=40.0)
+    cfg = pb.DbpConfig("ffe", pb.OverlapPlan(2048, 512), quiet_link(1, span))
+    x = (rng.normal(size=(2, n_total)) + 1j * rng.normal(size=(2, n_total))).astype(np.complex64)
+    got = _run(x, cfg)[0]
+    np.testing.assert_allclose(got, x, rtol=0, atol=2e-6 * np.max(np.abs(x)))
+
+
+def test_decisions_and_q_match_oracle(golden, manifest):
+    symbols = golden["link_tx_symbols"]
+    ref_bits = waveforms.hard_decisions(symbols)
+    for case in manifest["cases"]:
+        if case["signal"] != "link" or case["name"] not in ("c0_sym", "c0_lf", "c2_ssfm20"):
+            continue
+        x, c, want = _case_inputs(golden, case)
+        got = _run(x, case_config(case, c))[0]
+        bits_gpu = waveforms.hard_decisions(waveforms.receive_symbols(got))
+        bits_ref = waveforms.hard_decisions(waveforms.receive_symbols(want))
+        assert np.array_equal(bits_gpu, bits_ref), case["name"]
+        q_gpu = waveforms.q_factor_db(bits_gpu, ref_bits)
+        q_ref = waveforms.q_factor_db(bits_ref, ref_bits)
+        assert q_gpu == q_ref or abs(q_gpu - q_ref) <= 0.02
+
+
+def test_full_size_properties(rng):
+    # BASELINE config-3 item size (2^18 samples): linearity of FFE and ESSFM(identity) == SSFM
+    n = 1 << 18
+    x = (0.03 * (rng.normal(size=(2, 2, n)) + 1j * rng.normal(size=(2, 2, n)))).astype(np.complex64)
+    link = quiet_link(40, pb.FiberParams(-21.6826, 1.3, 0.2, 80.0))
+    plan = pb.OverlapPlan(2048, 700)
+    ffe = pb.DbpConfig("ffe", plan, link)
+    a, b = _run(x, ffe)
+    s = _run((x[0] + x[1])[None].astype(np.complex64), ffe)[0]
+    assert rel_l2(s, a + b) < 1e-5
+    plain = _run(x, pb.DbpConfig("ssfm", plan, link, num_steps=1))
+    ident = _run(x, pb.DbpConfig("essfm", plan, link, coeffs=pb.EssfmCoefficients.identity(17)))
+    np.testing.assert_array_equal(plain, ident)
+    # energy: the inverse-dispersion filter is unitary up to framing
+    assert abs(np.sum(np.abs(a) ** 2) / np.sum(np.abs(x[0]) ** 2) - 1.0) < 0.05
