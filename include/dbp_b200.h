@@ -133,6 +133,12 @@ int dbp_host_free(void* ptr);
 /* Kernel launches issued by this process so far (evidence counter). */
 int64_t dbp_launch_count(void);
 
+/* Measurement utility (not on the DBP path): FP32 FFMA throughput of
+ * ``device`` in TFLOP/s from an 8-accumulator FFMA kernel over all SMs,
+ * ``iters`` x 16 x 8 FMAs per thread; ``ms`` receives the kernel time.
+ * bench.py uses it as the FP32 roofline denominator.                        */
+int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

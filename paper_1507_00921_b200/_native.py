@@ -42,6 +42,8 @@ SIGNATURES = {
     "dbp_host_alloc": (_c_int, [ctypes.POINTER(_c_void_p), ctypes.c_size_t]),
     "dbp_host_free": (_c_int, [_c_void_p]),
     "dbp_launch_count": (_c_int64, []),
+    "dbp_probe_fp32_peak": (_c_int, [_c_int, _c_int, ctypes.POINTER(ctypes.c_double),
+                                     ctypes.POINTER(ctypes.c_double)]),
 }
 
 _lib = None
@@ -86,6 +88,14 @@ def device_count() -> int:
 
 def launch_count() -> int:
     return int(load_library().dbp_launch_count())
+
+
+def probe_fp32_peak(device: int = 0, iters: int = 4096) -> tuple[float, float]:
+    """(TFLOP/s, ms) of the FFMA throughput probe on ``device``."""
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    _check(load_library().dbp_probe_fp32_peak(int(device), int(iters), ctypes.byref(tf), ctypes.byref(ms)),
+           "dbp_probe_fp32_peak")
+    return tf.value, ms.value
 
 
 def _dptr(a: np.ndarray):

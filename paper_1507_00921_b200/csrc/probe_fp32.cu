@@ -1,0 +1,58 @@
+// FP32 FMA throughput probe (measurement utility, not on the DBP path).
+//
+// The roofline denominator for the FP32-bound DBP kernel: MEASURED_PEAKS.json
+// records only HBM copy and bf16 GEMM peaks, so bench.py measures the FP32
+// pipe on the same box and clocks with a dependent-chain-free FFMA kernel
+// (8 independent accumulators per thread, immediate-free 3-register form,
+// 148 x 8 CTAs of 256 threads), timed with CUDA events.
+#include <cuda_runtime.h>
+
+#include <string>
+
+#include "../../include/dbp_b200.h"
+
+namespace {
+
+__global__ void __launch_bounds__(256) fma_probe_kernel(float* sink, int iters, float a, float b) {
+  float r0 = threadIdx.x * 1e-7f, r1 = r0 + 1e-7f, r2 = r0 + 2e-7f, r3 = r0 + 3e-7f;
+  float r4 = r0 + 4e-7f, r5 = r0 + 5e-7f, r6 = r0 + 6e-7f, r7 = r0 + 7e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      r0 = fmaf(r0, a, b); r1 = fmaf(r1, a, b); r2 = fmaf(r2, a, b); r3 = fmaf(r3, a, b);
+      r4 = fmaf(r4, a, b); r5 = fmaf(r5, a, b); r6 = fmaf(r6, a, b); r7 = fmaf(r7, a, b);
+    }
+  }
+  const float s = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  if (s == 1234.5f) sink[threadIdx.x] = s;  // keep the chain alive
+}
+
+}  // namespace
+
+extern "C" int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms) {
+  if (!tflops || iters < 1) return DBP_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return DBP_ECUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float* sink = nullptr;
+  if (cudaMalloc(&sink, 256 * sizeof(float)) != cudaSuccess) return DBP_ENOMEM;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int blocks = sms * 8;
+  fma_probe_kernel<<<blocks, 256>>>(sink, iters / 8 + 1, 0.9999f, 1e-7f);  // warm-up
+  cudaEventRecord(e0);
+  fma_probe_kernel<<<blocks, 256>>>(sink, iters, 0.9999f, 1e-7f);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaEventSynchronize(e1);
+  float t = 0.f;
+  cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (err != cudaSuccess) return DBP_ECUDA;
+  const double flops = 2.0 * 8.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
+  *tflops = flops / (t * 1e-3) / 1e12;
+  if (ms) *ms = t;
+  return DBP_OK;
+}
