@@ -13,7 +13,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libdbp_b200.so"
+LIB_PATH = Path(os.environ.get("DBP_LIB") or Path(__file__).resolve().parent / "libdbp_b200.so")
 
 DBP_OK, DBP_EINVAL, DBP_ECUDA, DBP_ENOMEM, DBP_ESTATE = 0, -1, -2, -3, -4
 ALG_CODES = {"ffe": 0, "ssfm": 1, "essfm": 2, "rotate": 3}

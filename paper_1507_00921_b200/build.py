@@ -50,14 +50,18 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra_flags=None) -> Path:
-    BUILD.mkdir(parents=True, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, extra_flags=None, lib: Path | None = None,
+          obj_dir: Path | None = None) -> Path:
+    """Compile and link; ``lib`` / ``obj_dir`` redirect a variant build (A/B experiments)."""
+    obj_root = Path(obj_dir) if obj_dir else BUILD
+    lib_path = Path(lib) if lib else LIB
+    obj_root.mkdir(parents=True, exist_ok=True)
     extra = list(extra_flags or [])
     env_flags = os.environ.get("DBP_NVCC_FLAGS", "").split()
     headers = _headers()
     jobs = []
     for src in _sources():
-        obj = BUILD / (src.stem + ".o")
+        obj = obj_root / (src.stem + ".o")
         if force or _stale(obj, [src, *headers, Path(__file__)]):
             cmd = [nvcc(), *ARCH, *FLAGS, *extra, *env_flags, "-I", str(CSRC), "-I", str(INCLUDE),
                    "-c", str(src), "-o", str(obj)]
@@ -75,13 +79,13 @@ def build(force: bool = False, verbose: bool = False, extra_flags=None) -> Path:
     if jobs:
         with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as pool:
             list(pool.map(run, jobs))
-    objs = [BUILD / (s.stem + ".o") for s in _sources()]
-    if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs)]
+    objs = [obj_root / (s.stem + ".o") for s in _sources()]
+    if force or jobs or _stale(lib_path, objs):
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(lib_path), *map(str, objs)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    return LIB
+    return lib_path
 
 
 def main(argv=None):

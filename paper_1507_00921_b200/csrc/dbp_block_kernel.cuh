@@ -71,7 +71,10 @@ struct Geo {
   static constexpr int T = N / 16;                      // threads per block slice
   static constexpr int NP = (LOGN + 3) / 4;             // FFT passes
   static constexpr int RLAST = 1 << (LOGN - 4 * (NP - 1));
-  static constexpr int BPC = T >= 128 ? 1 : 128 / T;    // block slices per CTA
+#ifndef DBP_CTA_THREADS
+#define DBP_CTA_THREADS 128
+#endif
+  static constexpr int BPC = T >= DBP_CTA_THREADS ? 1 : DBP_CTA_THREADS / T;  // block slices per CTA
   static constexpr int THREADS = T * BPC;
 #ifndef DBP_THREADS_PER_SM
 #define DBP_THREADS_PER_SM 384
@@ -217,47 +220,54 @@ __device__ __forceinline__ void conv_pass(float2 (&x)[16], float2 (&y)[16], floa
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int fir_phys(int u) { return u + ((u >> 4) << 2); }  // pad 4 per 16
 
-// F for 16 consecutive outputs from a register window w[0 .. 16 + 2 PW)
+// F for 8 consecutive outputs p0 .. p0+7 (p0 = 16 t + 8 q) from a register
+// window of the padded intensity buffer; results go straight to fbuf.
+// Only 8 outputs per call keeps the unrolled code small (instruction-cache
+// footprint) at the price of re-reading 2 PW window floats per chunk.
 template <int NC>
-__device__ __forceinline__ void fir16_fixed(const float* __restrict__ ibuf, int t,
-                                            const KernelParams& kp, float (&f)[16]) {
+__device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float* __restrict__ fbuf,
+                                           int p0, const KernelParams& kp) {
   constexpr int PW = (NC + 3) & ~3;
-  constexpr int W = 16 + 2 * PW;
+  constexpr int W = 8 + 2 * PW;
   float w[W];
 #pragma unroll
   for (int m = 0; m < W / 4; ++m) {
-    const float4 v = *reinterpret_cast<const float4*>(ibuf + fir_phys(16 * t + 4 * m));
+    const float4 v = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
     w[4 * m] = v.x; w[4 * m + 1] = v.y; w[4 * m + 2] = v.z; w[4 * m + 3] = v.w;
   }
+  float f[8];
 #pragma unroll
-  for (int o = 0; o < 16; ++o) {
+  for (int o = 0; o < 8; ++o) {
     float acc = kp.c[0] * w[o + PW];
 #pragma unroll
     for (int i = 1; i <= NC; ++i) acc = fmaf(kp.c[i], w[o + PW - i] + w[o + PW + i], acc);
     f[o] = acc;
   }
+  *reinterpret_cast<float4*>(fbuf + fir_phys(p0)) = make_float4(f[0], f[1], f[2], f[3]);
+  *reinterpret_cast<float4*>(fbuf + fir_phys(p0 + 4)) = make_float4(f[4], f[5], f[6], f[7]);
 }
 
-// any nc: taps in chunks of four, windows re-read per chunk
-__device__ __forceinline__ void fir16_generic(const float* __restrict__ ibuf, int t, int pw,
-                                              const KernelParams& kp, float (&f)[16]) {
+// any nc: taps in chunks of four, windows re-read per chunk (same summation
+// order as fir8_fixed, so every path gives identical bits for a given c)
+__device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float* __restrict__ fbuf,
+                                             int p0, int pw, const KernelParams& kp) {
+  float f[8];
   {
-    const int u0 = 16 * t + pw;
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const float4 v = *reinterpret_cast<const float4*>(ibuf + fir_phys(u0 + 4 * m));
-      f[4 * m] = kp.c[0] * v.x; f[4 * m + 1] = kp.c[0] * v.y;
-      f[4 * m + 2] = kp.c[0] * v.z; f[4 * m + 3] = kp.c[0] * v.w;
-    }
+    const float4 a = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw));
+    const float4 b = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw + 4));
+    const float c0 = kp.c[0];
+    f[0] = c0 * a.x; f[1] = c0 * a.y; f[2] = c0 * a.z; f[3] = c0 * a.w;
+    f[4] = c0 * b.x; f[5] = c0 * b.y; f[6] = c0 * b.z; f[7] = c0 * b.w;
   }
+#pragma unroll 1
   for (int i0 = 1; i0 <= kp.nc; i0 += 4) {
-    // left: positions 16t - i0 - 3 .. 16t + 15 - i0  ->  window u from 16t + pw - i0 - 3
-    // right: positions 16t + i0 .. 16t + 18 + i0      ->  window u from 16t + pw + i0 - 1
-    float l[20], r[20];
-    const int ul = 16 * t + pw - i0 - 3;
-    const int ur = 16 * t + pw + i0 - 1;
+    // left: positions p0 - i0 - 3 .. p0 + 7 - i0  ->  window u from p0 + pw - i0 - 3
+    // right: positions p0 + i0 .. p0 + 10 + i0     ->  window u from p0 + pw + i0 - 1
+    float l[12], r[12];
+    const int ul = p0 + pw - i0 - 3;
+    const int ur = p0 + pw + i0 - 1;
 #pragma unroll
-    for (int m = 0; m < 5; ++m) {
+    for (int m = 0; m < 3; ++m) {
       const float4 a = *reinterpret_cast<const float4*>(ibuf + fir_phys(ul + 4 * m));
       const float4 b = *reinterpret_cast<const float4*>(ibuf + fir_phys(ur + 4 * m));
       l[4 * m] = a.x; l[4 * m + 1] = a.y; l[4 * m + 2] = a.z; l[4 * m + 3] = a.w;
@@ -266,12 +276,13 @@ __device__ __forceinline__ void fir16_generic(const float* __restrict__ ibuf, in
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       const float ci = __ldg(kp.coeff + i0 + d);
-      // tap i = i0 + d: left value at position p - i  ->  l[o + 3 - d]
-      //                 right value at position p + i ->  r[o + 1 + d]
+      // tap i = i0 + d: left value at position p - i -> l[o + 3 - d]; right p + i -> r[o + 1 + d]
 #pragma unroll
-      for (int o = 0; o < 16; ++o) f[o] = fmaf(ci, l[o + 3 - d] + r[o + 1 + d], f[o]);
+      for (int o = 0; o < 8; ++o) f[o] = fmaf(ci, l[o + 3 - d] + r[o + 1 + d], f[o]);
     }
   }
+  *reinterpret_cast<float4*>(fbuf + fir_phys(p0)) = make_float4(f[0], f[1], f[2], f[3]);
+  *reinterpret_cast<float4*>(fbuf + fir_phys(p0 + 4)) = make_float4(f[4], f[5], f[6], f[7]);
 }
 
 template <int LOGN>
@@ -301,19 +312,18 @@ __device__ __forceinline__ void rotate(float2 (&x)[16], float2 (&y)[16], float* 
       if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[n];
     }
     __syncthreads();
-    float acc[16];
-    switch (kp.nc) {
-      case 1: fir16_fixed<1>(ibuf, t, kp, acc); break;
-      case 9: fir16_fixed<9>(ibuf, t, kp, acc); break;
-      case 17: fir16_fixed<17>(ibuf, t, kp, acc); break;
-      case 32: fir16_fixed<32>(ibuf, t, kp, acc); break;
-      case 33: fir16_fixed<33>(ibuf, t, kp, acc); break;
-      default: fir16_generic(ibuf, t, pw, kp, acc); break;
+#pragma unroll 1
+    for (int q = 0; q < 2; ++q) {
+      const int p0 = 16 * t + 8 * q;
+      switch (kp.nc) {
+        case 1: fir8_fixed<1>(ibuf, fbuf, p0, kp); break;
+        case 9: fir8_fixed<9>(ibuf, fbuf, p0, kp); break;
+        case 17: fir8_fixed<17>(ibuf, fbuf, p0, kp); break;
+        case 32: fir8_fixed<32>(ibuf, fbuf, p0, kp); break;
+        case 33: fir8_fixed<33>(ibuf, fbuf, p0, kp); break;
+        default: fir8_generic(ibuf, fbuf, p0, pw, kp); break;
+      }
     }
-#pragma unroll
-    for (int m = 0; m < 4; ++m)
-      *reinterpret_cast<float4*>(fbuf + fir_phys(16 * t + 4 * m)) =
-          make_float4(acc[4 * m], acc[4 * m + 1], acc[4 * m + 2], acc[4 * m + 3]);
     __syncthreads();
 #pragma unroll
     for (int n = 0; n < 16; ++n) f[n] = fbuf[fir_phys(n * T + t)];
@@ -342,7 +352,7 @@ template <int LOGN>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
 dbp_block_kernel(const KernelParams kp) {
   using G = Geo<LOGN>;
-  constexpr int T = G::T;
+  constexpr int N = G::N, T = G::T;
   extern __shared__ float4 smem_raw[];
   const int t = threadIdx.x;
   float* smf = reinterpret_cast<float*>(smem_raw) + threadIdx.y * kp.slice_floats;
@@ -361,19 +371,26 @@ dbp_block_kernel(const KernelParams kp) {
   if (active) {
     const float2* px = kp.in + item * kp.in_item_stride;
     const float2* py = px + kp.in_pol_stride;
+    if (!kp.cyclic || (s0 >= 0 && s0 + N <= kp.n_total)) {
+      // interior block (or pre-extended chunk): one contiguous window, immediate offsets
+      const long long base = (kp.cyclic ? s0 : s0 - kp.in_origin) + t;
 #pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      long long gi = s0 + n * T + t;
-      if (kp.cyclic) {
+      for (int n = 0; n < 16; ++n) {
+        x[n] = ld_stream(px + base + n * T);
+        y[n] = ld_stream(py + base + n * T);
+      }
+    } else {
+      // edge block: circular extension of the whole signal (spectral.py:128)
+#pragma unroll
+      for (int n = 0; n < 16; ++n) {
+        long long gi = s0 + n * T + t;
         if (gi < 0 || gi >= kp.n_total) {
           gi %= kp.n_total;
           if (gi < 0) gi += kp.n_total;
         }
-      } else {
-        gi -= kp.in_origin;
+        x[n] = ld_stream(px + gi);
+        y[n] = ld_stream(py + gi);
       }
-      x[n] = ld_stream(px + gi);
-      y[n] = ld_stream(py + gi);
     }
   } else {
 #pragma unroll
@@ -416,16 +433,16 @@ dbp_block_kernel(const KernelParams kp) {
   if (active) {
     float2* ox = kp.out + item * kp.out_item_stride;
     float2* oy = ox + kp.out_pol_stride;
-    const long long keep_end = (long long)kp.lead + kp.step;
+    const long long ob = b * kp.step - kp.lead - kp.out_origin;  // output index of block sample 0
+    const bool whole = (b + 1) * kp.step <= kp.n_total;
 #pragma unroll
     for (int n = 0; n < 16; ++n) {
       const int j = n * T + t;
-      if (j >= kp.lead && j < keep_end) {
-        const long long go = b * kp.step + (j - kp.lead);
-        if (go < kp.n_total) {
-          st_stream(ox + (go - kp.out_origin), x[n]);
-          st_stream(oy + (go - kp.out_origin), y[n]);
-        }
+      const bool keep = j >= kp.lead && j < kp.lead + kp.step &&
+                        (whole || b * kp.step + (j - kp.lead) < kp.n_total);
+      if (keep) {
+        st_stream(ox + ob + j, x[n]);
+        st_stream(oy + ob + j, y[n]);
       }
     }
   }

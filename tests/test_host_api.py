@@ -1,0 +1,98 @@
+"""Host-side mirror of the reference API: validation, warnings, schedule, tables (no GPU)."""
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1507_00921_b200 as pb
+from paper_1507_00921_b200 import backprop
+from oracle import dbp_port
+
+STD = pb.FiberParams(beta2=-21.0, gamma=1.3, alpha_db_per_km=0.2, length=40.0)
+
+
+def quiet(n, span=STD):
+    return pb.LinkConfig(span=span, num_spans=n, amp_noise_figure_db=None, pol_rotation=False)
+
+
+def test_dbp_config_validation():                       # test_dbp.py:75-87
+    plan = pb.OverlapPlan(256, 64)
+    link = quiet(2)
+    for kw in (dict(algorithm="trellis"), dict(algorithm="ssfm", num_steps=0),
+               dict(algorithm="ssfm", arrangement="diagonal"), dict(algorithm="essfm"),
+               dict(algorithm="essfm", coeffs=pb.EssfmCoefficients.identity(128))):
+        alg = kw.pop("algorithm")
+        with pytest.raises(ValueError):
+            pb.DbpConfig(alg, plan, link, **kw)
+
+
+def test_value_type_validation():                       # test_sigkit.py / test_spectral.py
+    with pytest.raises(ValueError):
+        pb.DualPolSignal(np.zeros(3), np.zeros(4), 1e9)
+    with pytest.raises(ValueError):
+        pb.DualPolSignal(np.zeros(0), np.zeros(0), 1e9)
+    with pytest.raises(ValueError):
+        pb.DualPolSignal(np.zeros(3), np.zeros(3), 0.0)
+    with pytest.raises(ValueError):
+        pb.FiberParams(-21.0, 1.3, -0.1, 40.0)
+    with pytest.raises(ValueError):
+        pb.LinkConfig(STD, 0)
+    with pytest.raises(ValueError):
+        pb.EssfmCoefficients([])
+    with pytest.raises(ValueError):
+        pb.EssfmCoefficients([1.0, np.nan])
+    with pytest.raises(ValueError):
+        pb.OverlapPlan(1000, 100)
+    with pytest.raises(ValueError):
+        pb.OverlapPlan(1024, 1024)
+    assert pb.OverlapPlan(2048, 512).usable == 1536
+    s = pb.DualPolSignal([1, 2], [3, 4], 1e9)
+    assert s.x.dtype == np.complex128 and len(s) == 2
+
+
+def test_channel_memory_and_fft_grid():
+    assert pb.channel_memory_samples(21.0, 3000.0, 50e9) == pytest.approx(989.6016858807848)
+    assert pb.estimate_channel_memory(21.0, 3200.0, 56e9) == 2048
+    np.testing.assert_allclose(pb.fft_frequencies(8, 8e9), np.array([0, 1, 2, 3, -4, -3, -2, -1]) * 1e9)
+    with pytest.raises(ValueError):
+        pb.fft_frequencies(12, 8e9)
+
+
+def test_schedule_matches_reference_fixture(golden, manifest):
+    for i in range(manifest["sched_cases"]):
+        beta2, gamma, adb, span, ns, steps = golden[f"sched{i}_args"]
+        link = quiet(int(ns), pb.FiberParams(beta2, gamma, adb, span))
+        np.testing.assert_array_equal(np.array(backprop._reverse_step_schedule(link, int(steps))),
+                                      golden[f"sched{i}"])
+
+
+def test_short_overlap_warning_text():                  # dbp.py:175-181
+    cfg = pb.DbpConfig("ffe", pb.OverlapPlan(1024, 256), quiet(80))
+    with pytest.warns(UserWarning, match="channel memory"):
+        backprop._warn_short_overlap(cfg, 56e9, stacklevel=1)
+    cfg = pb.DbpConfig("ffe", pb.OverlapPlan(2048, 512), quiet(1))
+    with warnings.catch_warnings():
+        warnings.simplefilter("error")
+        backprop._warn_short_overlap(cfg, 56e9, stacklevel=1)
+
+
+def test_dispersion_tables_match_oracle():
+    f = pb.fft_frequencies(2048, 56e9)
+    np.testing.assert_array_equal(backprop._dispersion(f, -21.68, 3200.0),
+                                  dbp_port.dispersion_response(2048, 56e9, -21.68, 3200.0))
+
+
+def test_jobs_validated_before_gpu():
+    sig = pb.DualPolSignal(np.ones(8), np.ones(8), 56e9)
+    cfg = pb.DbpConfig("ffe", pb.OverlapPlan(16, 4), quiet(1))
+    with pytest.raises(ValueError):
+        pb.backpropagate(sig, cfg, jobs=0)
+
+
+def test_effective_length():
+    assert pb.effective_length(0.0461, 80.0) == pytest.approx(21.149197483217407)
+    assert pb.effective_length(0.0, 5.0) == 5.0
+    assert pb.effective_length(1e-12, 1.0) == pytest.approx(1.0)
+    assert pb.scale_to_power(pb.DualPolSignal([1, 1], [1, 1], 1.0), 0.0).x[0] == pytest.approx(math.sqrt(1e-3 / 2))

@@ -1,0 +1,18 @@
+"""Build A/B variants of libdbp_b200.so into build/variants/<name>.so (tuning experiments)."""
+import sys
+from pathlib import Path
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+from paper_1507_00921_b200 import build as B
+
+ROOT = Path(__file__).resolve().parent.parent / "build" / "variants"
+VARIANTS = {
+    "base": [],
+    "tps512": ["-DDBP_THREADS_PER_SM=512"],
+    "bpc3": ["-DDBP_CTA_THREADS=384"],
+    "bpc4": ["-DDBP_CTA_THREADS=512", "-DDBP_THREADS_PER_SM=512"],
+}
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    for name in names:
+        lib = B.build(extra_flags=VARIANTS[name], lib=ROOT / f"{name}.so", obj_dir=ROOT / f"obj_{name}")
+        print(name, lib)
