@@ -1,11 +1,13 @@
-// Fused overlap-save DBP block kernel for sm_100a.
+// Fused overlap-save DBP block kernel for sm_100a (v2: one polarisation per thread).
 //
-// One overlap-save block of N dual-polarisation samples per thread slice
-// (T = N/16 threads, 16 samples of BOTH polarisations per thread).  The
-// whole multi-step program -- dispersion filter (FFT -> x H -> IFFT), the
-// SSFM/ESSFM nonlinear rotation with the in-block cyclic intensity FIR,
-// gains -- runs on-chip between ONE coalesced load of the block (with its
-// halo, cyclic wrap of the whole signal) and ONE store of its centre.
+// One overlap-save block of N dual-polarisation samples per block slice of
+// 2T threads, T = N/16: lanes 0-15 of a warp carry polarisation x and lanes
+// 16-31 polarisation y of the same 16 sample positions, 16 samples per
+// thread (positions t + T m, m = 0..15).  The whole multi-step program --
+// dispersion filter (FFT -> x table -> IFFT), the SSFM / ESSFM nonlinear
+// rotation with the in-block cyclic intensity FIR, gains -- runs on-chip
+// between ONE coalesced load of the block (with its halo, cyclic wrap of the
+// whole signal) and ONE store of its centre.
 //
 // Reference behaviour reproduced (pkg/src/fiberdbp/...):
 //   framing  spectral.py:122-145  block b = samples [b*step - M/2, +N) mod n,
@@ -15,334 +17,371 @@
 //   rotate   dbp.py:49-75, channel.py:61-71
 //            b * exp(-j g w (c0 I_k + sum_i c_i (I_{k-i} + I_{k+i}))), cyclic in-block
 //
-// FFT: mixed radix, passes of radix 16 (last pass 2..16).  Forward passes
-// are decimation-in-frequency, so the spectrum ends digit-reversed across
-// threads; the dispersion table is read at each register's natural bin
-// index, and the inverse transform is the exact adjoint walk back, so no
-// reordering pass exists.  Between passes data moves through shared memory
-// as float4 {x.re, x.im, y.re, y.im} with an XOR swizzle that makes every
-// exchange bank-conflict free.
+// FFT: N = R0 * 16^(NP-1), passes radix R0 (2..16, G0 = 16/R0 groups per
+// thread) then radix 16.  Forward passes are decimation-in-frequency, so the
+// spectrum ends digit-reversed across threads; the dispersion table is read
+// at each register's natural bin index and the inverse is the exact adjoint
+// walk back (no reorder pass).  Every exchange writes register m to plane
+// position t + T m; reads gather a pass's 16 inputs.  Only the exchange into
+// the last pass (stride 1 reads) needs an XOR swizzle to stay conflict free
+// for 8-byte accesses (16 lanes per shared-memory phase).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cmath>
+#include <vector>
+
+#include "dbp_common.cuh"
 #include "dft_small.cuh"
 
 namespace dbp {
 
-constexpr int kMaxSideCoeffs = 64;
-
-enum Program : int { kFFE = 0, kSSFM = 1, kESSFM = 2, kRotateOnly = 3 };
-enum Arrangement : int { kSymmetric = 0, kLinearFirst = 1, kNonlinearFirst = 2 };
-
-struct KernelParams {
-  const float2* in;
-  float2* out;
-  long long n_total;          // samples per polarisation of the whole signal
-  long long in_pol_stride;    // float2 elements between the x and y rows
-  long long in_item_stride;   // float2 elements between batch items
-  long long out_pol_stride;
-  long long out_item_stride;
-  long long in_origin;        // global sample index of in[0]  (chunk mode)
-  long long out_origin;       // global sample index of out[0]
-  long long block_begin;      // first overlap-save block processed per item
-  long long blocks_per_item;  // blocks processed per item in this launch
-  long long total_blocks;     // blocks_per_item * items
-  int cyclic;                 // 1: global index taken modulo n_total
-  int step;                   // N - M
-  int lead;                   // M / 2
-  int program;                // Program
-  int arrangement;            // Arrangement
-  int n_steps;                // nonlinear steps
-  int nc;                     // side coefficients of the intensity FIR
-  int fir_pad;                // nc rounded up to a multiple of 4
-  int slice_floats;           // shared floats per block slice
-  const float2* tab_full;     // K (or H for FFE), natural bin order, 1/N folded in
-  const float2* tab_half;     // K^(1/2) (symmetric arrangement)
-  const float2* twiddle;      // per-pass twiddle tables
-  const float2* steps;        // per step (a_j, g_j): rotation exp(+j a_j F), gain g_j
-  const float* coeff;         // c_0..c_nc zero padded to nc + 4 (generic FIR path)
-  float c[kMaxSideCoeffs + 4];  // c_0..c_nc, zero padded
-};
+#ifndef DBP_THREADS_PER_SM
+#define DBP_THREADS_PER_SM 768
+#endif
+#ifndef DBP_CTA_POSITIONS
+#define DBP_CTA_POSITIONS 128
+#endif
 
 template <int LOGN>
 struct Geo {
   static constexpr int N = 1 << LOGN;
-  static constexpr int T = N / 16;                      // threads per block slice
-  static constexpr int NP = (LOGN + 3) / 4;             // FFT passes
-  static constexpr int RLAST = 1 << (LOGN - 4 * (NP - 1));
-#ifndef DBP_CTA_THREADS
-#define DBP_CTA_THREADS 128
-#endif
-  static constexpr int BPC = T >= DBP_CTA_THREADS ? 1 : DBP_CTA_THREADS / T;  // block slices per CTA
-  static constexpr int THREADS = T * BPC;
-#ifndef DBP_THREADS_PER_SM
-#define DBP_THREADS_PER_SM 384
-#endif
-  // resident-thread target per SM sets the register budget (65536 / target)
+  static constexpr int T = N / 16;                       // position-threads per block
+  static constexpr int NP = (LOGN + 3) / 4;              // FFT passes
+  static constexpr int LOGR0 = LOGN - 4 * (NP - 1);
+  static constexpr int R0 = 1 << LOGR0;                  // first-pass radix
+  static constexpr int G0 = 16 / R0;                     // first-pass groups per thread
+  static constexpr int BPC = T >= DBP_CTA_POSITIONS ? 1 : DBP_CTA_POSITIONS / T;
+  static constexpr int THREADS = 2 * T * BPC;
   static constexpr int MIN_CTAS = DBP_THREADS_PER_SM / THREADS > 0 ? DBP_THREADS_PER_SM / THREADS : 1;
-  __host__ __device__ static constexpr int radix(int p) { return p < NP - 1 ? 16 : RLAST; }
-  __host__ __device__ static constexpr int log_s(int p) { return p < NP - 1 ? LOGN - 4 * (p + 1) : 0; }
+  // log2 of the pass stride S_p = N / (L_p r_p)
+  __host__ __device__ static constexpr int log_s(int p) { return LOGN - LOGR0 - 4 * p; }
+  // offset of pass p's twiddle table: pass 0 holds (R0-1) N/R0 entries, pass q >= 1 15 S_q
   __host__ __device__ static constexpr int tw_offset(int p) {
     int off = 0;
-    for (int q = 0; q < p; ++q) off += 15 << log_s(q);
+    for (int q = 0; q < p; ++q) off += q == 0 ? (R0 - 1) * (N / R0) : 15 * (1 << log_s(q));
     return off;
   }
-  static constexpr int TW_ENTRIES = tw_offset(NP - 1);
 };
 
-// Swizzle of the exchange between pass P and P+1 (see header comment).
-template <int LOGN, int P>
-__device__ __forceinline__ int swz(int i) {
-  using G = Geo<LOGN>;
-  constexpr int ls = G::log_s(P), ls1 = G::log_s(P + 1);
-  if constexpr (ls1 >= 3) {
-    return i;
-  } else {
-    return i ^ (((i >> ls) << ls1) & 7);
+// Twiddle tables, float64 -> float32: pass 0 W_N^{g k} [k-1][g] (g < N/R0,
+// k < R0); pass p >= 1 W_{16 S_p}^{ns k} [k-1][ns] (ns < S_p, k < 16).
+inline std::vector<float2> make_twiddles(int logn) {
+  const int np = (logn + 3) / 4;
+  const int logr0 = logn - 4 * (np - 1);
+  const long long n = 1LL << logn, r0 = 1LL << logr0;
+  std::vector<float2> tw;
+  auto push = [&](long long m, long long period) {
+    const double ang = -2.0 * M_PI * (double)(m % period) / (double)period;
+    tw.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
+  };
+  if (np > 1) {
+    for (long long k = 1; k < r0; ++k)
+      for (long long g = 0; g < n / r0; ++g) push(g * k, n);
+    for (int p = 1; p < np - 1; ++p) {
+      const long long s = n >> (logr0 + 4 * p);
+      for (long long k = 1; k < 16; ++k)
+        for (long long ns = 0; ns < s; ++ns) push(ns * k, 16 * s);
+    }
   }
+  if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
+  return tw;
 }
 
-__device__ __forceinline__ float2 ld_stream(const float2* p) {
-  float2 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
-               : "=f"(v.x), "=f"(v.y) : "l"(p));
-  return v;
+__host__ __device__ inline int fir_phys(int u) { return u + ((u >> 4) << 2); }  // pad 4 per 16 floats
+__host__ __device__ inline int cs_phys(int j) { return j + ((j >> 4) << 1); }   // pad 2 per 16 float2
+
+// shared floats per block slice: max(exchange planes, FIR intensity + (cos, sin) buffers)
+inline int plane_elems(int n) { return n + n / 16; }  // padded exchange plane (float2)
+
+inline int slice_floats(int n, int pw) {
+  const int fir = fir_phys(n + 2 * pw) + 4 + 2 * (cs_phys(n) + 2);
+  const int planes = 4 * plane_elems(n);
+  const int v = planes > fir ? planes : fir;
+  return (v + 3) & ~3;
 }
 
-__device__ __forceinline__ void st_stream(float2* p, float2 v) {
-  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+// Final-boundary layout: one pad element per 16 (reads of the last pass
+// gather 16 consecutive elements per lane, i.e. a 128-byte lane stride,
+// which the pad turns into 136 bytes -> 16 distinct banks).  Linear in the
+// lane's base, so every access is base + immediate.
+__host__ __device__ constexpr int pad16(int i) { return i + (i >> 4); }
+
+template <int LOGN, int P>
+__device__ __forceinline__ int xchg_index(int i) {
+  if constexpr (P + 1 == Geo<LOGN>::NP - 1) return pad16(i);
+  else return i;
 }
 
 // ---------------------------------------------------------------------------
-// FFT -> x table -> IFFT, recursive over passes (forward on the way down,
-// adjoint on the way back up).  On entry and exit thread t holds samples
-// n*T + t (n = 0..15) of its block in x[n], y[n].
+// FFT -> x table -> IFFT on one polarisation, recursive over passes.
+// On entry and exit v[m] holds block position t + T m.
 // ---------------------------------------------------------------------------
 template <int LOGN, int P>
-__device__ __forceinline__ void conv_pass(float2 (&x)[16], float2 (&y)[16], float4* sm,
+__device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ plane,
                                           const float2* __restrict__ tab,
                                           const float2* __restrict__ tw, int t) {
   using G = Geo<LOGN>;
-  constexpr int N = G::N, T = G::T;
-  if constexpr (P < G::NP - 1) {
-    // forward radix-16 over one group (g = t), then twiddle W_{16 S}^{ns k}
-    constexpr int LS = G::log_s(P);
-    constexpr int S = 1 << LS;
-    dft<16, false>(x);
-    dft<16, false>(y);
-    const int ns = t & (S - 1);
-    const float2* twp = tw + G::tw_offset(P) + ns;
+  constexpr int N = G::N, T = G::T, NP = G::NP;
+  if constexpr (NP == 1) {
+    // N == 16: a single radix-16 pass, bins k = e
+    dft<16, false>(v);
 #pragma unroll
-    for (int k = 1; k < 16; ++k) {
-      const float2 wk = __ldg(twp + (k - 1) * S);
-      x[k] = c_mul(x[k], wk);
-      y[k] = c_mul(y[k], wk);
+    for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(tab + e));
+    dft<16, true>(v);
+  } else if constexpr (P == 0) {
+    // radix R0 over G0 groups: group q = registers q + G0 e, g = t + T q
+    constexpr int R0 = G::R0, G0 = G::G0, S0 = N / R0;
+#pragma unroll
+    for (int q = 0; q < G0; ++q) {
+      float2 u[R0];
+#pragma unroll
+      for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
+      dft<R0, false>(u);
+#pragma unroll
+      for (int k = 1; k < R0; ++k) u[k] = c_mul(u[k], ldg_table(tw + (k - 1) * S0 + t + T * q));
+#pragma unroll
+      for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
-    // exchange into pass P+1 layout
-    constexpr int R1 = G::radix(P + 1);
-    constexpr int LS1 = G::log_s(P + 1);
-    constexpr int GRP = 16 / R1;
+    // exchange into the pass-1 layout
+    constexpr int LS1 = G::log_s(1);
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      sm[swz<LOGN, P>(t + k * (N / 16))] = make_float4(x[k].x, x[k].y, y[k].x, y[k].y);
+    for (int m = 0; m < 16; ++m) plane[xchg_index<LOGN, 0>(t + T * m)] = v[m];
     __syncthreads();
+    {
+      const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
-    for (int q = 0; q < GRP; ++q) {
-      const int g = t + T * q;
-      const int base = ((g >> LS1) << LS) + (g & ((1 << LS1) - 1));
-#pragma unroll
-      for (int e = 0; e < R1; ++e) {
-        const float4 v = sm[swz<LOGN, P>(base + (e << LS1))];
-        x[q * R1 + e] = make_float2(v.x, v.y);
-        y[q * R1 + e] = make_float2(v.z, v.w);
-      }
+      for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
     }
 
-    conv_pass<LOGN, P + 1>(x, y, sm, tab, tw, t);
+    conv_pass<LOGN, 1>(v, plane, tab, tw, t);
+    t = opaque(t);
 
-    // adjoint exchange back into pass P layout
     __syncthreads();
+    {
+      const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
-    for (int q = 0; q < GRP; ++q) {
-      const int g = t + T * q;
-      const int base = ((g >> LS1) << LS) + (g & ((1 << LS1) - 1));
-#pragma unroll
-      for (int e = 0; e < R1; ++e)
-        sm[swz<LOGN, P>(base + (e << LS1))] =
-            make_float4(x[q * R1 + e].x, x[q * R1 + e].y, y[q * R1 + e].x, y[q * R1 + e].y);
+      for (int e = 0; e < 16; ++e) plane[xchg_index<LOGN, 0>(base + (e << LS1))] = v[e];
     }
     __syncthreads();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const float4 v = sm[swz<LOGN, P>(t + k * (N / 16))];
-      x[k] = make_float2(v.x, v.y);
-      y[k] = make_float2(v.z, v.w);
-    }
+    for (int m = 0; m < 16; ++m) v[m] = plane[xchg_index<LOGN, 0>(t + T * m)];
 #pragma unroll
-    for (int k = 1; k < 16; ++k) {
-      const float2 wk = __ldg(twp + (k - 1) * S);  // reloaded: keeps registers free below
-      x[k] = c_mulc(x[k], wk);
-      y[k] = c_mulc(y[k], wk);
+    for (int q = 0; q < G0; ++q) {
+      float2 u[R0];
+#pragma unroll
+      for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
+#pragma unroll
+      for (int k = 1; k < R0; ++k) u[k] = c_mulc(u[k], ldg_table(tw + (k - 1) * S0 + t + T * q));
+      dft<R0, true>(u);
+#pragma unroll
+      for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
-    dft<16, true>(x);
-    dft<16, true>(y);
+  } else if constexpr (P < NP - 1) {
+    // middle radix-16 pass: group g = t, ns = t mod S_P
+    constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
+    const float2* twp = tw + G::tw_offset(P) + (t & (S - 1));
+    dft<16, false>(v);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) v[k] = c_mul(v[k], ldg_table(twp + (k - 1) * S));
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) plane[xchg_index<LOGN, P>(t + T * m)] = v[m];
+    __syncthreads();
+    {
+      const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
+    }
+
+    conv_pass<LOGN, P + 1>(v, plane, tab, tw, t);
+    t = opaque(t);
+    twp = tw + G::tw_offset(P) + (t & (S - 1));
+
+    __syncthreads();
+    {
+      const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
+#pragma unroll
+      for (int e = 0; e < 16; ++e) plane[xchg_index<LOGN, P>(base + (e << LS1))] = v[e];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = plane[xchg_index<LOGN, P>(t + T * m)];
+#pragma unroll
+    for (int k = 1; k < 16; ++k) v[k] = c_mulc(v[k], ldg_table(twp + (k - 1) * S));
+    dft<16, true>(v);
   } else {
-    // last pass: S = 1, GRP groups of radix RL per thread, group g = t + T q
-    constexpr int RL = G::RLAST;
-    constexpr int GRP = 16 / RL;
-    constexpr int LL = N / RL;  // bin index k = g + LL * e
+    // last pass: S = 1, group g = t, bin k = t + T e
+    dft<16, false>(v);
 #pragma unroll
-    for (int q = 0; q < GRP; ++q) {
-      dft<RL, false>(x + q * RL);
-      dft<RL, false>(y + q * RL);
-    }
-#pragma unroll
-    for (int q = 0; q < GRP; ++q) {
-#pragma unroll
-      for (int e = 0; e < RL; ++e) {
-        const float2 h = __ldg(tab + (t + T * q) + LL * e);
-        x[q * RL + e] = c_mul(x[q * RL + e], h);
-        y[q * RL + e] = c_mul(y[q * RL + e], h);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < GRP; ++q) {
-      dft<RL, true>(x + q * RL);
-      dft<RL, true>(y + q * RL);
-    }
+    for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(tab + t + T * e));
+    dft<16, true>(v);
   }
 }
 
 // ---------------------------------------------------------------------------
 // Nonlinear rotation with the in-block cyclic intensity FIR.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ int fir_phys(int u) { return u + ((u >> 4) << 2); }  // pad 4 per 16
 
-// F for 8 consecutive outputs p0 .. p0+7 (p0 = 16 t + 8 q) from a register
-// window of the padded intensity buffer; results go straight to fbuf.
-// Only 8 outputs per call keeps the unrolled code small (instruction-cache
-// footprint) at the price of re-reading 2 PW window floats per chunk.
+// (cos, sin) * g of theta = a * F with explicit 2 pi range reduction
+__device__ __forceinline__ float2 rot_factor(float a, float g, float f) {
+  const float th = a * f;
+  const float k = rintf(th * 0.159154943091895336f);
+  float r = fmaf(k, -6.28318548202514648f, th);
+  r = fmaf(k, 1.74845553e-7f, r);
+  float s, c;
+  __sincosf(r, &s, &c);
+  return make_float2(c * g, s * g);
+}
+
+// 8 consecutive FIR outputs p0 .. p0+7 from a register window of the padded
+// intensity buffer, turned into rotation factors and stored to csbuf.
 template <int NC>
-__device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float* __restrict__ fbuf,
-                                           int p0, const KernelParams& kp) {
+__device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
+                                           int p0, float a, float g, const KernelParams& kp) {
   constexpr int PW = (NC + 3) & ~3;
   constexpr int W = 8 + 2 * PW;
   float w[W];
 #pragma unroll
   for (int m = 0; m < W / 4; ++m) {
-    const float4 v = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
-    w[4 * m] = v.x; w[4 * m + 1] = v.y; w[4 * m + 2] = v.z; w[4 * m + 3] = v.w;
+    const float4 q = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
+    w[4 * m] = q.x; w[4 * m + 1] = q.y; w[4 * m + 2] = q.z; w[4 * m + 3] = q.w;
   }
-  float f[8];
+  float2 cs[8];
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
     float acc = kp.c[0] * w[o + PW];
 #pragma unroll
     for (int i = 1; i <= NC; ++i) acc = fmaf(kp.c[i], w[o + PW - i] + w[o + PW + i], acc);
-    f[o] = acc;
+    cs[o] = rot_factor(a, g, acc);
   }
-  *reinterpret_cast<float4*>(fbuf + fir_phys(p0)) = make_float4(f[0], f[1], f[2], f[3]);
-  *reinterpret_cast<float4*>(fbuf + fir_phys(p0 + 4)) = make_float4(f[4], f[5], f[6], f[7]);
+#pragma unroll
+  for (int o = 0; o < 8; o += 2)
+    *reinterpret_cast<float4*>(csbuf + cs_phys(p0 + o)) = make_float4(cs[o].x, cs[o].y, cs[o + 1].x, cs[o + 1].y);
 }
 
-// any nc: taps in chunks of four, windows re-read per chunk (same summation
-// order as fir8_fixed, so every path gives identical bits for a given c)
-__device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float* __restrict__ fbuf,
-                                             int p0, int pw, const KernelParams& kp) {
+// any nc: taps in chunks of four (same summation order as fir8_fixed, so
+// every path gives identical bits for a given coefficient set)
+__device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
+                                             int p0, int pw, float a, float g, const KernelParams& kp) {
   float f[8];
   {
-    const float4 a = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw));
-    const float4 b = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw + 4));
+    const float4 u = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw));
+    const float4 w = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw + 4));
     const float c0 = kp.c[0];
-    f[0] = c0 * a.x; f[1] = c0 * a.y; f[2] = c0 * a.z; f[3] = c0 * a.w;
-    f[4] = c0 * b.x; f[5] = c0 * b.y; f[6] = c0 * b.z; f[7] = c0 * b.w;
+    f[0] = c0 * u.x; f[1] = c0 * u.y; f[2] = c0 * u.z; f[3] = c0 * u.w;
+    f[4] = c0 * w.x; f[5] = c0 * w.y; f[6] = c0 * w.z; f[7] = c0 * w.w;
   }
 #pragma unroll 1
   for (int i0 = 1; i0 <= kp.nc; i0 += 4) {
-    // left: positions p0 - i0 - 3 .. p0 + 7 - i0  ->  window u from p0 + pw - i0 - 3
-    // right: positions p0 + i0 .. p0 + 10 + i0     ->  window u from p0 + pw + i0 - 1
+    // left: positions p0 - i0 - 3 .. p0 + 7 - i0; right: p0 + i0 .. p0 + 10 + i0
     float l[12], r[12];
     const int ul = p0 + pw - i0 - 3;
     const int ur = p0 + pw + i0 - 1;
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
-      const float4 a = *reinterpret_cast<const float4*>(ibuf + fir_phys(ul + 4 * m));
-      const float4 b = *reinterpret_cast<const float4*>(ibuf + fir_phys(ur + 4 * m));
-      l[4 * m] = a.x; l[4 * m + 1] = a.y; l[4 * m + 2] = a.z; l[4 * m + 3] = a.w;
-      r[4 * m] = b.x; r[4 * m + 1] = b.y; r[4 * m + 2] = b.z; r[4 * m + 3] = b.w;
+      const float4 x = *reinterpret_cast<const float4*>(ibuf + fir_phys(ul + 4 * m));
+      const float4 y = *reinterpret_cast<const float4*>(ibuf + fir_phys(ur + 4 * m));
+      l[4 * m] = x.x; l[4 * m + 1] = x.y; l[4 * m + 2] = x.z; l[4 * m + 3] = x.w;
+      r[4 * m] = y.x; r[4 * m + 1] = y.y; r[4 * m + 2] = y.z; r[4 * m + 3] = y.w;
     }
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
       const float ci = __ldg(kp.coeff + i0 + d);
-      // tap i = i0 + d: left value at position p - i -> l[o + 3 - d]; right p + i -> r[o + 1 + d]
 #pragma unroll
       for (int o = 0; o < 8; ++o) f[o] = fmaf(ci, l[o + 3 - d] + r[o + 1 + d], f[o]);
     }
   }
-  *reinterpret_cast<float4*>(fbuf + fir_phys(p0)) = make_float4(f[0], f[1], f[2], f[3]);
-  *reinterpret_cast<float4*>(fbuf + fir_phys(p0 + 4)) = make_float4(f[4], f[5], f[6], f[7]);
+#pragma unroll
+  for (int o = 0; o < 8; o += 2) {
+    const float2 c0 = rot_factor(a, g, f[o]), c1 = rot_factor(a, g, f[o + 1]);
+    *reinterpret_cast<float4*>(csbuf + cs_phys(p0 + o)) = make_float4(c0.x, c0.y, c1.x, c1.y);
+  }
 }
 
 template <int LOGN>
-__device__ __forceinline__ void rotate(float2 (&x)[16], float2 (&y)[16], float* smf,
-                                       const KernelParams& kp, int step_idx, int t) {
+__device__ __forceinline__ void rotate(float2 (&v)[16], float* smf, const KernelParams& kp,
+                                       int step_idx, int t, int pol) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
+  const float2 sg = __ldg(kp.steps + step_idx);  // (a_j, g_j)
+  // total dual-pol intensity: own |v|^2 plus the partner lane's (lane ^ 16)
   float inten[16];
 #pragma unroll
-  for (int n = 0; n < 16; ++n)
-    inten[n] = fmaf(x[n].x, x[n].x, x[n].y * x[n].y) + fmaf(y[n].x, y[n].x, y[n].y * y[n].y);
-
-  float f[16];
+  for (int m = 0; m < 16; ++m) {
+    const float own = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
+    const float other = __shfl_xor_sync(0xffffffffu, own, 16);
+    inten[m] = pol ? other + own : own + other;
+  }
+  float2 cs[16];
   if (kp.nc == 0) {
+    // F = c0 I: each lane of the pair evaluates half the factors, then swaps
+    float2 mine[8];
 #pragma unroll
-    for (int n = 0; n < 16; ++n) f[n] = kp.c[0] * inten[n];
+    for (int i = 0; i < 8; ++i) mine[i] = rot_factor(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float2 oth = make_float2(__shfl_xor_sync(0xffffffffu, mine[i].x, 16),
+                                     __shfl_xor_sync(0xffffffffu, mine[i].y, 16));
+      cs[i] = pol ? oth : mine[i];
+      cs[8 + i] = pol ? mine[i] : oth;
+    }
   } else {
     const int pw = kp.fir_pad;
-    float* ibuf = smf;                                        // logical [-pw, N + pw)
-    float* fbuf = smf + fir_phys(N + 2 * pw) + 4;             // logical [0, N)
+    float* ibuf = smf;                                                      // logical [-pw, N + pw)
+    float2* csbuf = reinterpret_cast<float2*>(smf + fir_phys(N + 2 * pw) + 4);  // (cos, sin) per position
     __syncthreads();
+    // both lanes of a pair write the same 16 values (same addresses, no
+    // divergence): fir_phys(m T + t + pw) = m (5T/4) + fir_phys(t + pw) for T >= 16
+    if constexpr (T >= 16) {
+      float* ib = ibuf + fir_phys(t + pw);
 #pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      const int j = n * T + t;
-      ibuf[fir_phys(j + pw)] = inten[n];
-      if (j < pw) ibuf[fir_phys(j + N + pw)] = inten[n];
-      if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[n];
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int q = 0; q < 2; ++q) {
-      const int p0 = 16 * t + 8 * q;
-      switch (kp.nc) {
-        case 1: fir8_fixed<1>(ibuf, fbuf, p0, kp); break;
-        case 9: fir8_fixed<9>(ibuf, fbuf, p0, kp); break;
-        case 17: fir8_fixed<17>(ibuf, fbuf, p0, kp); break;
-        case 32: fir8_fixed<32>(ibuf, fbuf, p0, kp); break;
-        case 33: fir8_fixed<33>(ibuf, fbuf, p0, kp); break;
-        default: fir8_generic(ibuf, fbuf, p0, pw, kp); break;
+      for (int m = 0; m < 16; ++m) ib[m * (5 * T / 4)] = inten[m];
+      if (pw <= T) {
+        if (t < pw) ibuf[fir_phys(t + N + pw)] = inten[0];                    // j = t < pw
+        if (t >= T - pw) ibuf[fir_phys(15 * T + t - N + pw)] = inten[15];     // j >= N - pw
+      } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+          const int j = m * T + t;
+          if (j < pw) ibuf[fir_phys(j + N + pw)] = inten[m];
+          if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[m];
+        }
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int j = m * T + t;
+        ibuf[fir_phys(j + pw)] = inten[m];
+        if (j < pw) ibuf[fir_phys(j + N + pw)] = inten[m];
+        if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[m];
       }
     }
     __syncthreads();
+    const int p0 = 16 * t + 8 * pol;
+    switch (kp.nc) {
+      case 1: fir8_fixed<1>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
+      case 9: fir8_fixed<9>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
+      case 17: fir8_fixed<17>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
+      case 32: fir8_fixed<32>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
+      case 33: fir8_fixed<33>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
+      default: fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp); break;
+    }
+    __syncthreads();
+    if constexpr (T >= 16) {
+      const float2* cb = csbuf + cs_phys(t);  // cs_phys(m T + t) = m (9T/8) + cs_phys(t)
 #pragma unroll
-    for (int n = 0; n < 16; ++n) f[n] = fbuf[fir_phys(n * T + t)];
-  }
-
-  const float2 sg = __ldg(kp.steps + step_idx);  // (a_j, g_j)
+      for (int m = 0; m < 16; ++m) cs[m] = cb[m * (9 * T / 8)];
+    } else {
 #pragma unroll
-  for (int n = 0; n < 16; ++n) {
-    const float th = sg.x * f[n];
-    const float k = rintf(th * 0.159154943091895336f);
-    float r = fmaf(k, -6.28318548202514648f, th);
-    r = fmaf(k, 1.74845553e-7f, r);
-    float s, c;
-    __sincosf(r, &s, &c);
-    c *= sg.y;
-    s *= sg.y;
-    x[n] = make_float2(fmaf(x[n].x, c, -x[n].y * s), fmaf(x[n].x, s, x[n].y * c));
-    y[n] = make_float2(fmaf(y[n].x, c, -y[n].y * s), fmaf(y[n].x, s, y[n].y * c));
+      for (int m = 0; m < 16; ++m) cs[m] = csbuf[cs_phys(m * T + t)];
+    }
   }
+#pragma unroll
+  for (int m = 0; m < 16; ++m)
+    v[m] = make_float2(fmaf(v[m].x, cs[m].x, -v[m].y * cs[m].y), fmaf(v[m].x, cs[m].y, v[m].y * cs[m].x));
 }
 
 // ---------------------------------------------------------------------------
@@ -354,11 +393,15 @@ dbp_block_kernel(const KernelParams kp) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
   extern __shared__ float4 smem_raw[];
-  const int t = threadIdx.x;
-  float* smf = reinterpret_cast<float*>(smem_raw) + threadIdx.y * kp.slice_floats;
-  float4* sm = reinterpret_cast<float4*>(smf);
+  const int lane = threadIdx.x & 31;
+  const int pol = lane >> 4;
+  const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);  // position-thread index within the CTA
+  const int t = q % T;
+  const int slice = q / T;
+  float* smf = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats;
+  float2* plane = reinterpret_cast<float2*>(smf) + pol * (N + N / 16);
 
-  const long long blk = (long long)blockIdx.x * G::BPC + threadIdx.y;
+  const long long blk = (long long)blockIdx.x * G::BPC + slice;
   const bool active = blk < kp.total_blocks;
   long long item = 0, b = 0;
   if (active) {
@@ -366,35 +409,30 @@ dbp_block_kernel(const KernelParams kp) {
     b = kp.block_begin + (blk - item * kp.blocks_per_item);
   }
 
-  float2 x[16], y[16];
+  float2 v[16];
   const long long s0 = b * kp.step - kp.lead;  // global index of block sample 0
   if (active) {
-    const float2* px = kp.in + item * kp.in_item_stride;
-    const float2* py = px + kp.in_pol_stride;
+    const float2* pin = kp.in + item * kp.in_item_stride + pol * kp.in_pol_stride;
     if (!kp.cyclic || (s0 >= 0 && s0 + N <= kp.n_total)) {
       // interior block (or pre-extended chunk): one contiguous window, immediate offsets
-      const long long base = (kp.cyclic ? s0 : s0 - kp.in_origin) + t;
+      const float2* src = pin + (kp.cyclic ? s0 : s0 - kp.in_origin) + t;
 #pragma unroll
-      for (int n = 0; n < 16; ++n) {
-        x[n] = ld_stream(px + base + n * T);
-        y[n] = ld_stream(py + base + n * T);
-      }
+      for (int m = 0; m < 16; ++m) v[m] = ld_stream(src + m * T);
     } else {
       // edge block: circular extension of the whole signal (spectral.py:128)
 #pragma unroll
-      for (int n = 0; n < 16; ++n) {
-        long long gi = s0 + n * T + t;
+      for (int m = 0; m < 16; ++m) {
+        long long gi = s0 + m * T + t;
         if (gi < 0 || gi >= kp.n_total) {
           gi %= kp.n_total;
           if (gi < 0) gi += kp.n_total;
         }
-        x[n] = ld_stream(px + gi);
-        y[n] = ld_stream(py + gi);
+        v[m] = ld_stream(pin + gi);
       }
     }
   } else {
 #pragma unroll
-    for (int n = 0; n < 16; ++n) x[n] = y[n] = make_float2(0.f, 0.f);
+    for (int m = 0; m < 16; ++m) v[m] = make_float2(0.f, 0.f);
   }
 
   // operator program (dbp.py:212-233)
@@ -424,26 +462,23 @@ dbp_block_kernel(const KernelParams kp) {
       sidx = op >> 1;
     }
     if (is_conv) {
-      conv_pass<LOGN, 0>(x, y, sm, tab, kp.twiddle, t);
+      conv_pass<LOGN, 0>(v, plane, tab, kp.twiddle, t);
     } else {
-      rotate<LOGN>(x, y, smf, kp, sidx, t);
+      rotate<LOGN>(v, smf, kp, sidx, t, pol);
     }
   }
 
   if (active) {
-    float2* ox = kp.out + item * kp.out_item_stride;
-    float2* oy = ox + kp.out_pol_stride;
+    float2* pout = kp.out + item * kp.out_item_stride + pol * kp.out_pol_stride;
     const long long ob = b * kp.step - kp.lead - kp.out_origin;  // output index of block sample 0
-    const bool whole = (b + 1) * kp.step <= kp.n_total;
+    // kept samples j in [lead, min(lead + step, lead + n_total - b step))
+    const long long rem = kp.n_total - b * kp.step;
+    const int hi = kp.lead + (rem < kp.step ? (int)rem : kp.step);
+    float2* dst = pout + ob + t;
 #pragma unroll
-    for (int n = 0; n < 16; ++n) {
-      const int j = n * T + t;
-      const bool keep = j >= kp.lead && j < kp.lead + kp.step &&
-                        (whole || b * kp.step + (j - kp.lead) < kp.n_total);
-      if (keep) {
-        st_stream(ox + ob + j, x[n]);
-        st_stream(oy + ob + j, y[n]);
-      }
+    for (int m = 0; m < 16; ++m) {
+      const int j = m * T + t;
+      if (j >= kp.lead && j < hi) __stcs(dst + m * T, v[m]);
     }
   }
 }

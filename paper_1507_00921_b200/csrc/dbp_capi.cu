@@ -45,8 +45,6 @@ int ilog2_exact(int n) {
   return l;
 }
 
-int fir_phys(int u) { return u + ((u >> 4) << 2); }
-
 // RAII device switch
 struct DeviceGuard {
   int prev = -1;
@@ -104,25 +102,6 @@ struct dbp_plan {
 
 namespace {
 
-// Twiddles W_{16 S_p}^{ns k} for every pass p < NP-1, layout [p][k-1][ns], float64 -> float32.
-std::vector<float2> make_twiddles(int logn) {
-  const int np = (logn + 3) / 4;
-  std::vector<float2> tw;
-  for (int p = 0; p < np - 1; ++p) {
-    const int ls = logn - 4 * (p + 1);
-    const long long S = 1LL << ls;
-    const long long period = 16 * S;
-    for (int k = 1; k < 16; ++k) {
-      for (long long ns = 0; ns < S; ++ns) {
-        const long long m = (ns * k) % period;
-        const double ang = -2.0 * M_PI * (double)m / (double)period;
-        tw.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
-      }
-    }
-  }
-  return tw;
-}
-
 int upload(float2** dst, const std::vector<float2>& src) {
   if (*dst == nullptr) {
     DBP_CUDA(cudaMalloc(dst, src.size() * sizeof(float2)), "cudaMalloc(table)");
@@ -130,12 +109,6 @@ int upload(float2** dst, const std::vector<float2>& src) {
   DBP_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(float2), cudaMemcpyHostToDevice),
            "cudaMemcpy(table)");
   return DBP_OK;
-}
-
-int slice_floats(int N, int pw) {
-  int fir = fir_phys(N + 2 * pw) + 4 + fir_phys(N);
-  int v = 4 * N > fir ? 4 * N : fir;
-  return (v + 3) & ~3;
 }
 
 int check_ready(const dbp_plan* p) {
@@ -157,7 +130,7 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   kp.n_steps = p->n_steps;
   kp.nc = p->nc;
   kp.fir_pad = (p->nc + 3) & ~3;
-  kp.slice_floats = slice_floats(p->N, kp.fir_pad);
+  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad);
   kp.tab_full = p->d_full;
   kp.tab_half = p->d_half ? p->d_half : p->d_full;
   kp.twiddle = p->d_tw;
@@ -254,8 +227,7 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
   p->logn = logn;
   p->step = block_len - overlap;
   p->lead = overlap / 2;
-  std::vector<float2> tw = make_twiddles(logn);
-  if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
+  std::vector<float2> tw = dbp::make_twiddles(logn);
   int rc = upload(&p->d_tw, tw);
   if (rc != DBP_OK) {
     dbp_plan_destroy(p);

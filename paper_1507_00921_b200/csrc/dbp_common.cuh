@@ -1,0 +1,72 @@
+// Shared declarations of the fused DBP block kernels: launch parameters,
+// program / arrangement codes, streaming global memory helpers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dbp {
+
+
+constexpr int kMaxSideCoeffs = 64;
+
+enum Program : int { kFFE = 0, kSSFM = 1, kESSFM = 2, kRotateOnly = 3 };
+enum Arrangement : int { kSymmetric = 0, kLinearFirst = 1, kNonlinearFirst = 2 };
+
+struct KernelParams {
+  const float2* in;
+  float2* out;
+  long long n_total;          // samples per polarisation of the whole signal
+  long long in_pol_stride;    // float2 elements between the x and y rows
+  long long in_item_stride;   // float2 elements between batch items
+  long long out_pol_stride;
+  long long out_item_stride;
+  long long in_origin;        // global sample index of in[0]  (chunk mode)
+  long long out_origin;       // global sample index of out[0]
+  long long block_begin;      // first overlap-save block processed per item
+  long long blocks_per_item;  // blocks processed per item in this launch
+  long long total_blocks;     // blocks_per_item * items
+  int cyclic;                 // 1: global index taken modulo n_total
+  int step;                   // N - M
+  int lead;                   // M / 2
+  int program;                // Program
+  int arrangement;            // Arrangement
+  int n_steps;                // nonlinear steps
+  int nc;                     // side coefficients of the intensity FIR
+  int fir_pad;                // nc rounded up to a multiple of 4
+  int slice_floats;           // shared floats per block slice
+  const float2* tab_full;     // K (or H for FFE), natural bin order, 1/N folded in
+  const float2* tab_half;     // K^(1/2) (symmetric arrangement)
+  const float2* twiddle;      // per-pass twiddle tables
+  const float2* steps;        // per step (a_j, g_j): rotation exp(+j a_j F), gain g_j
+  const float* coeff;         // c_0..c_nc zero padded to nc + 4 (generic FIR path)
+  float c[kMaxSideCoeffs + 4];  // c_0..c_nc, zero padded
+};
+
+__device__ __forceinline__ float2 ld_stream(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];"
+               : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
+// read-only table load that the compiler may not merge with an earlier load
+// of the same address (keeps forward/inverse twiddles from living in registers
+// across the deeper FFT passes)
+__device__ __forceinline__ float2 ldg_table(const float2* p) {
+  float2 v;
+  asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "l"(p));
+  return v;
+}
+
+// value barrier: stops CSE of index arithmetic across the recursive passes
+__device__ __forceinline__ int opaque(int x) {
+  int y;
+  asm volatile("mov.b32 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+__device__ __forceinline__ void st_stream(float2* p, float2 v) {
+  asm volatile("st.global.cs.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(v.x), "f"(v.y) : "memory");
+}
+
+}  // namespace dbp

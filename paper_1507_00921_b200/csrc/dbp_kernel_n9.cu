@@ -13,7 +13,7 @@ cudaError_t launch_block_kernel<9>(const KernelParams& kp, long long n_ctas, siz
                                          (int)smem_bytes);
     if (e != cudaSuccess) return e;
   }
-  dbp_block_kernel<9><<<dim3((unsigned)n_ctas), dim3(G::T, G::BPC), smem_bytes, stream>>>(kp);
+  dbp_block_kernel<9><<<dim3((unsigned)n_ctas), dim3(launch_shape<9>().threads_x, launch_shape<9>().threads_y), smem_bytes, stream>>>(kp);
   return cudaGetLastError();
 }
 

@@ -3,7 +3,11 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#ifdef DBP_KERNEL_V1
+#include "dbp_block_kernel_v1.cuh"
+#else
 #include "dbp_block_kernel.cuh"
+#endif
 
 namespace dbp {
 
@@ -11,7 +15,8 @@ constexpr int kMinLogN = 4;   // N = 16
 constexpr int kMaxLogN = 13;  // N = 8192
 
 struct LaunchShape {
-  int threads_x;  // T = N / 16
+  int threads_x;  // threads per CTA along x
+  int threads_y;  // along y (v1: one row per block slice)
   int slices;     // block slices per CTA
 };
 
@@ -21,7 +26,11 @@ cudaError_t launch_block_kernel(const KernelParams& kp, long long n_ctas, size_t
 
 template <int LOGN>
 LaunchShape launch_shape() {
-  return LaunchShape{Geo<LOGN>::T, Geo<LOGN>::BPC};
+#ifdef DBP_KERNEL_V1
+  return LaunchShape{Geo<LOGN>::T, Geo<LOGN>::BPC, Geo<LOGN>::BPC};
+#else
+  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC};
+#endif
 }
 
 }  // namespace dbp

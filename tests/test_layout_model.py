@@ -57,3 +57,48 @@ def test_twiddle_table_size_matches_kernel_constant():
         g = Geo(logn)
         if g.NP > 1:
             assert twiddles(g).size == g.tw_offset(g.NP - 1)
+
+
+# ---- v2 (default) kernel: one polarisation per thread, radix R0 first ----
+
+from .layout_model import Geo2, conv_model2, twiddles2, xchg2  # noqa: E402
+
+
+@pytest.mark.parametrize("logn", list(range(4, 14)))
+def test_v2_conv_model_equals_fft_filter(logn):
+    n = 1 << logn
+    if n > 4096:
+        pytest.skip("pure-python model too slow above 4096")
+    rng = np.random.default_rng(100 + logn)
+    x = rng.normal(size=n) + 1j * rng.normal(size=n)
+    h = np.exp(1j * rng.uniform(-np.pi, np.pi, n))
+    got = conv_model2(x, h / n, logn)
+    want = np.fft.ifft(np.fft.fft(x) * h)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-11 * np.max(np.abs(want)))
+
+
+@pytest.mark.parametrize("logn", list(range(5, 14)))
+def test_v2_exchanges_bijective_and_conflict_free(logn):
+    # 8-byte accesses: the 16 lanes of one polarisation share a shared-memory phase
+    g = Geo2(logn)
+    n, T = g.N, g.T
+    for p in range(g.NP - 1):
+        assert len({xchg2(g, p, i) for i in range(n)}) == n and max(xchg2(g, p, i) for i in range(n)) < n + n // 16
+        if T < 16:
+            continue
+        ls1 = g.log_s(p + 1)
+        for h0 in range(0, T, 16):
+            lanes = range(h0, h0 + 16)
+            for m in range(16):
+                assert len({xchg2(g, p, t + T * m) % 16 for t in lanes}) == 16
+            for e in range(16):
+                banks = {xchg2(g, p, ((t >> ls1) << (ls1 + 4)) + (t & ((1 << ls1) - 1)) + (e << ls1)) % 16
+                         for t in lanes}
+                assert len(banks) == 16, (p, e)
+
+
+def test_v2_twiddle_table_size():
+    for logn in range(4, 14):
+        g = Geo2(logn)
+        if g.NP > 1:
+            assert twiddles2(g).size == g.tw_offset(g.NP - 1)

@@ -7,9 +7,10 @@ from paper_1507_00921_b200 import build as B
 ROOT = Path(__file__).resolve().parent.parent / "build" / "variants"
 VARIANTS = {
     "base": [],
-    "tps512": ["-DDBP_THREADS_PER_SM=512"],
-    "bpc3": ["-DDBP_CTA_THREADS=384"],
-    "bpc4": ["-DDBP_CTA_THREADS=512", "-DDBP_THREADS_PER_SM=512"],
+    "v1": ["-DDBP_KERNEL_V1"],
+    "v2_512": ["-DDBP_THREADS_PER_SM=512"],
+    "v2_1024": ["-DDBP_THREADS_PER_SM=1024"],
+    "v2_cta64": ["-DDBP_CTA_POSITIONS=64", "-DDBP_THREADS_PER_SM=768"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
