@@ -114,6 +114,16 @@ __device__ __forceinline__ int xchg_index(int i) {
   else return i;
 }
 
+// plane index of position t + T m; linear in m (base + m * stride) whenever
+// T % 16 == 0, so the 16 accesses are one base plus immediates
+template <int LOGN, int P>
+__device__ __forceinline__ int side_index(int t, int m) {
+  constexpr int T = Geo<LOGN>::T;
+  if constexpr (P + 1 != Geo<LOGN>::NP - 1) return t + T * m;
+  else if constexpr (T % 16 == 0) return pad16(t) + m * (T + T / 16);
+  else return pad16(t + T * m);
+}
+
 // ---------------------------------------------------------------------------
 // FFT -> x table -> IFFT on one polarisation, recursive over passes.
 // On entry and exit v[m] holds block position t + T m.
@@ -148,7 +158,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ 
     constexpr int LS1 = G::log_s(1);
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; ++m) plane[xchg_index<LOGN, 0>(t + T * m)] = v[m];
+    for (int m = 0; m < 16; ++m) plane[side_index<LOGN, 0>(t, m)] = v[m];
     __syncthreads();
     {
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
@@ -167,7 +177,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ 
     }
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = plane[xchg_index<LOGN, 0>(t + T * m)];
+    for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, 0>(t, m)];
 #pragma unroll
     for (int q = 0; q < G0; ++q) {
       float2 u[R0];
@@ -188,7 +198,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ 
     for (int k = 1; k < 16; ++k) v[k] = c_mul(v[k], ldg_table(twp + (k - 1) * S));
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; ++m) plane[xchg_index<LOGN, P>(t + T * m)] = v[m];
+    for (int m = 0; m < 16; ++m) plane[side_index<LOGN, P>(t, m)] = v[m];
     __syncthreads();
     {
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
@@ -208,7 +218,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ 
     }
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = plane[xchg_index<LOGN, P>(t + T * m)];
+    for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
 #pragma unroll
     for (int k = 1; k < 16; ++k) v[k] = c_mulc(v[k], ldg_table(twp + (k - 1) * S));
     dft<16, true>(v);
@@ -315,18 +325,15 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], float* smf, const Kernel
     const float other = __shfl_xor_sync(0xffffffffu, own, 16);
     inten[m] = pol ? other + own : own + other;
   }
-  float2 cs[16];
   if (kp.nc == 0) {
     // F = c0 I: each lane of the pair evaluates half the factors, then swaps
-    float2 mine[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) mine[i] = rot_factor(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float2 oth = make_float2(__shfl_xor_sync(0xffffffffu, mine[i].x, 16),
-                                     __shfl_xor_sync(0xffffffffu, mine[i].y, 16));
-      cs[i] = pol ? oth : mine[i];
-      cs[8 + i] = pol ? mine[i] : oth;
+      const float2 mine = rot_factor(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
+      const float2 oth = make_float2(__shfl_xor_sync(0xffffffffu, mine.x, 16),
+                                     __shfl_xor_sync(0xffffffffu, mine.y, 16));
+      v[i] = c_mul(v[i], pol ? oth : mine);
+      v[8 + i] = c_mul(v[8 + i], pol ? mine : oth);
     }
   } else {
     const int pw = kp.fir_pad;
@@ -373,15 +380,12 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], float* smf, const Kernel
     if constexpr (T >= 16) {
       const float2* cb = csbuf + cs_phys(t);  // cs_phys(m T + t) = m (9T/8) + cs_phys(t)
 #pragma unroll
-      for (int m = 0; m < 16; ++m) cs[m] = cb[m * (9 * T / 8)];
+      for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], cb[m * (9 * T / 8)]);
     } else {
 #pragma unroll
-      for (int m = 0; m < 16; ++m) cs[m] = csbuf[cs_phys(m * T + t)];
+      for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], csbuf[cs_phys(m * T + t)]);
     }
   }
-#pragma unroll
-  for (int m = 0; m < 16; ++m)
-    v[m] = make_float2(fmaf(v[m].x, cs[m].x, -v[m].y * cs[m].y), fmaf(v[m].x, cs[m].y, v[m].y * cs[m].x));
 }
 
 // ---------------------------------------------------------------------------
