@@ -43,6 +43,9 @@ namespace dbp {
 #ifndef DBP_CTA_POSITIONS
 #define DBP_CTA_POSITIONS 128
 #endif
+#ifndef DBP_DOUBLE_BUFFER
+#define DBP_DOUBLE_BUFFER 0
+#endif
 
 template <int LOGN>
 struct Geo {
@@ -55,6 +58,9 @@ struct Geo {
   static constexpr int BPC = T >= DBP_CTA_POSITIONS ? 1 : DBP_CTA_POSITIONS / T;
   static constexpr int THREADS = 2 * T * BPC;
   static constexpr int MIN_CTAS = DBP_THREADS_PER_SM / THREADS > 0 ? DBP_THREADS_PER_SM / THREADS : 1;
+  // two shared buffers per slice (one barrier per exchange instead of two)
+  // while both fit next to the L1-resident tables
+  static constexpr bool DB = DBP_DOUBLE_BUFFER && (2 * 16 * (N + N / 16) * BPC <= 80 * 1024);
   // log2 of the pass stride S_p = N / (L_p r_p)
   __host__ __device__ static constexpr int log_s(int p) { return LOGN - LOGR0 - 4 * p; }
   // offset of pass p's twiddle table: pass 0 holds (R0-1) N/R0 entries, pass q >= 1 15 S_q
@@ -124,12 +130,36 @@ __device__ __forceinline__ int side_index(int t, int m) {
   else return pad16(t + T * m);
 }
 
+// Shared-memory phases.  Single-buffered: barrier before and after every
+// write phase.  Double-buffered: consecutive phases alternate buffers, so the
+// barrier after a phase's writes also proves every reader of the other
+// buffer is done -- one barrier per phase.
+template <int LOGN>
+struct Shm {
+  float* base;   // slice base
+  int half;      // floats per buffer
+  int par;       // buffer of the next write phase
+  int pol;
+  __device__ __forceinline__ float* buf(int which) const { return base + which * half; }
+  __device__ __forceinline__ float2* plane() const {
+    constexpr int N = Geo<LOGN>::N;
+    return reinterpret_cast<float2*>(buf(Geo<LOGN>::DB ? par : 0)) + pol * (N + N / 16);
+  }
+  __device__ __forceinline__ void before_write() const {
+    if constexpr (!Geo<LOGN>::DB) __syncthreads();
+  }
+  __device__ __forceinline__ void after_write() const { __syncthreads(); }
+  __device__ __forceinline__ void flip() {
+    if constexpr (Geo<LOGN>::DB) par ^= 1;
+  }
+};
+
 // ---------------------------------------------------------------------------
 // FFT -> x table -> IFFT on one polarisation, recursive over passes.
 // On entry and exit v[m] holds block position t + T m.
 // ---------------------------------------------------------------------------
 template <int LOGN, int P>
-__device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ plane,
+__device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
                                           const float2* __restrict__ tab,
                                           const float2* __restrict__ tw, int t) {
   using G = Geo<LOGN>;
@@ -156,28 +186,38 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ 
     }
     // exchange into the pass-1 layout
     constexpr int LS1 = G::log_s(1);
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < 16; ++m) plane[side_index<LOGN, 0>(t, m)] = v[m];
-    __syncthreads();
+    sh.before_write();
     {
+      float2* plane = sh.plane();
+#pragma unroll
+      for (int m = 0; m < 16; ++m) plane[side_index<LOGN, 0>(t, m)] = v[m];
+    }
+    sh.after_write();
+    {
+      const float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
     }
+    sh.flip();
 
-    conv_pass<LOGN, 1>(v, plane, tab, tw, t);
+    conv_pass<LOGN, 1>(v, sh, tab, tw, t);
     t = opaque(t);
 
-    __syncthreads();
+    sh.before_write();
     {
+      float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) plane[xchg_index<LOGN, 0>(base + (e << LS1))] = v[e];
     }
-    __syncthreads();
+    sh.after_write();
+    {
+      const float2* plane = sh.plane();
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, 0>(t, m)];
+      for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, 0>(t, m)];
+    }
+    sh.flip();
 #pragma unroll
     for (int q = 0; q < G0; ++q) {
       float2 u[R0];
@@ -196,29 +236,39 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], float2* __restrict__ 
     dft<16, false>(v);
 #pragma unroll
     for (int k = 1; k < 16; ++k) v[k] = c_mul(v[k], ldg_table(twp + (k - 1) * S));
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < 16; ++m) plane[side_index<LOGN, P>(t, m)] = v[m];
-    __syncthreads();
+    sh.before_write();
     {
+      float2* plane = sh.plane();
+#pragma unroll
+      for (int m = 0; m < 16; ++m) plane[side_index<LOGN, P>(t, m)] = v[m];
+    }
+    sh.after_write();
+    {
+      const float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
     }
+    sh.flip();
 
-    conv_pass<LOGN, P + 1>(v, plane, tab, tw, t);
+    conv_pass<LOGN, P + 1>(v, sh, tab, tw, t);
     t = opaque(t);
     twp = tw + G::tw_offset(P) + (t & (S - 1));
 
-    __syncthreads();
+    sh.before_write();
     {
+      float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) plane[xchg_index<LOGN, P>(base + (e << LS1))] = v[e];
     }
-    __syncthreads();
+    sh.after_write();
+    {
+      const float2* plane = sh.plane();
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
+      for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
+    }
+    sh.flip();
 #pragma unroll
     for (int k = 1; k < 16; ++k) v[k] = c_mulc(v[k], ldg_table(twp + (k - 1) * S));
     dft<16, true>(v);
@@ -312,7 +362,7 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
 }
 
 template <int LOGN>
-__device__ __forceinline__ void rotate(float2 (&v)[16], float* smf, const KernelParams& kp,
+__device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const KernelParams& kp,
                                        int step_idx, int t, int pol) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
@@ -337,9 +387,11 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], float* smf, const Kernel
     }
   } else {
     const int pw = kp.fir_pad;
-    float* ibuf = smf;                                                      // logical [-pw, N + pw)
-    float2* csbuf = reinterpret_cast<float2*>(smf + fir_phys(N + 2 * pw) + 4);  // (cos, sin) per position
-    __syncthreads();
+    // intensity buffer (logical [-pw, N + pw)) in this phase's buffer; (cos, sin)
+    // buffer behind it, in the other buffer when double-buffered
+    float* ibuf = sh.buf(Geo<LOGN>::DB ? sh.par : 0);
+    float2* csbuf = reinterpret_cast<float2*>(sh.buf(Geo<LOGN>::DB ? sh.par ^ 1 : 0) + fir_phys(N + 2 * pw) + 4);
+    sh.before_write();
     // both lanes of a pair write the same 16 values (same addresses, no
     // divergence): fir_phys(m T + t + pw) = m (5T/4) + fir_phys(t + pw) for T >= 16
     if constexpr (T >= 16) {
@@ -366,7 +418,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], float* smf, const Kernel
         if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[m];
       }
     }
-    __syncthreads();
+    sh.after_write();
     const int p0 = 16 * t + 8 * pol;
     switch (kp.nc) {
       case 1: fir8_fixed<1>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
@@ -402,8 +454,11 @@ dbp_block_kernel(const KernelParams kp) {
   const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);  // position-thread index within the CTA
   const int t = q % T;
   const int slice = q / T;
-  float* smf = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats;
-  float2* plane = reinterpret_cast<float2*>(smf) + pol * (N + N / 16);
+  Shm<LOGN> sh;
+  sh.base = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats * (G::DB ? 2 : 1);
+  sh.half = kp.slice_floats;
+  sh.par = 0;
+  sh.pol = pol;
 
   const long long blk = (long long)blockIdx.x * G::BPC + slice;
   const bool active = blk < kp.total_blocks;
@@ -466,9 +521,9 @@ dbp_block_kernel(const KernelParams kp) {
       sidx = op >> 1;
     }
     if (is_conv) {
-      conv_pass<LOGN, 0>(v, plane, tab, kp.twiddle, t);
+      conv_pass<LOGN, 0>(v, sh, tab, kp.twiddle, t);
     } else {
-      rotate<LOGN>(v, smf, kp, sidx, t, pol);
+      rotate<LOGN>(v, sh, kp, sidx, t, pol);
     }
   }
 

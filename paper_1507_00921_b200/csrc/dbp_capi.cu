@@ -145,7 +145,8 @@ int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
   const dbp::LaunchShape sh = d.shape[p->logn]();
   const long long ctas = (kp.total_blocks + sh.slices - 1) / sh.slices;
   if (ctas > 0x7fffffffLL) return fail(DBP_EINVAL, "too many blocks for one launch");
-  const size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices;
+  const size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices * sh.buffers;
+  if (smem > 227 * 1024) return fail(DBP_EINVAL, "shared memory per CTA exceeds 227 KB for this block length");
   cudaError_t e = d.launch[p->logn](kp, ctas, smem, s);
   if (e != cudaSuccess) return cuda_fail(e, "dbp_block_kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);

@@ -29,31 +29,6 @@ __device__ __forceinline__ float2 c_rot90(float2 a) {
   return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
 }
 
-// W_16^m for the forward kernel, conjugated for the inverse one.
-template <bool INV, int M>
-__device__ __forceinline__ float2 w16_apply(float2 a) {
-  constexpr float C1 = 0.92387953251128674f;  // cos(pi/8)
-  constexpr float S1 = 0.38268343236508978f;  // sin(pi/8)
-  constexpr float R2 = 0.70710678118654752f;  // 1/sqrt(2)
-  constexpr float sg = INV ? 1.0f : -1.0f;    // sign of the imaginary part
-  if constexpr (M == 0) {
-    return a;
-  } else if constexpr (M == 1) {
-    return c_mul(a, make_float2(C1, sg * S1));
-  } else if constexpr (M == 2) {
-    return c_mul(a, make_float2(R2, sg * R2));
-  } else if constexpr (M == 3) {
-    return c_mul(a, make_float2(S1, sg * C1));
-  } else if constexpr (M == 4) {
-    return c_rot90<INV>(a);
-  } else if constexpr (M == 6) {
-    return c_mul(a, make_float2(-R2, sg * R2));
-  } else {
-    static_assert(M == 9, "unsupported W16 exponent");
-    return c_mul(a, make_float2(-C1, -sg * S1));
-  }
-}
-
 template <bool INV>
 __device__ __forceinline__ void dft2(float2& a, float2& b) {
   const float2 t = a;
@@ -71,19 +46,64 @@ __device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2&
   a3 = c_sub(t1, t3);
 }
 
+// W_16^M of the forward kernel (conjugate for INV) as a compile-time constant
+template <bool INV, int M>
+__device__ __forceinline__ float2 w16() {
+  constexpr int m = M & 15;
+  constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508978f, R2 = 0.70710678118654752f;
+  constexpr float tab_re[16] = {1.f, C1, R2, S1, 0.f, -S1, -R2, -C1, -1.f, -C1, -R2, -S1, 0.f, S1, R2, C1};
+  constexpr float tab_im[16] = {0.f, -S1, -R2, -C1, -1.f, -C1, -R2, -S1, 0.f, S1, R2, C1, 1.f, C1, R2, S1};
+  return make_float2(tab_re[m], INV ? -tab_im[m] : tab_im[m]);
+}
+
+// (p + w q, p - w q) for w = W_16^M: plain adds for the four trivial roots,
+// otherwise 4 FFMA for the sum and 2 FFMA for the difference (2p - sum)
+template <bool INV, int M>
+__device__ __forceinline__ void pm_w16(float2 p, float2 q, float2& plus, float2& minus) {
+  constexpr int m = M & 15;
+  if constexpr (m == 0) {
+    plus = c_add(p, q); minus = c_sub(p, q);
+  } else if constexpr (m == 8) {
+    plus = c_sub(p, q); minus = c_add(p, q);
+  } else if constexpr (m == 4) {
+    const float2 r = c_rot90<INV>(q);   // forward: -j q
+    plus = c_add(p, r); minus = c_sub(p, r);
+  } else if constexpr (m == 12) {
+    const float2 r = c_rot90<!INV>(q);  // forward: +j q
+    plus = c_add(p, r); minus = c_sub(p, r);
+  } else {
+    const float2 w = w16<INV, M>();
+    plus = make_float2(fmaf(w.x, q.x, fmaf(-w.y, q.y, p.x)), fmaf(w.x, q.y, fmaf(w.y, q.x, p.y)));
+    minus = make_float2(fmaf(2.0f, p.x, -plus.x), fmaf(2.0f, p.y, -plus.y));
+  }
+}
+
+// Second Cooley-Tukey stage of a 4 x S split with the inner twiddles fused:
+// inputs a_n2 = Y[n2][k1] (n2 = 0..3, untwiddled), twiddles W^{n2 k1} of the
+// length-4S transform (W = W_16^(16/(4S)) steps); outputs for k2 = 0..3.
+// With b_n2 = W^{n2 k1} a_n2:  b0 +- b2 = a0 +- W^{2k1} a2,
+// b1 +- b3 = W^{k1} (a1 +- W^{2k1} a3).
+template <bool INV, int MK1, int M2K1>
+__device__ __forceinline__ void row4_fused(float2 a0, float2 a1, float2 a2, float2 a3,
+                                           float2& x0, float2& x1, float2& x2, float2& x3) {
+  float2 t0, t1, u2, u3;
+  pm_w16<INV, M2K1>(a0, a2, t0, t1);
+  pm_w16<INV, M2K1>(a1, a3, u2, u3);
+  pm_w16<INV, MK1>(t0, u2, x0, x2);        // k2 = 0, 2
+  pm_w16<INV, MK1 + 4>(t1, u3, x1, x3);    // k2 = 1, 3 (multiplier -j W^{k1})
+}
+
 // 8 = 2 x 4: n = 4 n1 + n2, k = k1 + 2 k2
 template <bool INV>
 __device__ __forceinline__ void dft8(float2* v) {
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) dft2<INV>(v[n2], v[n2 + 4]);
-  v[5] = w16_apply<INV, 2>(v[5]);
-  v[6] = w16_apply<INV, 4>(v[6]);
-  v[7] = w16_apply<INV, 6>(v[7]);
-  dft4<INV>(v[0], v[1], v[2], v[3]);
-  dft4<INV>(v[4], v[5], v[6], v[7]);
-  // v[4 k1 + k2] holds X[k1 + 2 k2]
-  const float2 u1 = v[1], u2 = v[2], u3 = v[3], u4 = v[4], u5 = v[5], u6 = v[6];
-  v[1] = u4; v[2] = u1; v[3] = u5; v[4] = u2; v[5] = u6; v[6] = u3;
+  // row k1 = 0: Y[n2][0] = v[n2]; row k1 = 1: Y[n2][1] = v[4 + n2] with W_8^{n2}
+  float2 x[8];
+  row4_fused<INV, 0, 0>(v[0], v[1], v[2], v[3], x[0], x[2], x[4], x[6]);
+  row4_fused<INV, 2, 4>(v[4], v[5], v[6], v[7], x[1], x[3], x[5], x[7]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = x[i];
 }
 
 // 16 = 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2
@@ -91,26 +111,14 @@ template <bool INV>
 __device__ __forceinline__ void dft16(float2* v) {
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2]);
-  // v[4 k1 + n2] *= W16^{n2 k1}
-  v[5] = w16_apply<INV, 1>(v[5]);
-  v[6] = w16_apply<INV, 2>(v[6]);
-  v[7] = w16_apply<INV, 3>(v[7]);
-  v[9] = w16_apply<INV, 2>(v[9]);
-  v[10] = w16_apply<INV, 4>(v[10]);
-  v[11] = w16_apply<INV, 6>(v[11]);
-  v[13] = w16_apply<INV, 3>(v[13]);
-  v[14] = w16_apply<INV, 6>(v[14]);
-  v[15] = w16_apply<INV, 9>(v[15]);
+  // v[4 k1 + n2] holds Y[n2][k1]; fused twiddle W_16^{n2 k1} + DFT4 over n2
+  float2 x[16];
+  row4_fused<INV, 0, 0>(v[0], v[1], v[2], v[3], x[0], x[4], x[8], x[12]);
+  row4_fused<INV, 1, 2>(v[4], v[5], v[6], v[7], x[1], x[5], x[9], x[13]);
+  row4_fused<INV, 2, 4>(v[8], v[9], v[10], v[11], x[2], x[6], x[10], x[14]);
+  row4_fused<INV, 3, 6>(v[12], v[13], v[14], v[15], x[3], x[7], x[11], x[15]);
 #pragma unroll
-  for (int k1 = 0; k1 < 4; ++k1) dft4<INV>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
-  // v[4 k1 + k2] holds X[k1 + 4 k2]: transpose the 4x4 register tile
-  float2 u[16];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) u[i] = v[i];
-#pragma unroll
-  for (int k1 = 0; k1 < 4; ++k1)
-#pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = u[4 * k1 + k2];
+  for (int i = 0; i < 16; ++i) v[i] = x[i];
 }
 
 template <int R, bool INV>

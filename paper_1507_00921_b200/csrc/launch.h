@@ -18,6 +18,7 @@ struct LaunchShape {
   int threads_x;  // threads per CTA along x
   int threads_y;  // along y (v1: one row per block slice)
   int slices;     // block slices per CTA
+  int buffers;    // shared buffers per slice (2 = double-buffered exchanges)
 };
 
 template <int LOGN>
@@ -27,9 +28,9 @@ cudaError_t launch_block_kernel(const KernelParams& kp, long long n_ctas, size_t
 template <int LOGN>
 LaunchShape launch_shape() {
 #ifdef DBP_KERNEL_V1
-  return LaunchShape{Geo<LOGN>::T, Geo<LOGN>::BPC, Geo<LOGN>::BPC};
+  return LaunchShape{Geo<LOGN>::T, Geo<LOGN>::BPC, Geo<LOGN>::BPC, 1};
 #else
-  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC};
+  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::DB ? 2 : 1};
 #endif
 }
 

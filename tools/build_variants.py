@@ -11,6 +11,8 @@ VARIANTS = {
     "v2_512": ["-DDBP_THREADS_PER_SM=512"],
     "v2_1024": ["-DDBP_THREADS_PER_SM=1024"],
     "v2_cta64": ["-DDBP_CTA_POSITIONS=64", "-DDBP_THREADS_PER_SM=768"],
+    "single": ["-DDBP_DOUBLE_BUFFER=0"],
+    "double": ["-DDBP_DOUBLE_BUFFER=1"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
