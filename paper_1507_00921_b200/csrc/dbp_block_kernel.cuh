@@ -286,14 +286,56 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 // ---------------------------------------------------------------------------
 
 // (cos, sin) * g of theta = a * F with explicit 2 pi range reduction
+// (cos, sin) * g of theta = a * F.  ``precise``: quadrant reduction
+// r = th - k pi/2 (two-constant Cody-Waite) and minimax polynomials on
+// [-pi/4, pi/4], about 1 ulp and unbiased; otherwise 2 pi reduction and the
+// SFU's __sincosf, whose smooth argument-correlated absolute error (up to
+// 2^-21.4) accumulates coherently over many SSFM steps -- the host picks the
+// precise form for programs with >= 3 nonlinear steps.
+template <bool PRECISE>
 __device__ __forceinline__ float2 rot_factor(float a, float g, float f) {
   const float th = a * f;
-  const float k = rintf(th * 0.159154943091895336f);
-  float r = fmaf(k, -6.28318548202514648f, th);
-  r = fmaf(k, 1.74845553e-7f, r);
   float s, c;
-  __sincosf(r, &s, &c);
+  if constexpr (PRECISE) {
+    const float k = rintf(th * 0.636619772367581343f);
+    float r = fmaf(k, -1.57079637050628662f, th);
+    r = fmaf(k, 4.37113900018624283e-8f, r);
+    const float z = r * r;
+    float sp = fmaf(z, -1.9515295891e-4f, 8.3321608736e-3f);
+    sp = fmaf(z, sp, -1.6666654611e-1f);
+    const float sn = fmaf(r * z, sp, r);
+    float cp = fmaf(z, 2.443315711809948e-5f, -1.388731625493765e-3f);
+    cp = fmaf(z, cp, 4.166664568298827e-2f);
+    const float cs = fmaf(z * z, cp, fmaf(z, -0.5f, 1.0f));
+    const int q = static_cast<int>(k) & 3;
+    s = (q & 1) ? cs : sn;
+    c = (q & 1) ? sn : cs;
+    if (q & 2) s = -s;
+    if ((q + 1) & 2) c = -c;
+  } else {
+    const float k = rintf(th * 0.159154943091895336f);
+    float r = fmaf(k, -6.28318548202514648f, th);
+    r = fmaf(k, 1.74845553e-7f, r);
+    __sincosf(r, &s, &c);
+  }
   return make_float2(c * g, s * g);
+}
+
+// 8 filtered intensities -> rotation factors -> (cos, sin) buffer
+template <bool PRECISE>
+__device__ __forceinline__ void store_factors8(float2* __restrict__ csbuf, int p0, const float (&f)[8],
+                                               float a, float g) {
+#pragma unroll
+  for (int o = 0; o < 8; o += 2) {
+    const float2 c0 = rot_factor<PRECISE>(a, g, f[o]), c1 = rot_factor<PRECISE>(a, g, f[o + 1]);
+    *reinterpret_cast<float4*>(csbuf + cs_phys(p0 + o)) = make_float4(c0.x, c0.y, c1.x, c1.y);
+  }
+}
+
+__device__ __forceinline__ void store_factors8(float2* __restrict__ csbuf, int p0, const float (&f)[8],
+                                               float a, float g, bool precise) {
+  if (precise) store_factors8<true>(csbuf, p0, f, a, g);
+  else store_factors8<false>(csbuf, p0, f, a, g);
 }
 
 // 8 consecutive FIR outputs p0 .. p0+7 from a register window of the padded
@@ -309,17 +351,15 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
     const float4 q = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
     w[4 * m] = q.x; w[4 * m + 1] = q.y; w[4 * m + 2] = q.z; w[4 * m + 3] = q.w;
   }
-  float2 cs[8];
+  float f[8];
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
     float acc = kp.c[0] * w[o + PW];
 #pragma unroll
     for (int i = 1; i <= NC; ++i) acc = fmaf(kp.c[i], w[o + PW - i] + w[o + PW + i], acc);
-    cs[o] = rot_factor(a, g, acc);
+    f[o] = acc;
   }
-#pragma unroll
-  for (int o = 0; o < 8; o += 2)
-    *reinterpret_cast<float4*>(csbuf + cs_phys(p0 + o)) = make_float4(cs[o].x, cs[o].y, cs[o + 1].x, cs[o + 1].y);
+  store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
 }
 
 // any nc: taps in chunks of four (same summation order as fir8_fixed, so
@@ -354,11 +394,7 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
       for (int o = 0; o < 8; ++o) f[o] = fmaf(ci, l[o + 3 - d] + r[o + 1 + d], f[o]);
     }
   }
-#pragma unroll
-  for (int o = 0; o < 8; o += 2) {
-    const float2 c0 = rot_factor(a, g, f[o]), c1 = rot_factor(a, g, f[o + 1]);
-    *reinterpret_cast<float4*>(csbuf + cs_phys(p0 + o)) = make_float4(c0.x, c0.y, c1.x, c1.y);
-  }
+  store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
 }
 
 template <int LOGN>
@@ -377,9 +413,17 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
   }
   if (kp.nc == 0) {
     // F = c0 I: each lane of the pair evaluates half the factors, then swaps
+    float2 fac[8];
+    if (kp.precise_sincos) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<true>(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<false>(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float2 mine = rot_factor(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
+      const float2 mine = fac[i];
       const float2 oth = make_float2(__shfl_xor_sync(0xffffffffu, mine.x, 16),
                                      __shfl_xor_sync(0xffffffffu, mine.y, 16));
       v[i] = c_mul(v[i], pol ? oth : mine);

@@ -131,6 +131,7 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   kp.nc = p->nc;
   kp.fir_pad = (p->nc + 3) & ~3;
   kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad);
+  kp.precise_sincos = p->n_steps >= 3 ? 1 : 0;
   kp.tab_full = p->d_full;
   kp.tab_half = p->d_half ? p->d_half : p->d_full;
   kp.twiddle = p->d_tw;

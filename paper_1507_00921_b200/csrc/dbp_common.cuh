@@ -34,6 +34,7 @@ struct KernelParams {
   int nc;                     // side coefficients of the intensity FIR
   int fir_pad;                // nc rounded up to a multiple of 4
   int slice_floats;           // shared floats per block slice
+  int precise_sincos;         // 1: polynomial sincos (multi-step programs), 0: SFU
   const float2* tab_full;     // K (or H for FFE), natural bin order, 1/N folded in
   const float2* tab_half;     // K^(1/2) (symmetric arrangement)
   const float2* twiddle;      // per-pass twiddle tables

@@ -261,3 +261,19 @@ def test_full_size_properties(rng):
     np.testing.assert_array_equal(plain, ident)
     # energy: the inverse-dispersion filter is unitary up to framing
     assert abs(np.sum(np.abs(a) ** 2) / np.sum(np.abs(x[0]) ** 2) - 1.0) < 0.05
+
+
+@pytest.mark.parametrize("power_dbm", [-4.0, 0.0, 4.0])
+def test_config2_ssfm20_power_sweep(power_dbm):
+    # BASELINE configs[2]: 20-step SSFM (dispersion then rotation), gamma' = 8/9 * 1.3,
+    # launch power -4..+4 dBm; per-block rel-L2 <= 1e-5 (multi-step programs use the
+    # polynomial sincos -- the SFU's correlated error would exceed the bar at +4 dBm)
+    beta2 = waveforms.d_to_beta2(17.0)
+    tx, _ = waveforms.qpsk_rrc(2 ** 12, 2, 0.1, seed=4, power_dbm=power_dbm)
+    rx = waveforms.forward_link(tx, 56e9, beta2, 1.3 * 8 / 9, 0.2, 80.0, 40, 4).astype(np.complex64)
+    span = pb.FiberParams(beta2, 1.3 * 8 / 9, 0.2, 80.0)
+    cfg = pb.DbpConfig("ssfm", pb.OverlapPlan(2048, 700), quiet_link(40, span), num_steps=20,
+                       arrangement="linear-first")
+    got = _run(rx, cfg)[0]
+    want = dbp_port.backpropagate_arrays(rx.astype(np.complex128), 56e9, port_config(cfg))
+    assert dbp_port.per_block_rel_l2(got, want, 2048, 700).max() <= TOL_BLOCK
