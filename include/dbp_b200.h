@@ -123,6 +123,22 @@ int dbp_plan_set_staging(dbp_plan* plan, size_t bytes);
 int dbp_process_blocks(dbp_plan* plan, const void* d_blocks, void* d_out, int64_t n_blocks,
                        void* stream);
 
+/* Per-item coefficient sets for ESSFM training batches (the reference's
+ * finite-difference Jacobian evaluates N_c+1 perturbed sets on one
+ * waveform, train.py:153-158): ``coeffs`` is [n_sets][n_coeffs + 1]
+ * float64.  Used only by the *_coeff_batch entry points.                   */
+int dbp_plan_set_coeff_batch(dbp_plan* plan, const double* coeffs, int n_sets, int n_coeffs);
+
+/* One waveform d_in [2][n_total], every coefficient set: d_out is
+ * [n_sets][2][n_total], item i processed with set i (blocks
+ * [block_begin, block_end)).  Asynchronous on ``stream``.                   */
+int dbp_run_coeff_batch(dbp_plan* plan, const void* d_in, void* d_out, int64_t n_total,
+                        int64_t block_begin, int64_t block_end, void* stream);
+
+/* Host-buffer form of dbp_run_coeff_batch (synchronous): h_in [2][n_total],
+ * h_out [n_sets][2][n_total] complex64.                                     */
+int dbp_run_host_coeff_batch(dbp_plan* plan, const void* h_in, void* h_out, int64_t n_total);
+
 /* Wait for all work the plan queued on its internal streams. */
 int dbp_plan_synchronize(dbp_plan* plan);
 

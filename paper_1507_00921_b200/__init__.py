@@ -34,6 +34,8 @@ from .backprop import (
     nonlinear_substep_ssfm,
 )
 
+from .training import TrainConfig, TrainResult, load_coefficients, mse, optimize_coefficients, save_coefficients
+
 __version__ = "0.1.0"
 
 __all__ = [
@@ -42,5 +44,6 @@ __all__ = [
     "OverlapPlan", "fft_frequencies", "is_power_of_two", "next_power_of_two", "shard_blocks",
     "ALGORITHMS", "ARRANGEMENTS", "DbpConfig", "DbpEngine", "backpropagate", "backpropagate_batch",
     "channel_memory_samples", "estimate_channel_memory", "get_engine", "nonlinear_substep_essfm",
-    "nonlinear_substep_ssfm", "__version__",
+    "nonlinear_substep_ssfm", "TrainConfig", "TrainResult", "load_coefficients", "mse",
+    "optimize_coefficients", "save_coefficients", "__version__",
 ]

@@ -44,6 +44,10 @@ SIGNATURES = {
     "dbp_launch_count": (_c_int64, []),
     "dbp_probe_fp32_peak": (_c_int, [_c_int, _c_int, ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)]),
+    "dbp_plan_set_coeff_batch": (_c_int, [_c_void_p, _c_double_p, _c_int, _c_int]),
+    "dbp_run_coeff_batch": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int64, _c_int64,
+                                     _c_void_p]),
+    "dbp_run_host_coeff_batch": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64]),
 }
 
 _lib = None
@@ -185,6 +189,26 @@ class NativePlan:
     def process_blocks(self, d_in: int, d_out: int, n_blocks: int, stream: int = 0):
         _check(self._lib.dbp_process_blocks(self._h, d_in, d_out, int(n_blocks), stream or None),
                "dbp_process_blocks")
+
+    def set_coeff_batch(self, coeff_sets: np.ndarray):
+        """coeff_sets: (n_sets, n_coeffs + 1) float64."""
+        c = np.ascontiguousarray(np.asarray(coeff_sets, dtype=np.float64))
+        if c.ndim != 2:
+            raise ValueError("coefficient sets must be a (n_sets, n_coeffs + 1) array")
+        _check(self._lib.dbp_plan_set_coeff_batch(self._h, _dptr(c), int(c.shape[0]), int(c.shape[1] - 1)),
+               "dbp_plan_set_coeff_batch")
+        self.n_sets = int(c.shape[0])
+
+    def run_host_coeff_batch(self, h_in: np.ndarray, h_out: np.ndarray, n_total: int):
+        """h_in (2, n) complex64, h_out (n_sets, 2, n) complex64, both C-contiguous."""
+        if h_in.dtype != np.complex64 or h_out.dtype != np.complex64:
+            raise ValueError("host buffers must be complex64")
+        if not (h_in.flags.c_contiguous and h_out.flags.c_contiguous):
+            raise ValueError("host buffers must be C-contiguous")
+        if h_in.size != 2 * n_total or h_out.size != self.n_sets * 2 * n_total:
+            raise ValueError("host buffer sizes do not match (2, n) / (n_sets, 2, n)")
+        _check(self._lib.dbp_run_host_coeff_batch(self._h, h_in.ctypes.data, h_out.ctypes.data, int(n_total)),
+               "dbp_run_host_coeff_batch")
 
     def synchronize(self):
         _check(self._lib.dbp_plan_synchronize(self._h), "dbp_plan_synchronize")

@@ -365,12 +365,12 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
 // any nc: taps in chunks of four (same summation order as fir8_fixed, so
 // every path gives identical bits for a given coefficient set)
 __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
-                                             int p0, int pw, float a, float g, const KernelParams& kp) {
+                                             int p0, int pw, float a, float g, const KernelParams& kp,
+                                             const float* __restrict__ cptr, float c0) {
   float f[8];
   {
     const float4 u = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw));
     const float4 w = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw + 4));
-    const float c0 = kp.c[0];
     f[0] = c0 * u.x; f[1] = c0 * u.y; f[2] = c0 * u.z; f[3] = c0 * u.w;
     f[4] = c0 * w.x; f[5] = c0 * w.y; f[6] = c0 * w.z; f[7] = c0 * w.w;
   }
@@ -389,7 +389,7 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
     }
 #pragma unroll
     for (int d = 0; d < 4; ++d) {
-      const float ci = __ldg(kp.coeff + i0 + d);
+      const float ci = __ldg(cptr + i0 + d);
 #pragma unroll
       for (int o = 0; o < 8; ++o) f[o] = fmaf(ci, l[o + 3 - d] + r[o + 1 + d], f[o]);
     }
@@ -399,7 +399,9 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
 
 template <int LOGN>
 __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const KernelParams& kp,
-                                       int step_idx, int t, int pol) {
+                                       int step_idx, int t, int pol, const float* __restrict__ cptr) {
+  // per-item coefficient sets (training batches) read from global memory
+  const float c0 = kp.coeff_stride ? __ldg(cptr) : kp.c[0];
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
   const float2 sg = __ldg(kp.steps + step_idx);  // (a_j, g_j)
@@ -416,10 +418,10 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
     float2 fac[8];
     if (kp.precise_sincos) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<true>(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
+      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<true>(sg.x, sg.y, c0 * (pol ? inten[8 + i] : inten[i]));
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<false>(sg.x, sg.y, kp.c[0] * (pol ? inten[8 + i] : inten[i]));
+      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<false>(sg.x, sg.y, c0 * (pol ? inten[8 + i] : inten[i]));
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -464,13 +466,13 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
     }
     sh.after_write();
     const int p0 = 16 * t + 8 * pol;
-    switch (kp.nc) {
+    switch (kp.coeff_stride ? -1 : kp.nc) {
       case 1: fir8_fixed<1>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
       case 9: fir8_fixed<9>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
       case 17: fir8_fixed<17>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
       case 32: fir8_fixed<32>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
       case 33: fir8_fixed<33>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
-      default: fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp); break;
+      default: fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp, cptr, c0); break;
     }
     __syncthreads();
     if constexpr (T >= 16) {
@@ -512,6 +514,7 @@ dbp_block_kernel(const KernelParams kp) {
     b = kp.block_begin + (blk - item * kp.blocks_per_item);
   }
 
+  const float* cptr = kp.coeff + (kp.coeff_stride ? item * kp.coeff_stride : 0);
   float2 v[16];
   const long long s0 = b * kp.step - kp.lead;  // global index of block sample 0
   if (active) {
@@ -567,7 +570,7 @@ dbp_block_kernel(const KernelParams kp) {
     if (is_conv) {
       conv_pass<LOGN, 0>(v, sh, tab, kp.twiddle, t);
     } else {
-      rotate<LOGN>(v, sh, kp, sidx, t, pol);
+      rotate<LOGN>(v, sh, kp, sidx, t, pol, cptr);
     }
   }
 

@@ -93,6 +93,10 @@ struct dbp_plan {
   bool have_full = false, have_half = false, have_steps = false;
   int program = dbp::kFFE, arrangement = dbp::kSymmetric, n_steps = 0, nc = 0;
   float c[dbp::kMaxSideCoeffs + 4] = {};
+  // per-item coefficient sets (dbp_plan_set_coeff_batch)
+  float* d_coeff_batch = nullptr;
+  int batch_sets = 0, batch_nc = 0, batch_stride = 0;
+  size_t batch_cap = 0;
   // host-run staging
   size_t staging_budget = size_t(1) << 30;
   cudaStream_t streams[2] = {nullptr, nullptr};
@@ -253,6 +257,7 @@ int dbp_plan_destroy(dbp_plan* p) {
   cudaFree(p->d_tw);
   cudaFree(p->d_steps);
   cudaFree(p->d_coeff);
+  cudaFree(p->d_coeff_batch);
   delete p;
   return DBP_OK;
 }
@@ -539,6 +544,90 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
     }
   }
   for (int s = 0; s < 2; ++s) DBP_CUDA(cudaStreamSynchronize(p->streams[s]), "cudaStreamSynchronize");
+  return DBP_OK;
+}
+
+int dbp_plan_set_coeff_batch(dbp_plan* p, const double* coeffs, int n_sets, int n_coeffs) {
+  if (!p) return fail(DBP_EINVAL, "null plan");
+  if (!coeffs || n_sets < 1) return fail(DBP_EINVAL, "need at least one coefficient set");
+  if (n_coeffs < 0 || n_coeffs > DBP_MAX_SIDE_COEFFS)
+    return fail(DBP_EINVAL, "n_coeffs must be in [0, " + std::to_string(DBP_MAX_SIDE_COEFFS) + "]");
+  if (p->N <= 2 * n_coeffs) return fail(DBP_EINVAL, "block length too short for the coefficient memory");
+  DeviceGuard g(p->device);
+  const int stride = (n_coeffs + 1 + 3 + 3) & ~3;  // c_0..c_nc + 4-tap chunk padding
+  std::vector<float> h((size_t)n_sets * stride, 0.0f);
+  for (int s = 0; s < n_sets; ++s)
+    for (int i = 0; i <= n_coeffs; ++i) {
+      const double v = coeffs[(size_t)s * (n_coeffs + 1) + i];
+      if (!std::isfinite(v)) return fail(DBP_EINVAL, "coefficients must be finite");
+      h[(size_t)s * stride + i] = (float)v;
+    }
+  const size_t bytes = h.size() * sizeof(float);
+  if (bytes > p->batch_cap) {
+    cudaFree(p->d_coeff_batch);
+    p->d_coeff_batch = nullptr;
+    DBP_CUDA(cudaMalloc(&p->d_coeff_batch, bytes), "cudaMalloc(coeff batch)");
+    p->batch_cap = bytes;
+  }
+  DBP_CUDA(cudaMemcpy(p->d_coeff_batch, h.data(), bytes, cudaMemcpyHostToDevice), "cudaMemcpy(coeff batch)");
+  p->batch_sets = n_sets;
+  p->batch_nc = n_coeffs;
+  p->batch_stride = stride;
+  return DBP_OK;
+}
+
+int dbp_run_coeff_batch(dbp_plan* p, const void* d_in, void* d_out, int64_t n_total,
+                        int64_t block_begin, int64_t block_end, void* stream) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (p->batch_sets < 1) return fail(DBP_ESTATE, "dbp_plan_set_coeff_batch has not been called");
+  if (p->program != dbp::kESSFM && p->program != dbp::kRotateOnly)
+    return fail(DBP_EINVAL, "coefficient batches need an essfm (or rotation) program");
+  rc = check_range(p, n_total, p->batch_sets, block_begin, block_end);
+  if (rc) return rc;
+  if (!d_in || !d_out) return fail(DBP_EINVAL, "null device buffer");
+  DeviceGuard g(p->device);
+  dbp::KernelParams kp;
+  base_params(p, kp);
+  kp.nc = p->batch_nc;
+  kp.fir_pad = (p->batch_nc + 3) & ~3;
+  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad);
+  kp.coeff = p->d_coeff_batch;
+  kp.coeff_stride = p->batch_stride;
+  kp.in = static_cast<const float2*>(d_in);
+  kp.out = static_cast<float2*>(d_out);
+  kp.n_total = n_total;
+  kp.in_pol_stride = n_total;
+  kp.in_item_stride = 0;  // every coefficient set reads the same waveform
+  kp.out_pol_stride = n_total;
+  kp.out_item_stride = 2 * n_total;
+  kp.block_begin = block_begin;
+  kp.blocks_per_item = block_end - block_begin;
+  kp.total_blocks = kp.blocks_per_item * p->batch_sets;
+  kp.cyclic = 1;
+  kp.step = p->step;
+  kp.lead = p->lead;
+  return launch(p, kp, static_cast<cudaStream_t>(stream));
+}
+
+int dbp_run_host_coeff_batch(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (p->batch_sets < 1) return fail(DBP_ESTATE, "dbp_plan_set_coeff_batch has not been called");
+  if (!h_in || !h_out) return fail(DBP_EINVAL, "null host buffer");
+  if (n_total < 1) return fail(DBP_EINVAL, "signal must contain at least one sample");
+  DeviceGuard g(p->device);
+  const size_t in_bytes = (size_t)n_total * 2 * sizeof(float2);
+  const size_t out_bytes = in_bytes * p->batch_sets;
+  rc = ensure_staging(p, out_bytes > in_bytes ? out_bytes : in_bytes);
+  if (rc) return rc;
+  cudaStream_t s = p->streams[0];
+  DBP_CUDA(cudaMemcpyAsync(p->d_stage[0][0], h_in, in_bytes, cudaMemcpyHostToDevice, s), "H2D");
+  const int64_t nb = (n_total + p->step - 1) / p->step;
+  rc = dbp_run_coeff_batch(p, p->d_stage[0][0], p->d_stage[0][1], n_total, 0, nb, s);
+  if (rc) return rc;
+  DBP_CUDA(cudaMemcpyAsync(h_out, p->d_stage[0][1], out_bytes, cudaMemcpyDeviceToHost, s), "D2H");
+  DBP_CUDA(cudaStreamSynchronize(s), "cudaStreamSynchronize");
   return DBP_OK;
 }
 

@@ -40,6 +40,7 @@ struct KernelParams {
   const float2* twiddle;      // per-pass twiddle tables
   const float2* steps;        // per step (a_j, g_j): rotation exp(+j a_j F), gain g_j
   const float* coeff;         // c_0..c_nc zero padded to nc + 4 (generic FIR path)
+  int coeff_stride;           // 0: shared coefficients; > 0: item i uses coeff + i * stride
   float c[kMaxSideCoeffs + 4];  // c_0..c_nc, zero padded
 };
 

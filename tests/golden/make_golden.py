@@ -205,6 +205,19 @@ def main():
                           n_coeffs=17 if cfg.algorithm == "essfm" else None, signal="link",
                           picks=list(picks)))
 
+    # ---- coefficient training (train.py:86-188) on the link waveform ----
+    from fiberdbp import TrainConfig, optimize_coefficients
+    tcfg = TrainConfig(n_coeffs=4, target_steps_per_span=2, train_samples=8192, max_iterations=6)
+    dcfg = DbpConfig("essfm", OverlapPlan(2048, 700), link, num_steps=1,
+                     coeffs=EssfmCoefficients.identity(4), arrangement="symmetric")
+    t1 = time.time()
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        res = optimize_coefficients(sig, dcfg, tcfg)
+    print(f"training {time.time() - t1:.1f}s iterations {res.iterations} mse {res.initial_mse:.4e} -> {res.final_mse:.4e}")
+    arrays["train_c"] = res.coefficients.c
+    arrays["train_mse"] = np.array([res.initial_mse, res.final_mse, res.iterations, float(res.converged)])
+
     np.savez_compressed(OUT, **arrays)
     MANIFEST.write_text(json.dumps(dict(
         generator="tests/golden/make_golden.py", reference="fiberdbp " + fiberdbp.__version__,

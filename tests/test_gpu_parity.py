@@ -277,3 +277,37 @@ def test_config2_ssfm20_power_sweep(power_dbm):
     got = _run(rx, cfg)[0]
     want = dbp_port.backpropagate_arrays(rx.astype(np.complex128), 56e9, port_config(cfg))
     assert dbp_port.per_block_rel_l2(got, want, 2048, 700).max() <= TOL_BLOCK
+
+
+def test_coefficient_training_matches_reference(golden):
+    # the reference's Gauss-Newton fit (train.py:86-188) with every
+    # coefficient batch evaluated in one launch; float32 central differences
+    link = quiet_link(40, pb.FiberParams(waveforms.d_to_beta2(17.0), 1.3, 0.2, 80.0))
+    rx = golden["link_rx"]
+    sig = pb.DualPolSignal(rx[0], rx[1], 56e9)
+    tcfg = pb.TrainConfig(n_coeffs=4, target_steps_per_span=2, train_samples=8192, max_iterations=6)
+    dcfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), link, coeffs=pb.EssfmCoefficients.identity(4))
+    res = pb.optimize_coefficients(sig, dcfg, tcfg)
+    ref_initial, ref_final, ref_iters, _ = golden["train_mse"]
+    print("gpu", res.initial_mse, res.final_mse, res.iterations, res.coefficients.c)
+    print("ref", ref_initial, ref_final, ref_iters, golden["train_c"])
+    assert abs(res.initial_mse - ref_initial) <= 1e-4 * ref_initial
+    assert res.final_mse <= ref_final * 1.01
+    np.testing.assert_allclose(res.coefficients.c, golden["train_c"], rtol=0, atol=2e-2)
+
+
+def test_coeff_batch_items_match_single_runs(rng):
+    # per-item coefficient sets (one launch) == separate ESSFM runs with each set
+    link = quiet_link(8, STD)
+    plan = pb.OverlapPlan(1024, 256)
+    x = (0.03 * (rng.normal(size=(2, 6000)) + 1j * rng.normal(size=(2, 6000)))).astype(np.complex64)
+    sets = np.stack([waveforms.gaussian_coeffs(5, w) for w in (1.0, 2.0, 3.5)])
+    eng = pb.get_engine(pb.DbpConfig("essfm", plan, link, num_steps=2,
+                                     coeffs=pb.EssfmCoefficients.identity(5)), 56e9, 0)
+    out = np.empty((3, 2, 6000), dtype=np.complex64)
+    with eng.native.lock:
+        eng.native.set_coeff_batch(sets)
+        eng.native.run_host_coeff_batch(np.ascontiguousarray(x), out, 6000)
+    for i in range(3):
+        single = _run(x, pb.DbpConfig("essfm", plan, link, num_steps=2, coeffs=pb.EssfmCoefficients(sets[i])))[0]
+        assert rel_l2(out[i], single) < 1e-6

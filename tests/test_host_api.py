@@ -96,3 +96,17 @@ def test_effective_length():
     assert pb.effective_length(0.0, 5.0) == 5.0
     assert pb.effective_length(1e-12, 1.0) == pytest.approx(1.0)
     assert pb.scale_to_power(pb.DualPolSignal([1, 1], [1, 1], 1.0), 0.0).x[0] == pytest.approx(math.sqrt(1e-3 / 2))
+
+
+def test_train_config_validation_and_coefficient_files(tmp_path):   # test_train.py
+    with pytest.raises(ValueError):
+        pb.TrainConfig(n_coeffs=-1)
+    with pytest.raises(ValueError):
+        pb.TrainConfig(n_coeffs=32, train_samples=100)
+    c = pb.EssfmCoefficients(np.array([0.9, 0.05, -0.01]))
+    pb.save_coefficients(tmp_path / "c.txt", c)
+    np.testing.assert_array_equal(pb.load_coefficients(tmp_path / "c.txt").c, c.c)
+    (tmp_path / "bad.txt").write_text("3\n1.0\n")
+    with pytest.raises(ValueError):
+        pb.load_coefficients(tmp_path / "bad.txt")
+    assert pb.mse(np.ones((2, 4)), np.ones((2, 4))) == 0.0
