@@ -37,9 +37,17 @@
 
 namespace dbp {
 
-#ifndef DBP_THREADS_PER_SM
-#define DBP_THREADS_PER_SM 768
+// Resident threads per SM targeted by __launch_bounds__ (sets the register
+// budget 65536 / target).  Tuned per block length on B200 (tools/ab_sweep.sh):
+// N <= 1024: 512 (2 x 256-thread CTAs, 128 regs), N = 2048: 768 (3 CTAs,
+// 80 regs), N >= 4096: 1024 (64 regs).  -DDBP_THREADS_PER_SM overrides.
+__host__ __device__ constexpr int threads_per_sm(int logn) {
+#ifdef DBP_THREADS_PER_SM
+  return DBP_THREADS_PER_SM + 0 * logn;
+#else
+  return logn <= 10 ? 512 : (logn == 11 ? 768 : 1024);
 #endif
+}
 #ifndef DBP_CTA_POSITIONS
 #define DBP_CTA_POSITIONS 128
 #endif
@@ -57,7 +65,7 @@ struct Geo {
   static constexpr int G0 = 16 / R0;                     // first-pass groups per thread
   static constexpr int BPC = T >= DBP_CTA_POSITIONS ? 1 : DBP_CTA_POSITIONS / T;
   static constexpr int THREADS = 2 * T * BPC;
-  static constexpr int MIN_CTAS = DBP_THREADS_PER_SM / THREADS > 0 ? DBP_THREADS_PER_SM / THREADS : 1;
+  static constexpr int MIN_CTAS = threads_per_sm(LOGN) / THREADS > 0 ? threads_per_sm(LOGN) / THREADS : 1;
   // two shared buffers per slice (one barrier per exchange instead of two)
   // while both fit next to the L1-resident tables
   static constexpr bool DB = DBP_DOUBLE_BUFFER && (2 * 16 * (N + N / 16) * BPC <= 80 * 1024);

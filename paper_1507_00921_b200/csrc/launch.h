@@ -3,11 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#ifdef DBP_KERNEL_V1
-#include "dbp_block_kernel_v1.cuh"
-#else
 #include "dbp_block_kernel.cuh"
-#endif
 
 namespace dbp {
 
@@ -16,7 +12,7 @@ constexpr int kMaxLogN = 13;  // N = 8192
 
 struct LaunchShape {
   int threads_x;  // threads per CTA along x
-  int threads_y;  // along y (v1: one row per block slice)
+  int threads_y;  // along y
   int slices;     // block slices per CTA
   int buffers;    // shared buffers per slice (2 = double-buffered exchanges)
 };
@@ -27,11 +23,7 @@ cudaError_t launch_block_kernel(const KernelParams& kp, long long n_ctas, size_t
 
 template <int LOGN>
 LaunchShape launch_shape() {
-#ifdef DBP_KERNEL_V1
-  return LaunchShape{Geo<LOGN>::T, Geo<LOGN>::BPC, Geo<LOGN>::BPC, 1};
-#else
   return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::DB ? 2 : 1};
-#endif
 }
 
 }  // namespace dbp

@@ -1,8 +1,8 @@
 """Executable numpy model of the fused kernel's FFT data movement.
 
-A line-by-line restatement of ``conv_pass`` / ``swz`` in
-paper_1507_00921_b200/csrc/dbp_block_kernel.cuh (thread registers, shared
-memory exchange addresses, twiddle table layout of dbp_capi.cu
+A line-by-line restatement of ``conv_pass`` / ``side_index`` /
+``xchg_index`` in paper_1507_00921_b200/csrc/dbp_block_kernel.cuh (thread
+registers, shared-memory exchange addresses, the twiddle table layout of
 ``make_twiddles``), evaluated in complex128.  The CPU tests use it to prove
 the index algebra (pass decomposition, digit-reversed spectrum order, swizzle
 bijectivity and bank-conflict freedom) before any GPU run.
@@ -11,122 +11,6 @@ bijectivity and bank-conflict freedom) before any GPU run.
 from __future__ import annotations
 
 import numpy as np
-
-
-class Geo:
-    def __init__(self, logn: int):
-        self.logn = logn
-        self.N = 1 << logn
-        self.T = self.N // 16
-        self.NP = (logn + 3) // 4
-        self.RLAST = 1 << (logn - 4 * (self.NP - 1))
-
-    def radix(self, p):
-        return 16 if p < self.NP - 1 else self.RLAST
-
-    def log_s(self, p):
-        return self.logn - 4 * (p + 1) if p < self.NP - 1 else 0
-
-    def tw_offset(self, p):
-        return sum(15 << self.log_s(q) for q in range(p))
-
-
-def swz(g: Geo, p: int, i: int) -> int:
-    ls, ls1 = g.log_s(p), g.log_s(p + 1)
-    if ls1 >= 3:
-        return i
-    return i ^ (((i >> ls) << ls1) & 7)
-
-
-def twiddles(g: Geo) -> np.ndarray:
-    out = []
-    for p in range(g.NP - 1):
-        s = 1 << g.log_s(p)
-        period = 16 * s
-        for k in range(1, 16):
-            for ns in range(s):
-                m = (ns * k) % period
-                out.append(np.exp(-2j * np.pi * m / period))
-    return np.asarray(out if out else [1.0 + 0j])
-
-
-def dft(v: np.ndarray, inverse: bool) -> np.ndarray:
-    return np.fft.ifft(v) * v.size if inverse else np.fft.fft(v)
-
-
-def conv_model(block: np.ndarray, table: np.ndarray, logn: int, trace=None) -> np.ndarray:
-    """Emulate conv_pass<LOGN,0> on one polarisation; table is natural-order H (1/N folded)."""
-    g = Geo(logn)
-    N, T = g.N, g.T
-    tw = twiddles(g)
-    regs = np.zeros((T, 16), dtype=np.complex128)
-    for t in range(T):
-        for n in range(16):
-            regs[t, n] = block[n * T + t]
-    sm = np.full(N, np.nan + 0j)
-
-    def rec(p):
-        nonlocal regs, sm
-        if p < g.NP - 1:
-            ls = g.log_s(p)
-            S = 1 << ls
-            for t in range(T):
-                regs[t] = dft(regs[t], False)
-                ns = t & (S - 1)
-                for k in range(1, 16):
-                    regs[t, k] *= tw[g.tw_offset(p) + ns + (k - 1) * S]
-            r1, ls1 = g.radix(p + 1), g.log_s(p + 1)
-            grp = 16 // r1
-            sm[:] = np.nan
-            for t in range(T):
-                for k in range(16):
-                    a = swz(g, p, t + k * (N // 16))
-                    if trace is not None:
-                        trace.append(("w", p, t, a))
-                    sm[a] = regs[t, k]
-            for t in range(T):
-                for q in range(grp):
-                    gg = t + T * q
-                    base = ((gg >> ls1) << ls) + (gg & ((1 << ls1) - 1))
-                    for e in range(r1):
-                        a = swz(g, p, base + (e << ls1))
-                        if trace is not None:
-                            trace.append(("r", p, t, a))
-                        regs[t, q * r1 + e] = sm[a]
-            rec(p + 1)
-            sm[:] = np.nan
-            for t in range(T):
-                for q in range(grp):
-                    gg = t + T * q
-                    base = ((gg >> ls1) << ls) + (gg & ((1 << ls1) - 1))
-                    for e in range(r1):
-                        sm[swz(g, p, base + (e << ls1))] = regs[t, q * r1 + e]
-            for t in range(T):
-                for k in range(16):
-                    regs[t, k] = sm[swz(g, p, t + k * (N // 16))]
-            for t in range(T):
-                ns = t & (S - 1)
-                for k in range(1, 16):
-                    regs[t, k] *= np.conj(tw[g.tw_offset(p) + ns + (k - 1) * S])
-                regs[t] = dft(regs[t], True)
-        else:
-            rl = g.RLAST
-            grp = 16 // rl
-            ll = N // rl
-            for t in range(T):
-                for q in range(grp):
-                    seg = slice(q * rl, (q + 1) * rl)
-                    regs[t, seg] = dft(regs[t, seg], False)
-                    for e in range(rl):
-                        regs[t, q * rl + e] *= table[(t + T * q) + ll * e]
-                    regs[t, seg] = dft(regs[t, seg], True)
-
-    rec(0)
-    out = np.zeros(N, dtype=np.complex128)
-    for t in range(T):
-        for n in range(16):
-            out[n * T + t] = regs[t, n]
-    return out
 
 
 def fir_phys(u: int) -> int:

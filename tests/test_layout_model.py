@@ -3,45 +3,7 @@
 import numpy as np
 import pytest
 
-from .layout_model import Geo, conv_model, fir_phys, swz
-
-
-@pytest.mark.parametrize("logn", list(range(4, 14)))
-def test_conv_model_equals_fft_filter(logn):
-    n = 1 << logn
-    if n > 4096:
-        pytest.skip("pure-python model too slow above 4096")
-    rng = np.random.default_rng(logn)
-    x = rng.normal(size=n) + 1j * rng.normal(size=n)
-    h = np.exp(1j * rng.uniform(-np.pi, np.pi, n))
-    got = conv_model(x, h / n, logn)
-    want = np.fft.ifft(np.fft.fft(x) * h)
-    np.testing.assert_allclose(got, want, rtol=0, atol=1e-11 * np.max(np.abs(want)))
-
-
-@pytest.mark.parametrize("logn", list(range(4, 14)))
-def test_swizzle_is_bijective_and_conflict_free(logn):
-    g = Geo(logn)
-    n = g.N
-    for p in range(g.NP - 1):
-        img = sorted(swz(g, p, i) for i in range(n))
-        assert img == list(range(n))
-        # writers: lanes t (8 per 16-byte phase) write t + k N/16; readers: pass p+1 layout
-        r1, ls, ls1 = g.radix(p + 1), g.log_s(p), g.log_s(p + 1)
-        grp = 16 // r1
-        for phase in range(0, g.T, 8):
-            lanes = range(phase, min(phase + 8, g.T))
-            for k in range(16):
-                banks = [swz(g, p, t + k * (n // 16)) % 8 for t in lanes]
-                assert len(set(banks)) == len(banks), ("write", p, k)
-            for q in range(grp):
-                for e in range(r1):
-                    banks = []
-                    for t in lanes:
-                        gg = t + g.T * q
-                        base = ((gg >> ls1) << ls) + (gg & ((1 << ls1) - 1))
-                        banks.append(swz(g, p, base + (e << ls1)) % 8)
-                    assert len(set(banks)) == len(banks), ("read", p, q, e)
+from .layout_model import fir_phys
 
 
 def test_fir_padding_conflict_free():
@@ -49,14 +11,6 @@ def test_fir_padding_conflict_free():
     for m in range(0, 40, 4):
         groups = [(fir_phys(16 * t + m) // 4) % 8 for t in range(8)]
         assert len(set(groups)) == 8
-
-
-def test_twiddle_table_size_matches_kernel_constant():
-    from .layout_model import twiddles
-    for logn in range(4, 14):
-        g = Geo(logn)
-        if g.NP > 1:
-            assert twiddles(g).size == g.tw_offset(g.NP - 1)
 
 
 # ---- v2 (default) kernel: one polarisation per thread, radix R0 first ----

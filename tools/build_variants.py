@@ -7,8 +7,8 @@ from paper_1507_00921_b200 import build as B
 ROOT = Path(__file__).resolve().parent.parent / "build" / "variants"
 VARIANTS = {
     "base": [],
-    "v1": ["-DDBP_KERNEL_V1"],
     "v2_512": ["-DDBP_THREADS_PER_SM=512"],
+    "tps640": ["-DDBP_THREADS_PER_SM=640"],
     "v2_1024": ["-DDBP_THREADS_PER_SM=1024"],
     "v2_cta64": ["-DDBP_CTA_POSITIONS=64", "-DDBP_THREADS_PER_SM=768"],
     "single": ["-DDBP_DOUBLE_BUFFER=0"],
