@@ -1,0 +1,121 @@
+"""BASELINE configs[4]: one continuous 2^30-sample dual-pol stream, sharded by block range.
+
+    python tools/stream_bench.py [--log2-samples 30] [--steps 5]
+    torchrun --nproc-per-node G tools/stream_bench.py ...
+
+The stream (28 GBd, 2 sps, 0 dBm complex Gaussian stand-in) is defined tile
+by tile (2^20 samples, torch generator seeded with the tile index), so every
+GPU count sees the identical stream.  Rank g owns blocks [b_g, b_{g+1}),
+b_g = floor(g nb / G) (multiples of N - M), builds its halo'd span
+[b_g step - M/2, b_{g+1} step - M/2 + M) on its own device (cyclic wrap at
+the stream ends) and runs ``dbp_run_chunk`` -- no collective on the data
+path.  Prints one JSON line (rank 0): whole-stream Gsamples/s (max over
+ranks), per-chunk latency, and a per-rank output checksum that must be
+identical to the 1-GPU run's for the same sample ranges.
+"""
+
+import argparse
+import hashlib
+import json
+import math
+import os
+import sys
+import warnings
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+TILE = 1 << 20
+
+
+def tile_values(torch, idx, dev, amp):
+    g = torch.Generator(device=dev)
+    g.manual_seed(10_000 + idx)
+    return torch.randn((2, TILE, 2), generator=g, device=dev) * amp
+
+
+def build_span(torch, lo, hi, n, dev, amp):
+    """Samples [lo, hi) of the circular stream as a (2, hi-lo, 2) float32 tensor."""
+    out = torch.empty((2, hi - lo, 2), device=dev)
+    pos = lo
+    while pos < hi:
+        g = pos % n
+        tile, off = divmod(g, TILE)
+        take = min(hi - pos, TILE - off, n - g)
+        out[:, pos - lo:pos - lo + take] = tile_values(torch, tile, dev, amp)[:, off:off + take]
+        pos += take
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--log2-samples", type=int, default=30)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    a = ap.parse_args()
+
+    import torch
+    import torch.distributed as dist
+
+    import bench
+    import paper_1507_00921_b200 as pb
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = f"cuda:{local}"
+    warnings.simplefilter("ignore")
+    args = bench.parse_args([])
+    cfg = bench.make_cfg(args)
+    eng = pb.get_engine(cfg, bench.SAMPLE_RATE, local)
+    n = 1 << a.log2_samples
+    nb = eng.num_blocks(n)
+    b0, b1 = pb.shard_blocks(nb, world)[rank]
+    lo, hi = cfg.plan.input_span(b0, b1)
+    olo, ohi = cfg.plan.output_span(b0, b1, n)
+    amp = math.sqrt(1e-3 / 4.0)
+    span = build_span(torch, lo, hi, n, dev, amp)
+    out = torch.empty((2, ohi - olo, 2), device=dev)
+    stream = torch.cuda.Stream()
+
+    def step():
+        eng.native.run_chunk(span.data_ptr(), out.data_ptr(), n, 1, b0, b1, hi - lo, ohi - olo, stream.cuda_stream)
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(a.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    digest = hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()[:16]
+    digests = [None] * world
+    if world > 1:
+        dist.all_gather_object(digests, (rank, olo, ohi, digest))
+    else:
+        digests = [(0, olo, ohi, digest)]
+    if rank == 0:
+        ms_max = float(t.item())
+        print(json.dumps({
+            "metric": "ESSFM 1-step DBP Gsamples/s (dual-pol), configs[4] stream", "unit": "Gsamples/s",
+            "value": n / (ms_max * 1e-3) / 1e9, "n_gpus": world, "stream_samples": n, "blocks": nb,
+            "chunk_latency_ms": ms_max, "halo_samples": [cfg.plan.lead, cfg.plan.overlap - cfg.plan.lead],
+            "shards": [list(d) for d in digests], "device_resident": True,
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
