@@ -116,26 +116,48 @@ inline int slice_floats(int n, int pw) {
   return (v + 3) & ~3;
 }
 
-// Final-boundary layout: one pad element per 16 (reads of the last pass
-// gather 16 consecutive elements per lane, i.e. a 128-byte lane stride,
-// which the pad turns into 136 bytes -> 16 distinct banks).  Linear in the
-// lane's base, so every access is base + immediate.
+// Exchange layouts.
+//  * NP == 2 (N <= 256): the one exchange feeds the last pass, whose lanes
+//    gather 16 consecutive elements (128-byte lane stride): one pad element
+//    per 16 ("pad16") makes it conflict free.
+//  * NP >= 3: the exchange INTO pass NP-2 uses one pad of 16 elements per
+//    256 ("pad256"), so half-warp h gathers exactly [272 h, 272 h + 256); the
+//    exchange into the last pass then stays inside half-warp h's own
+//    272-element tile (see conv_pass) and needs only __syncwarp.
+//  * all other exchanges: plain.
+// Every form is linear in the register index, so accesses are base + immediates.
 __host__ __device__ constexpr int pad16(int i) { return i + (i >> 4); }
+__host__ __device__ constexpr int pad256(int i) { return i + ((i >> 8) << 4); }
 
 template <int LOGN, int P>
 __device__ __forceinline__ int xchg_index(int i) {
-  if constexpr (P + 1 == Geo<LOGN>::NP - 1) return pad16(i);
+  constexpr int NP = Geo<LOGN>::NP;
+  if constexpr (NP == 2 && P == 0) return pad16(i);
+  else if constexpr (NP >= 3 && P + 1 == NP - 2) return pad256(i);
   else return i;
 }
 
-// plane index of position t + T m; linear in m (base + m * stride) whenever
-// T % 16 == 0, so the 16 accesses are one base plus immediates
+// plane index of position t + T m (the strided side of exchange P)
 template <int LOGN, int P>
 __device__ __forceinline__ int side_index(int t, int m) {
-  constexpr int T = Geo<LOGN>::T;
-  if constexpr (P + 1 != Geo<LOGN>::NP - 1) return t + T * m;
-  else if constexpr (T % 16 == 0) return pad16(t) + m * (T + T / 16);
-  else return pad16(t + T * m);
+  constexpr int T = Geo<LOGN>::T, NP = Geo<LOGN>::NP;
+  if constexpr (NP == 2 && P == 0) {
+    if constexpr (T % 16 == 0) return pad16(t) + m * (T + T / 16);
+    else return pad16(t + T * m);
+  } else if constexpr (NP >= 3 && P + 1 == NP - 2) {
+    // t < T: for T <= 256, (t + T m) >> 8 == (T m) >> 8 (no carry); else linear
+    if constexpr (T <= 256) return t + T * m + (((T * m) >> 8) << 4);
+    else return pad256(t) + m * (T + T / 16);
+  } else {
+    return t + T * m;
+  }
+}
+
+// Bin index held by register e of thread t after the last forward pass
+// (host-side permutation of the dispersion tables, read as tab[t + T e]).
+__host__ __device__ constexpr int last_pass_bin(int logn, int t, int e) {
+  const int n = 1 << logn, tt = n / 16, np = (logn + 3) / 4;
+  return np >= 3 ? (t >> 4) + (n / 256) * (t & 15) + (n / 16) * e : t + tt * e;
 }
 
 // Shared-memory phases.  Single-buffered: barrier before and after every
@@ -237,6 +259,46 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
+  } else if constexpr (NP >= 3 && P == NP - 2) {
+    // second-to-last pass (S = 16) + last pass, joined by a half-warp-local
+    // 16 x 16 transpose: half-warp h = t >> 4 owns sub-problem h, lane
+    // ns = t & 15 holds its register k; the last pass's group (h, k) goes to
+    // lane k of the same half-warp.  The tile [272 h, 272 h + 272) is the
+    // region this half-warp alone read in the previous (pad256) exchange.
+    const float2* twp = tw + G::tw_offset(P) + (t & 15);
+    dft<16, false>(v);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) v[k] = c_mul(v[k], ldg_table(twp + (k - 1) * 16));
+    {
+      float2* tile = sh.plane() + 272 * (t >> 4);
+      const int l = t & 15;
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) tile[l + 17 * k] = v[k];
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = tile[17 * l + e];
+    }
+    // last pass: group (h, l), bins last_pass_bin(t, e) (table pre-permuted)
+    dft<16, false>(v);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(tab + t + T * e));
+    dft<16, true>(v);
+    t = opaque(t);
+    {
+      float2* tile = sh.plane() + 272 * (t >> 4);
+      const int l = t & 15;
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < 16; ++e) tile[17 * l + e] = v[e];
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] = tile[l + 17 * k];
+    }
+    twp = tw + G::tw_offset(P) + (t & 15);
+#pragma unroll
+    for (int k = 1; k < 16; ++k) v[k] = c_mulc(v[k], ldg_table(twp + (k - 1) * 16));
+    dft<16, true>(v);
   } else if constexpr (P < NP - 1) {
     // middle radix-16 pass: group g = t, ns = t mod S_P
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);

@@ -274,20 +274,28 @@ int dbp_plan_set_linear(dbp_plan* p, const double* kernel, const double* half_ke
   if (!kernel) return fail(DBP_EINVAL, "null kernel");
   DeviceGuard g(p->device);
   const double inv_n = 1.0 / (double)p->N;
+  const int T = p->N / 16;
+  // stored in the kernel's register order: entry t + T e holds the bin that
+  // register e of thread t carries after the last forward FFT pass
+  std::vector<int> bin(p->N);
+  for (int t = 0; t < T; ++t)
+    for (int e = 0; e < 16; ++e) bin[t + T * e] = dbp::last_pass_bin(p->logn, t, e);
   std::vector<float2> h(p->N);
-  for (int k = 0; k < p->N; ++k) {
+  for (int j = 0; j < p->N; ++j) {
+    const int k = bin[j];
     const double re = kernel[2 * k], im = kernel[2 * k + 1];
     if (!std::isfinite(re) || !std::isfinite(im)) return fail(DBP_EINVAL, "kernel must be finite");
-    h[k] = make_float2((float)(re * inv_n), (float)(im * inv_n));
+    h[j] = make_float2((float)(re * inv_n), (float)(im * inv_n));
   }
   int rc = upload(&p->d_full, h);
   if (rc != DBP_OK) return rc;
   p->have_full = true;
   if (half_kernel) {
-    for (int k = 0; k < p->N; ++k) {
+    for (int j = 0; j < p->N; ++j) {
+      const int k = bin[j];
       const double re = half_kernel[2 * k], im = half_kernel[2 * k + 1];
       if (!std::isfinite(re) || !std::isfinite(im)) return fail(DBP_EINVAL, "half kernel must be finite");
-      h[k] = make_float2((float)(re * inv_n), (float)(im * inv_n));
+      h[j] = make_float2((float)(re * inv_n), (float)(im * inv_n));
     }
     rc = upload(&p->d_half, h);
     if (rc != DBP_OK) return rc;

@@ -57,16 +57,31 @@ def twiddles2(g: Geo2) -> np.ndarray:
 
 
 def xchg2(g: Geo2, p: int, i: int) -> int:
-    if p + 1 == g.NP - 1:
-        return i + (i >> 4)          # pad16: one pad element per 16
+    """Gather-side plane index of exchange p (kernel xchg_index)."""
+    if g.NP == 2 and p == 0:
+        return i + (i >> 4)                      # pad16
+    if g.NP >= 3 and p + 1 == g.NP - 2:
+        return i + ((i >> 8) << 4)               # pad256
     return i
 
 
+def side2(g: Geo2, p: int, t: int, m: int) -> int:
+    """Strided-side plane index of exchange p (kernel side_index)."""
+    return xchg2(g, p, t + g.T * m)
+
+
+def last_pass_bin(g: Geo2, t: int, e: int) -> int:
+    if g.NP >= 3:
+        return (t >> 4) + (g.N // 256) * (t & 15) + (g.N // 16) * e
+    return t + g.T * e
+
+
 def conv_model2(block: np.ndarray, table: np.ndarray, logn: int, trace=None) -> np.ndarray:
-    """Emulate the v2 conv_pass<LOGN,0> on one polarisation."""
+    """Emulate the kernel's conv_pass<LOGN,0> on one polarisation (table: natural order, 1/N folded)."""
     g = Geo2(logn)
     N, T = g.N, g.T
     tw = twiddles2(g)
+    tab = np.array([table[last_pass_bin(g, t, e)] for e in range(16) for t in range(T)])  # [t + T e]
     regs = np.zeros((T, 16), dtype=np.complex128)
     for t in range(T):
         for m in range(16):
@@ -79,67 +94,97 @@ def conv_model2(block: np.ndarray, table: np.ndarray, logn: int, trace=None) -> 
     def read_base(t, ls1):
         return ((t >> ls1) << (ls1 + 4)) + (t & ((1 << ls1) - 1))
 
+    def cta_exchange_fwd(p):
+        ls1 = g.log_s(p + 1)
+        plane[:] = np.nan
+        for t in range(T):
+            for m in range(16):
+                plane[side2(g, p, t, m)] = regs[t, m]
+        for t in range(T):
+            for e in range(16):
+                regs[t, e] = plane[xchg2(g, p, read_base(t, ls1) + (e << ls1))]
+
+    def cta_exchange_inv(p):
+        ls1 = g.log_s(p + 1)
+        plane[:] = np.nan
+        for t in range(T):
+            for e in range(16):
+                plane[xchg2(g, p, read_base(t, ls1) + (e << ls1))] = regs[t, e]
+        for t in range(T):
+            for m in range(16):
+                regs[t, m] = plane[side2(g, p, t, m)]
+
+    def last(t):
+        u = dft(regs[t], False)
+        for e in range(16):
+            u[e] *= tab[t + T * e]
+        regs[t] = dft(u, True)
+
     def rec(p):
         if g.NP == 1:
             for t in range(T):
-                regs[t] = dft(regs[t], False) * table[:16]
+                regs[t] = dft(regs[t], False) * tab[:16]
                 regs[t] = dft(regs[t], True)
             return
-        if p < g.NP - 1:
-            ls1 = g.log_s(p + 1)
+        if p == 0:
             for t in range(T):
-                if p == 0:
-                    for q in range(g.G0):
-                        idx = [q + g.G0 * e for e in range(g.R0)]
-                        u = dft(regs[t, idx], False)
-                        for k in range(1, g.R0):
-                            u[k] *= tw[(k - 1) * (N // g.R0) + t + T * q]
-                        regs[t, idx] = u
-                else:
-                    s = 1 << g.log_s(p)
-                    regs[t] = dft(regs[t], False)
-                    for k in range(1, 16):
-                        regs[t, k] *= tw[g.tw_offset(p) + (t & (s - 1)) + (k - 1) * s]
-            plane[:] = np.nan
+                for q in range(g.G0):
+                    idx = [q + g.G0 * e for e in range(g.R0)]
+                    u = dft(regs[t, idx], False)
+                    for k in range(1, g.R0):
+                        u[k] *= tw[(k - 1) * (N // g.R0) + t + T * q]
+                    regs[t, idx] = u
+            cta_exchange_fwd(0)
+            if g.NP == 2:
+                for t in range(T):
+                    last(t)
+            else:
+                rec(1)
+            cta_exchange_inv(0)
             for t in range(T):
-                for m in range(16):
-                    a = xchg2(g, p, t + T * m)
-                    if trace is not None:
-                        trace.append(("w", p, t, a))
-                    plane[a] = regs[t, m]
+                for q in range(g.G0):
+                    idx = [q + g.G0 * e for e in range(g.R0)]
+                    u = regs[t, idx].copy()
+                    for k in range(1, g.R0):
+                        u[k] *= np.conj(tw[(k - 1) * (N // g.R0) + t + T * q])
+                    regs[t, idx] = dft(u, True)
+            return
+        s = 1 << g.log_s(p)
+        for t in range(T):
+            regs[t] = dft(regs[t], False)
+            for k in range(1, 16):
+                regs[t, k] *= tw[g.tw_offset(p) + (t & (s - 1)) + (k - 1) * s]
+        if p == g.NP - 2:
+            # half-warp-local transpose through the 272-element tile
+            for h in range(T // 16):
+                tile = np.full(272, np.nan + 0j)
+                base = 272 * h
+                for l in range(16):
+                    for k in range(16):
+                        tile[l + 17 * k] = regs[16 * h + l, k]
+                        if trace is not None:
+                            trace.append(("tile", h, base + l + 17 * k))
+                for l in range(16):
+                    for e in range(16):
+                        regs[16 * h + l, e] = tile[17 * l + e]
             for t in range(T):
-                for e in range(16):
-                    a = xchg2(g, p, read_base(t, ls1) + (e << ls1))
-                    if trace is not None:
-                        trace.append(("r", p, t, a))
-                    regs[t, e] = plane[a]
-            rec(p + 1)
-            plane[:] = np.nan
-            for t in range(T):
-                for e in range(16):
-                    plane[xchg2(g, p, read_base(t, ls1) + (e << ls1))] = regs[t, e]
-            for t in range(T):
-                for m in range(16):
-                    regs[t, m] = plane[xchg2(g, p, t + T * m)]
-            for t in range(T):
-                if p == 0:
-                    for q in range(g.G0):
-                        idx = [q + g.G0 * e for e in range(g.R0)]
-                        u = regs[t, idx].copy()
-                        for k in range(1, g.R0):
-                            u[k] *= np.conj(tw[(k - 1) * (N // g.R0) + t + T * q])
-                        regs[t, idx] = dft(u, True)
-                else:
-                    s = 1 << g.log_s(p)
-                    for k in range(1, 16):
-                        regs[t, k] *= np.conj(tw[g.tw_offset(p) + (t & (s - 1)) + (k - 1) * s])
-                    regs[t] = dft(regs[t], True)
+                last(t)
+            for h in range(T // 16):
+                tile = np.full(272, np.nan + 0j)
+                for l in range(16):
+                    for e in range(16):
+                        tile[17 * l + e] = regs[16 * h + l, e]
+                for l in range(16):
+                    for k in range(16):
+                        regs[16 * h + l, k] = tile[l + 17 * k]
         else:
-            for t in range(T):
-                u = dft(regs[t], False)
-                for e in range(16):
-                    u[e] *= table[t + T * e]
-                regs[t] = dft(u, True)
+            cta_exchange_fwd(p)
+            rec(p + 1)
+            cta_exchange_inv(p)
+        for t in range(T):
+            for k in range(1, 16):
+                regs[t, k] *= np.conj(tw[g.tw_offset(p) + (t & (s - 1)) + (k - 1) * s])
+            regs[t] = dft(regs[t], True)
 
     rec(0)
     out = np.zeros(N, dtype=np.complex128)

@@ -15,7 +15,7 @@ def test_fir_padding_conflict_free():
 
 # ---- v2 (default) kernel: one polarisation per thread, radix R0 first ----
 
-from .layout_model import Geo2, conv_model2, twiddles2, xchg2  # noqa: E402
+from .layout_model import Geo2, conv_model2, side2, twiddles2, xchg2  # noqa: E402
 
 
 @pytest.mark.parametrize("logn", list(range(4, 14)))
@@ -36,19 +36,47 @@ def test_v2_exchanges_bijective_and_conflict_free(logn):
     # 8-byte accesses: the 16 lanes of one polarisation share a shared-memory phase
     g = Geo2(logn)
     n, T = g.N, g.T
-    for p in range(g.NP - 1):
-        assert len({xchg2(g, p, i) for i in range(n)}) == n and max(xchg2(g, p, i) for i in range(n)) < n + n // 16
+    cta_boundaries = [p for p in range(g.NP - 1) if not (g.NP >= 3 and p == g.NP - 2)]
+    for p in cta_boundaries:
+        idx = [xchg2(g, p, i) for i in range(n)]
+        assert len(set(idx)) == n and max(idx) < n + n // 16
         if T < 16:
             continue
         ls1 = g.log_s(p + 1)
         for h0 in range(0, T, 16):
             lanes = range(h0, h0 + 16)
             for m in range(16):
-                assert len({xchg2(g, p, t + T * m) % 16 for t in lanes}) == 16
+                assert len({side2(g, p, t, m) % 16 for t in lanes}) == 16
+                assert side2(g, p, h0, m) == xchg2(g, p, h0 + T * m)
             for e in range(16):
                 banks = {xchg2(g, p, ((t >> ls1) << (ls1 + 4)) + (t & ((1 << ls1) - 1)) + (e << ls1)) % 16
                          for t in lanes}
                 assert len(banks) == 16, (p, e)
+    if g.NP >= 3:
+        # the gathers of the exchange into pass NP-2 stay inside each half-warp's tile
+        p, ls1 = g.NP - 3, 4
+        for h in range(T // 16):
+            reads = {xchg2(g, p, ((t >> ls1) << (ls1 + 4)) + (t & 15) + (e << ls1))
+                     for t in range(16 * h, 16 * h + 16) for e in range(16)}
+            assert min(reads) >= 272 * h and max(reads) < 272 * h + 256
+        # tile accesses: writes l + 17 k (fixed k), gathers 17 l + e (fixed e): 16 distinct banks
+        for k in range(16):
+            assert len({(l + 17 * k) % 16 for l in range(16)}) == 16
+            assert len({(17 * l + k) % 16 for l in range(16)}) == 16
+
+
+def test_v2_side_index_linear_forms():
+    # the kernel's closed forms equal the padded index of t + T m
+    for logn in range(5, 14):
+        g = Geo2(logn)
+        for p in range(g.NP - 1):
+            for t in range(g.T):
+                for m in range(16):
+                    i = t + g.T * m
+                    if g.NP >= 3 and p + 1 == g.NP - 2:
+                        closed = (t + g.T * m + (((g.T * m) >> 8) << 4)) if g.T <= 256 else \
+                                 (t + ((t >> 8) << 4)) + m * (g.T + g.T // 16)
+                        assert closed == i + ((i >> 8) << 4)
 
 
 def test_v2_twiddle_table_size():
