@@ -41,7 +41,7 @@ POWER_DBM = 0.0
 def parse_args(argv=None):
     ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--waveforms", type=int, default=512, help="waveforms per GPU")
@@ -252,6 +252,18 @@ def run_ours(a) -> int:
     peaks = json.loads((REPO / "MEASURED_PEAKS.json").read_text()) if (REPO / "MEASURED_PEAKS.json").exists() else {}
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
 
+    # DRAM traffic of the same kernel from the committed ncu capture of this command
+    traffic, traffic_src = None, None
+    prof = REPO / "profiles" / "latest_ncu.json"
+    default = (a.algorithm, a.arrangement, a.num_steps, a.nc, a.block_len, a.overlap) == \
+        ("essfm", "symmetric", 1, 17, 2048, 700)
+    if prof.exists() and default:
+        pj = json.loads(prof.read_text())
+        if f"dbp_block_kernel<{int(math.log2(a.block_len))}>" in str(pj.get("kernel", "")):
+            traffic = pj["dram_bytes_per_sample"] * per_launch_samples
+            traffic_src = ("profiles/latest_ncu.json: dram__bytes_read.sum + dram__bytes_write.sum of one "
+                           "ncu --set full launch of this command, scaled per launch")
+
     # ---- end to end through the public API with pinned host buffers ----
     e2e = None
     if not a.no_e2e:
@@ -304,8 +316,10 @@ def run_ours(a) -> int:
                          "frac": achieved_tf / peak_tf,
                          "peak_source": "measured in this run: FFMA probe (dbp_probe_fp32_peak); "
                                         "MEASURED_PEAKS.json has no FP32 entry",
-                         "flops_per_sample": f_s, "traffic": None,
-                         "kernel": "dbp::dbp_block_kernel<11>"},
+                         "flops_per_sample": f_s, "traffic": traffic, "traffic_unit": "bytes per launch",
+                         "traffic_source": traffic_src,
+                         "algorithmic_bytes_per_launch": b_s * per_launch_samples,
+                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}>"},
             "roofline_hbm": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved_gbs / hbm_peak, "bytes_per_sample": b_s,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},

@@ -114,7 +114,9 @@ int dbp_run_chunk(dbp_plan* plan, const void* d_in, void* d_out, int64_t n_total
 int dbp_run_host(dbp_plan* plan, const void* h_in, void* h_out, int64_t n_total, int batch,
                  int64_t block_begin, int64_t block_end);
 
-/* Device staging budget (bytes) used by dbp_run_host (default 1 GiB).       */
+/* Device staging budget (bytes) used by dbp_run_host (default 256 MiB: 32   
+ * pipelined chunks for the configs[3] batch, so the un-overlapped first    
+ * H2D and last D2H stay short).                                             */
 int dbp_plan_set_staging(dbp_plan* plan, size_t bytes);
 
 /* Unit seam: apply the configured per-block operator (the reference's

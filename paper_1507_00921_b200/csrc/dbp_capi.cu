@@ -98,7 +98,7 @@ struct dbp_plan {
   int batch_sets = 0, batch_nc = 0, batch_stride = 0;
   size_t batch_cap = 0;
   // host-run staging
-  size_t staging_budget = size_t(1) << 30;
+  size_t staging_budget = size_t(256) << 20;
   cudaStream_t streams[2] = {nullptr, nullptr};
   void* d_stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][in/out]
   size_t stage_bytes = 0;
