@@ -188,11 +188,17 @@ def run_ours(a) -> int:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev = local
+    # one process per GPU; BENCH_DIST_BACKEND=gloo (CPU reductions) lets the
+    # multi-rank path be exercised with several ranks on one device
+    backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+    dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
+    if world > 1:
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    red_dev = f"cuda:{dev}" if backend == "nccl" else "cpu"
     n = 1 << a.log2_samples
     B = a.waveforms
     cfg = make_cfg(a)
@@ -237,7 +243,7 @@ def run_ours(a) -> int:
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    t = torch.tensor([ms], dtype=torch.float64, device=f"cuda:{dev}")
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -278,7 +284,7 @@ def run_ours(a) -> int:
         for _ in range(a.e2e_steps):
             eng.run_host(hin.array, hout.array)
         e2e_s = time.perf_counter() - t0
-        te = torch.tensor([e2e_s], dtype=torch.float64, device=f"cuda:{dev}")
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
