@@ -71,36 +71,53 @@ struct Geo {
   static constexpr bool DB = DBP_DOUBLE_BUFFER && (2 * 16 * (N + N / 16) * BPC <= 80 * 1024);
   // log2 of the pass stride S_p = N / (L_p r_p)
   __host__ __device__ static constexpr int log_s(int p) { return LOGN - LOGR0 - 4 * p; }
-  // offset of pass p's twiddle table: pass 0 holds (R0-1) N/R0 entries, pass q >= 1 15 S_q
+  // offset (float2 units) of pass p's twiddle table.  Tables are k-paired:
+  // row r holds (W^{(2r+1) c}, W^{(2r+2) c}) for every column c as one
+  // 16-byte entry, so a thread fetches two twiddles per load.  Pass 0: R0/2
+  // rows x N/R0 columns; pass q >= 1: 8 rows x S_q columns.
   __host__ __device__ static constexpr int tw_offset(int p) {
     int off = 0;
-    for (int q = 0; q < p; ++q) off += q == 0 ? (R0 - 1) * (N / R0) : 15 * (1 << log_s(q));
+    for (int q = 0; q < p; ++q) off += q == 0 ? (R0 / 2) * (N / R0) * 2 : 8 * (1 << log_s(q)) * 2;
     return off;
   }
 };
 
-// Twiddle tables, float64 -> float32: pass 0 W_N^{g k} [k-1][g] (g < N/R0,
-// k < R0); pass p >= 1 W_{16 S_p}^{ns k} [k-1][ns] (ns < S_p, k < 16).
+// Twiddle tables, float64 -> float32, k-paired (see Geo::tw_offset):
+// pass 0 W_N^{g k} (g < N/R0, k < R0), pass p >= 1 W_{16 S_p}^{ns k}
+// (ns < S_p, k < 16); entry [r][c] = (W^{(2r+1) c}, W^{(2r+2) c}), the
+// second half zero when 2r+2 reaches the radix.
 inline std::vector<float2> make_twiddles(int logn) {
   const int np = (logn + 3) / 4;
   const int logr0 = logn - 4 * (np - 1);
   const long long n = 1LL << logn, r0 = 1LL << logr0;
   std::vector<float2> tw;
-  auto push = [&](long long m, long long period) {
+  auto w = [](long long m, long long period) {
     const double ang = -2.0 * M_PI * (double)(m % period) / (double)period;
-    tw.push_back(make_float2((float)std::cos(ang), (float)std::sin(ang)));
+    return make_float2((float)std::cos(ang), (float)std::sin(ang));
+  };
+  auto table = [&](long long radix, long long cols, long long period) {
+    for (long long r = 0; r < radix / 2; ++r)
+      for (long long c = 0; c < cols; ++c) {
+        const long long k0 = 2 * r + 1, k1 = 2 * r + 2;
+        tw.push_back(w(c * k0, period));
+        tw.push_back(k1 < radix ? w(c * k1, period) : make_float2(0.f, 0.f));
+      }
   };
   if (np > 1) {
-    for (long long k = 1; k < r0; ++k)
-      for (long long g = 0; g < n / r0; ++g) push(g * k, n);
+    table(r0, n / r0, n);
     for (int p = 1; p < np - 1; ++p) {
       const long long s = n >> (logr0 + 4 * p);
-      for (long long k = 1; k < 16; ++k)
-        for (long long ns = 0; ns < s; ++ns) push(ns * k, 16 * s);
+      table(16, s, 16 * s);
     }
   }
   if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
   return tw;
+}
+
+// Dispersion-table entry index of (thread t, register e): tables are
+// e-paired like the twiddles, [e/2][t] -> (H_e, H_{e+1}) per 16 bytes.
+__host__ __device__ constexpr int tab_index(int logn, int t, int e) {
+  return (e >> 1) * 2 * ((1 << logn) / 16) + 2 * t + (e & 1);
 }
 
 __host__ __device__ inline int fir_phys(int u) { return u + ((u >> 4) << 2); }  // pad 4 per 16 floats
@@ -184,6 +201,32 @@ struct Shm {
   }
 };
 
+// u[k] *= W (or conj W) for k = 1 .. R-1 from a k-paired table column
+// (``col`` points at row 0 of this thread's column, rows ``row_stride``
+// float2 apart): two twiddles per 16-byte load.
+template <int R, bool CONJ>
+__device__ __forceinline__ void twiddle_paired(float2* u, const float2* col, int row_stride) {
+#pragma unroll
+  for (int k = 1; k < R; k += 2) {
+    float2 w0, w1;
+    ldg_table_pair(col + ((k - 1) >> 1) * row_stride, w0, w1);
+    u[k] = CONJ ? c_mulc(u[k], w0) : c_mul(u[k], w0);
+    if (k + 1 < R) u[k + 1] = CONJ ? c_mulc(u[k + 1], w1) : c_mul(u[k + 1], w1);
+  }
+}
+
+// v[e] *= table entry of (t, e), e-paired dispersion table
+template <int LOGN>
+__device__ __forceinline__ void apply_table(float2 (&v)[16], const float2* __restrict__ tab, int t) {
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) {
+    float2 h0, h1;
+    ldg_table_pair(tab + tab_index(LOGN, t, e), h0, h1);
+    v[e] = c_mul(v[e], h0);
+    v[e + 1] = c_mul(v[e + 1], h1);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // FFT -> x table -> IFFT on one polarisation, recursive over passes.
 // On entry and exit v[m] holds block position t + T m.
@@ -197,8 +240,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
   if constexpr (NP == 1) {
     // N == 16: a single radix-16 pass, bins k = e
     dft<16, false>(v);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(tab + e));
+    apply_table<LOGN>(v, tab, 0);
     dft<16, true>(v);
   } else if constexpr (P == 0) {
     // radix R0 over G0 groups: group q = registers q + G0 e, g = t + T q
@@ -209,8 +251,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
       dft<R0, false>(u);
-#pragma unroll
-      for (int k = 1; k < R0; ++k) u[k] = c_mul(u[k], ldg_table(tw + (k - 1) * S0 + t + T * q));
+      twiddle_paired<R0, false>(u, tw + 2 * (t + T * q), 2 * S0);
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
@@ -253,8 +294,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       float2 u[R0];
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
-#pragma unroll
-      for (int k = 1; k < R0; ++k) u[k] = c_mulc(u[k], ldg_table(tw + (k - 1) * S0 + t + T * q));
+      twiddle_paired<R0, true>(u, tw + 2 * (t + T * q), 2 * S0);
       dft<R0, true>(u);
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
@@ -265,10 +305,9 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     // ns = t & 15 holds its register k; the last pass's group (h, k) goes to
     // lane k of the same half-warp.  The tile [272 h, 272 h + 272) is the
     // region this half-warp alone read in the previous (pad256) exchange.
-    const float2* twp = tw + G::tw_offset(P) + (t & 15);
+    const float2* twp = tw + G::tw_offset(P) + 2 * (t & 15);
     dft<16, false>(v);
-#pragma unroll
-    for (int k = 1; k < 16; ++k) v[k] = c_mul(v[k], ldg_table(twp + (k - 1) * 16));
+    twiddle_paired<16, false>(v, twp, 2 * 16);
     {
       float2* tile = sh.plane() + 272 * (t >> 4);
       const int l = t & 15;
@@ -281,8 +320,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     }
     // last pass: group (h, l), bins last_pass_bin(t, e) (table pre-permuted)
     dft<16, false>(v);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(tab + t + T * e));
+    apply_table<LOGN>(v, tab, t);
     dft<16, true>(v);
     t = opaque(t);
     {
@@ -295,17 +333,15 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int k = 0; k < 16; ++k) v[k] = tile[l + 17 * k];
     }
-    twp = tw + G::tw_offset(P) + (t & 15);
-#pragma unroll
-    for (int k = 1; k < 16; ++k) v[k] = c_mulc(v[k], ldg_table(twp + (k - 1) * 16));
+    twp = tw + G::tw_offset(P) + 2 * (t & 15);
+    twiddle_paired<16, true>(v, twp, 2 * 16);
     dft<16, true>(v);
   } else if constexpr (P < NP - 1) {
     // middle radix-16 pass: group g = t, ns = t mod S_P
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
-    const float2* twp = tw + G::tw_offset(P) + (t & (S - 1));
+    const float2* twp = tw + G::tw_offset(P) + 2 * (t & (S - 1));
     dft<16, false>(v);
-#pragma unroll
-    for (int k = 1; k < 16; ++k) v[k] = c_mul(v[k], ldg_table(twp + (k - 1) * S));
+    twiddle_paired<16, false>(v, twp, 2 * S);
     sh.before_write();
     {
       float2* plane = sh.plane();
@@ -323,7 +359,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 
     conv_pass<LOGN, P + 1>(v, sh, tab, tw, t);
     t = opaque(t);
-    twp = tw + G::tw_offset(P) + (t & (S - 1));
+    twp = tw + G::tw_offset(P) + 2 * (t & (S - 1));
 
     sh.before_write();
     {
@@ -339,14 +375,12 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
     sh.flip();
-#pragma unroll
-    for (int k = 1; k < 16; ++k) v[k] = c_mulc(v[k], ldg_table(twp + (k - 1) * S));
+    twiddle_paired<16, true>(v, twp, 2 * S);
     dft<16, true>(v);
   } else {
     // last pass: S = 1, group g = t, bin k = t + T e
     dft<16, false>(v);
-#pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(tab + t + T * e));
+    apply_table<LOGN>(v, tab, t);
     dft<16, true>(v);
   }
 }

@@ -275,11 +275,11 @@ int dbp_plan_set_linear(dbp_plan* p, const double* kernel, const double* half_ke
   DeviceGuard g(p->device);
   const double inv_n = 1.0 / (double)p->N;
   const int T = p->N / 16;
-  // stored in the kernel's register order: entry t + T e holds the bin that
-  // register e of thread t carries after the last forward FFT pass
+  // stored in the kernel's register order: entry tab_index(t, e) holds the bin
+  // that register e of thread t carries after the last forward FFT pass
   std::vector<int> bin(p->N);
   for (int t = 0; t < T; ++t)
-    for (int e = 0; e < 16; ++e) bin[t + T * e] = dbp::last_pass_bin(p->logn, t, e);
+    for (int e = 0; e < 16; ++e) bin[dbp::tab_index(p->logn, t, e)] = dbp::last_pass_bin(p->logn, t, e);
   std::vector<float2> h(p->N);
   for (int j = 0; j < p->N; ++j) {
     const int k = bin[j];

@@ -60,6 +60,14 @@ __device__ __forceinline__ float2 ldg_table(const float2* p) {
   return v;
 }
 
+__device__ __forceinline__ void ldg_table_pair(const float2* p, float2& a, float2& b) {
+  float4 v;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  a = make_float2(v.x, v.y);
+  b = make_float2(v.z, v.w);
+}
+
 // value barrier: stops CSE of index arithmetic across the recursive passes
 __device__ __forceinline__ int opaque(int x) {
   int y;
