@@ -215,6 +215,47 @@ __device__ __forceinline__ void twiddle_paired(float2* u, const float2* col, int
   }
 }
 
+// Same twiddles from ONE 8-byte load of W (row 0 first half) and complex
+// products of depth <= 4 (W^2, W^4, W^8 by squaring): trades L1 table
+// traffic for FP32 work.  Selected per pass by DBP_TW_POWERS (bit 0: first
+// pass, bit 1: later passes).  Default 1: the first pass's table is the big
+// one (N/R0 columns); measured +3% (ESSFM) / +3% (FFE) at N = 2048, worst
+// golden-case error 3.4e-6 -> 3.6e-6.  Later passes keep table loads.
+__device__ __forceinline__ float2 c_sqr(float2 a) {
+  return make_float2(fmaf(a.x, a.x, -a.y * a.y), fmaf(a.x, a.y, a.x * a.y));
+}
+
+template <int R, bool CONJ>
+__device__ __forceinline__ void twiddle_powers(float2* u, const float2* col) {
+  float2 p[16];
+  p[1] = ldg_table(col);
+  if constexpr (R > 2) p[2] = c_sqr(p[1]);
+  if constexpr (R > 3) p[3] = c_mul(p[2], p[1]);
+  if constexpr (R > 4) {
+    p[4] = c_sqr(p[2]);
+    p[5] = c_mul(p[4], p[1]);
+    p[6] = c_sqr(p[3]);
+    p[7] = c_mul(p[4], p[3]);
+  }
+  if constexpr (R > 8) {
+    p[8] = c_sqr(p[4]);
+#pragma unroll
+    for (int k = 9; k < 16; ++k) p[k] = c_mul(p[8], p[k - 8]);
+  }
+#pragma unroll
+  for (int k = 1; k < R; ++k) u[k] = CONJ ? c_mulc(u[k], p[k]) : c_mul(u[k], p[k]);
+}
+
+#ifndef DBP_TW_POWERS
+#define DBP_TW_POWERS 1
+#endif
+
+template <int R, bool CONJ, bool FIRST>
+__device__ __forceinline__ void twiddle(float2* u, const float2* col, int row_stride) {
+  if constexpr ((DBP_TW_POWERS & (FIRST ? 1 : 2)) != 0) twiddle_powers<R, CONJ>(u, col);
+  else twiddle_paired<R, CONJ>(u, col, row_stride);
+}
+
 // v[e] *= table entry of (t, e), e-paired dispersion table
 template <int LOGN>
 __device__ __forceinline__ void apply_table(float2 (&v)[16], const float2* __restrict__ tab, int t) {
@@ -251,7 +292,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
       dft<R0, false>(u);
-      twiddle_paired<R0, false>(u, tw + 2 * (t + T * q), 2 * S0);
+      twiddle<R0, false, true>(u, tw + 2 * (t + T * q), 2 * S0);
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
@@ -294,7 +335,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       float2 u[R0];
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
-      twiddle_paired<R0, true>(u, tw + 2 * (t + T * q), 2 * S0);
+      twiddle<R0, true, true>(u, tw + 2 * (t + T * q), 2 * S0);
       dft<R0, true>(u);
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
@@ -307,7 +348,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     // region this half-warp alone read in the previous (pad256) exchange.
     const float2* twp = tw + G::tw_offset(P) + 2 * (t & 15);
     dft<16, false>(v);
-    twiddle_paired<16, false>(v, twp, 2 * 16);
+    twiddle<16, false, false>(v, twp, 2 * 16);
     {
       float2* tile = sh.plane() + 272 * (t >> 4);
       const int l = t & 15;
@@ -334,14 +375,14 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       for (int k = 0; k < 16; ++k) v[k] = tile[l + 17 * k];
     }
     twp = tw + G::tw_offset(P) + 2 * (t & 15);
-    twiddle_paired<16, true>(v, twp, 2 * 16);
+    twiddle<16, true, false>(v, twp, 2 * 16);
     dft<16, true>(v);
   } else if constexpr (P < NP - 1) {
     // middle radix-16 pass: group g = t, ns = t mod S_P
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
     const float2* twp = tw + G::tw_offset(P) + 2 * (t & (S - 1));
     dft<16, false>(v);
-    twiddle_paired<16, false>(v, twp, 2 * S);
+    twiddle<16, false, false>(v, twp, 2 * S);
     sh.before_write();
     {
       float2* plane = sh.plane();
@@ -375,7 +416,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
     sh.flip();
-    twiddle_paired<16, true>(v, twp, 2 * S);
+    twiddle<16, true, false>(v, twp, 2 * S);
     dft<16, true>(v);
   } else {
     // last pass: S = 1, group g = t, bin k = t + T e

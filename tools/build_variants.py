@@ -13,8 +13,9 @@ VARIANTS = {
     "v2_cta64": ["-DDBP_CTA_POSITIONS=64", "-DDBP_THREADS_PER_SM=768"],
     "single": ["-DDBP_DOUBLE_BUFFER=0"],
     "double": ["-DDBP_DOUBLE_BUFFER=1"],
-    "powers": ["-DDBP_TWIDDLE_POWERS=1"],
-    "powers_db": ["-DDBP_TWIDDLE_POWERS=1", "-DDBP_DOUBLE_BUFFER=1"],
+    "pw1": ["-DDBP_TW_POWERS=1"],
+    "pw2": ["-DDBP_TW_POWERS=2"],
+    "pw3": ["-DDBP_TW_POWERS=3"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
