@@ -69,6 +69,8 @@ struct Geo {
   // two shared buffers per slice (one barrier per exchange instead of two)
   // while both fit next to the L1-resident tables
   static constexpr bool DB = DBP_DOUBLE_BUFFER && (2 * 16 * (N + N / 16) * BPC <= 80 * 1024);
+  // first exchange with 16-byte paired accesses (see conv_pass)
+  static constexpr bool X01_PAIRED = (NP == 3 && R0 == 8);
   // log2 of the pass stride S_p = N / (L_p r_p)
   __host__ __device__ static constexpr int log_s(int p) { return LOGN - LOGR0 - 4 * p; }
   // offset (float2 units) of pass p's twiddle table.  Tables are k-paired:
@@ -175,6 +177,15 @@ __device__ __forceinline__ int side_index(int t, int m) {
 __host__ __device__ constexpr int last_pass_bin(int logn, int t, int e) {
   const int n = 1 << logn, tt = n / 16, np = (logn + 3) / 4;
   return np >= 3 ? (t >> 4) + (n / 256) * (t & 15) + (n / 16) * e : t + tt * e;
+}
+
+__device__ __forceinline__ void st_pair(float2* p, float2 a, float2 b) {
+  *reinterpret_cast<float4*>(p) = make_float4(a.x, a.y, b.x, b.y);
+}
+__device__ __forceinline__ void ld_pair(const float2* p, float2& a, float2& b) {
+  const float4 q = *reinterpret_cast<const float4*>(p);
+  a = make_float2(q.x, q.y);
+  b = make_float2(q.z, q.w);
 }
 
 // Shared-memory phases.  Single-buffered: barrier before and after every
@@ -299,13 +310,26 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     // exchange into the pass-1 layout
     constexpr int LS1 = G::log_s(1);
     sh.before_write();
-    {
+    if constexpr (G::X01_PAIRED) {
+      // R0 = 8, N = 2048: positions i and i + T pair up on both sides of this
+      // exchange (registers (m, m+1) when writing, gathers (e, e+8) when
+      // reading), so the plane stores them adjacently -- layout
+      // pad256(256 (i >> 8) + 2 (i & 127) + ((i >> 7) & 1)) -- and every
+      // access is a conflict-free 16-byte vector: half the LDS/STS.
+      float2* plane = sh.plane() + 2 * t;
+#pragma unroll
+      for (int m = 0; m < 16; m += 2) st_pair(plane + 272 * (m >> 1), v[m], v[m + 1]);
+    } else {
       float2* plane = sh.plane();
 #pragma unroll
       for (int m = 0; m < 16; ++m) plane[side_index<LOGN, 0>(t, m)] = v[m];
     }
     sh.after_write();
-    {
+    if constexpr (G::X01_PAIRED) {
+      const float2* plane = sh.plane() + 272 * (t >> 4) + 2 * (t & 15);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ld_pair(plane + 32 * e, v[e], v[e + 8]);
+    } else {
       const float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
@@ -317,14 +341,22 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     t = opaque(t);
 
     sh.before_write();
-    {
+    if constexpr (G::X01_PAIRED) {
+      float2* plane = sh.plane() + 272 * (t >> 4) + 2 * (t & 15);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) st_pair(plane + 32 * e, v[e], v[e + 8]);
+    } else {
       float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) plane[xchg_index<LOGN, 0>(base + (e << LS1))] = v[e];
     }
     sh.after_write();
-    {
+    if constexpr (G::X01_PAIRED) {
+      const float2* plane = sh.plane() + 2 * t;
+#pragma unroll
+      for (int m = 0; m < 16; m += 2) ld_pair(plane + 272 * (m >> 1), v[m], v[m + 1]);
+    } else {
       const float2* plane = sh.plane();
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, 0>(t, m)];

@@ -56,8 +56,16 @@ def twiddles2(g: Geo2) -> np.ndarray:
     return np.asarray(out if out else [1.0 + 0j])
 
 
+def pair_layout(i: int) -> int:
+    """X01_PAIRED layout (N = 2048): i and i + 128 adjacent, then pad256."""
+    j = 256 * (i >> 8) + 2 * (i & 127) + ((i >> 7) & 1)
+    return j + ((j >> 8) << 4)
+
+
 def xchg2(g: Geo2, p: int, i: int) -> int:
     """Gather-side plane index of exchange p (kernel xchg_index)."""
+    if g.NP == 3 and g.R0 == 8 and p == 0:
+        return pair_layout(i)
     if g.NP == 2 and p == 0:
         return i + (i >> 4)                      # pad16
     if g.NP >= 3 and p + 1 == g.NP - 2:
