@@ -51,8 +51,8 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
 #ifndef DBP_CTA_POSITIONS
 #define DBP_CTA_POSITIONS 128
 #endif
-#ifndef DBP_DOUBLE_BUFFER
-#define DBP_DOUBLE_BUFFER 0
+#ifndef DBP_SEPARATE_FIR
+#define DBP_SEPARATE_FIR 0
 #endif
 
 template <int LOGN>
@@ -66,9 +66,13 @@ struct Geo {
   static constexpr int BPC = T >= DBP_CTA_POSITIONS ? 1 : DBP_CTA_POSITIONS / T;
   static constexpr int THREADS = 2 * T * BPC;
   static constexpr int MIN_CTAS = threads_per_sm(LOGN) / THREADS > 0 ? threads_per_sm(LOGN) / THREADS : 1;
-  // two shared buffers per slice (one barrier per exchange instead of two)
-  // while both fit next to the L1-resident tables
-  static constexpr bool DB = DBP_DOUBLE_BUFFER && (2 * 16 * (N + N / 16) * BPC <= 80 * 1024);
+  // FIR intensity / rotation-factor buffers in their own shared region (not
+  // aliased with the exchange planes) while a slice stays <= 72 KB: the
+  // first exchange of a conv and the intensity writes then need no
+  // barrier before writing (3 fewer CTA barriers per ESSFM block).  Off by
+  // default: measured -0.7% (ESSFM) / -3% (FFE) at N = 2048, the larger
+  // shared carve-out costs more L1 table hits than the barriers cost.
+  static constexpr bool SEP_FIR = DBP_SEPARATE_FIR && (16 * (N + N / 16) + 10 * N + 2048) * BPC <= 72 * 1024;
   // first exchange with 16-byte paired accesses (see conv_pass)
   static constexpr bool X01_PAIRED = (NP == 3 && R0 == 8);
   // log2 of the pass stride S_p = N / (L_p r_p)
@@ -128,10 +132,12 @@ __host__ __device__ inline int cs_phys(int j) { return j + ((j >> 4) << 1); }   
 // shared floats per block slice: max(exchange planes, FIR intensity + (cos, sin) buffers)
 inline int plane_elems(int n) { return n + n / 16; }  // padded exchange plane (float2)
 
-inline int slice_floats(int n, int pw) {
-  const int fir = fir_phys(n + 2 * pw) + 4 + 2 * (cs_phys(n) + 2);
+inline int fir_floats(int n, int pw) { return fir_phys(n + 2 * pw) + 4 + 2 * (cs_phys(n) + 2); }
+
+inline int slice_floats(int n, int pw, bool separate_fir) {
+  const int fir = fir_floats(n, pw);
   const int planes = 4 * plane_elems(n);
-  const int v = planes > fir ? planes : fir;
+  const int v = separate_fir ? planes + fir : (planes > fir ? planes : fir);
   return (v + 3) & ~3;
 }
 
@@ -188,28 +194,28 @@ __device__ __forceinline__ void ld_pair(const float2* p, float2& a, float2& b) {
   b = make_float2(q.z, q.w);
 }
 
-// Shared-memory phases.  Single-buffered: barrier before and after every
-// write phase.  Double-buffered: consecutive phases alternate buffers, so the
-// barrier after a phase's writes also proves every reader of the other
-// buffer is done -- one barrier per phase.
+// Shared memory of one block slice: two exchange planes (x, y) and the FIR
+// buffers -- aliased with the planes, or behind them when Geo::SEP_FIR.
+// Exchanges are "barrier; write; barrier; read"; with separate FIR buffers
+// the leading barrier of a conv's first exchange is provably redundant (the
+// planes' previous readers finished before the rotation's barriers).
 template <int LOGN>
 struct Shm {
   float* base;   // slice base
-  int half;      // floats per buffer
-  int par;       // buffer of the next write phase
   int pol;
-  __device__ __forceinline__ float* buf(int which) const { return base + which * half; }
   __device__ __forceinline__ float2* plane() const {
     constexpr int N = Geo<LOGN>::N;
-    return reinterpret_cast<float2*>(buf(Geo<LOGN>::DB ? par : 0)) + pol * (N + N / 16);
+    return reinterpret_cast<float2*>(base) + pol * (N + N / 16);
   }
-  __device__ __forceinline__ void before_write() const {
-    if constexpr (!Geo<LOGN>::DB) __syncthreads();
+  __device__ __forceinline__ float* fir() const {
+    constexpr int N = Geo<LOGN>::N;
+    return base + (Geo<LOGN>::SEP_FIR ? 4 * (N + N / 16) : 0);
   }
+  __device__ __forceinline__ void before_first_write() const {
+    if constexpr (!Geo<LOGN>::SEP_FIR) __syncthreads();
+  }
+  __device__ __forceinline__ void before_write() const { __syncthreads(); }
   __device__ __forceinline__ void after_write() const { __syncthreads(); }
-  __device__ __forceinline__ void flip() {
-    if constexpr (Geo<LOGN>::DB) par ^= 1;
-  }
 };
 
 // u[k] *= W (or conj W) for k = 1 .. R-1 from a k-paired table column
@@ -309,7 +315,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     }
     // exchange into the pass-1 layout
     constexpr int LS1 = G::log_s(1);
-    sh.before_write();
+    sh.before_first_write();
     if constexpr (G::X01_PAIRED) {
       // R0 = 8, N = 2048: positions i and i + T pair up on both sides of this
       // exchange (registers (m, m+1) when writing, gathers (e, e+8) when
@@ -335,7 +341,6 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
     }
-    sh.flip();
 
     conv_pass<LOGN, 1>(v, sh, tab, tw, t);
     t = opaque(t);
@@ -361,7 +366,6 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, 0>(t, m)];
     }
-    sh.flip();
 #pragma unroll
     for (int q = 0; q < G0; ++q) {
       float2 u[R0];
@@ -428,7 +432,6 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
     }
-    sh.flip();
 
     conv_pass<LOGN, P + 1>(v, sh, tab, tw, t);
     t = opaque(t);
@@ -447,7 +450,6 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
-    sh.flip();
     twiddle<16, true, false>(v, twp, 2 * S);
     dft<16, true>(v);
   } else {
@@ -610,11 +612,10 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
     }
   } else {
     const int pw = kp.fir_pad;
-    // intensity buffer (logical [-pw, N + pw)) in this phase's buffer; (cos, sin)
-    // buffer behind it, in the other buffer when double-buffered
-    float* ibuf = sh.buf(Geo<LOGN>::DB ? sh.par : 0);
-    float2* csbuf = reinterpret_cast<float2*>(sh.buf(Geo<LOGN>::DB ? sh.par ^ 1 : 0) + fir_phys(N + 2 * pw) + 4);
-    sh.before_write();
+    // intensity buffer (logical [-pw, N + pw)), (cos, sin) buffer behind it
+    float* ibuf = sh.fir();
+    float2* csbuf = reinterpret_cast<float2*>(sh.fir() + fir_phys(N + 2 * pw) + 4);
+    if constexpr (!Geo<LOGN>::SEP_FIR) __syncthreads();
     // both lanes of a pair write the same 16 values (same addresses, no
     // divergence): fir_phys(m T + t + pw) = m (5T/4) + fir_phys(t + pw) for T >= 16
     if constexpr (T >= 16) {
@@ -678,9 +679,7 @@ dbp_block_kernel(const KernelParams kp) {
   const int t = q % T;
   const int slice = q / T;
   Shm<LOGN> sh;
-  sh.base = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats * (G::DB ? 2 : 1);
-  sh.half = kp.slice_floats;
-  sh.par = 0;
+  sh.base = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats;
   sh.pol = pol;
 
   const long long blk = (long long)blockIdx.x * G::BPC + slice;

@@ -134,7 +134,7 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   kp.n_steps = p->n_steps;
   kp.nc = p->nc;
   kp.fir_pad = (p->nc + 3) & ~3;
-  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad);
+  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().separate_fir);
   kp.precise_sincos = p->n_steps >= 3 ? 1 : 0;
   kp.tab_full = p->d_full;
   kp.tab_half = p->d_half ? p->d_half : p->d_full;
@@ -150,7 +150,7 @@ int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
   const dbp::LaunchShape sh = d.shape[p->logn]();
   const long long ctas = (kp.total_blocks + sh.slices - 1) / sh.slices;
   if (ctas > 0x7fffffffLL) return fail(DBP_EINVAL, "too many blocks for one launch");
-  const size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices * sh.buffers;
+  const size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices;
   if (smem > 227 * 1024) return fail(DBP_EINVAL, "shared memory per CTA exceeds 227 KB for this block length");
   cudaError_t e = d.launch[p->logn](kp, ctas, smem, s);
   if (e != cudaSuccess) return cuda_fail(e, "dbp_block_kernel launch");
@@ -599,7 +599,7 @@ int dbp_run_coeff_batch(dbp_plan* p, const void* d_in, void* d_out, int64_t n_to
   base_params(p, kp);
   kp.nc = p->batch_nc;
   kp.fir_pad = (p->batch_nc + 3) & ~3;
-  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad);
+  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().separate_fir);
   kp.coeff = p->d_coeff_batch;
   kp.coeff_stride = p->batch_stride;
   kp.in = static_cast<const float2*>(d_in);

@@ -14,7 +14,7 @@ struct LaunchShape {
   int threads_x;  // threads per CTA along x
   int threads_y;  // along y
   int slices;     // block slices per CTA
-  int buffers;    // shared buffers per slice (2 = double-buffered exchanges)
+  bool separate_fir;  // FIR buffers behind the exchange planes (Geo::SEP_FIR)
 };
 
 template <int LOGN>
@@ -23,7 +23,7 @@ cudaError_t launch_block_kernel(const KernelParams& kp, long long n_ctas, size_t
 
 template <int LOGN>
 LaunchShape launch_shape() {
-  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::DB ? 2 : 1};
+  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::SEP_FIR};
 }
 
 }  // namespace dbp

@@ -12,7 +12,7 @@ VARIANTS = {
     "v2_1024": ["-DDBP_THREADS_PER_SM=1024"],
     "v2_cta64": ["-DDBP_CTA_POSITIONS=64", "-DDBP_THREADS_PER_SM=768"],
     "single": ["-DDBP_DOUBLE_BUFFER=0"],
-    "double": ["-DDBP_DOUBLE_BUFFER=1"],
+    "aliasfir": ["-DDBP_SEPARATE_FIR=0"],
     "pw1": ["-DDBP_TW_POWERS=1"],
     "pw2": ["-DDBP_TW_POWERS=2"],
     "pw3": ["-DDBP_TW_POWERS=3"],
