@@ -51,6 +51,19 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
 #ifndef DBP_CTA_POSITIONS
 #define DBP_CTA_POSITIONS 128
 #endif
+// Bounds checks for debug builds (compute-sanitizer is closed on the pool):
+// -DDBP_DEBUG_BOUNDS=1 asserts every shared-memory and global index against
+// its region; tools/build_variants.py "bounds" + tests -m gpu exercise it.
+#ifndef DBP_DEBUG_BOUNDS
+#define DBP_DEBUG_BOUNDS 0
+#endif
+#if DBP_DEBUG_BOUNDS
+#include <cassert>
+#define DBP_CHECK(...) assert((__VA_ARGS__))
+#else
+#define DBP_CHECK(...) ((void)0)
+#endif
+
 #ifndef DBP_SEPARATE_FIR
 #define DBP_SEPARATE_FIR 0
 #endif
@@ -203,6 +216,10 @@ template <int LOGN>
 struct Shm {
   float* base;   // slice base
   int pol;
+  __device__ __forceinline__ static int plane_len() {
+    constexpr int N = Geo<LOGN>::N;
+    return N + N / 16;
+  }
   __device__ __forceinline__ float2* plane() const {
     constexpr int N = Geo<LOGN>::N;
     return reinterpret_cast<float2*>(base) + pol * (N + N / 16);
@@ -328,7 +345,10 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     } else {
       float2* plane = sh.plane();
 #pragma unroll
-      for (int m = 0; m < 16; ++m) plane[side_index<LOGN, 0>(t, m)] = v[m];
+      for (int m = 0; m < 16; ++m) {
+        DBP_CHECK(side_index<LOGN, 0>(t, m) < Shm<LOGN>::plane_len());
+        plane[side_index<LOGN, 0>(t, m)] = v[m];
+      }
     }
     sh.after_write();
     if constexpr (G::X01_PAIRED) {
@@ -339,7 +359,10 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       const float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
+      for (int e = 0; e < 16; ++e) {
+        DBP_CHECK(xchg_index<LOGN, 0>(base + (e << LS1)) < Shm<LOGN>::plane_len());
+        v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
+      }
     }
 
     conv_pass<LOGN, 1>(v, sh, tab, tw, t);
@@ -390,6 +413,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       const int l = t & 15;
       __syncwarp();
 #pragma unroll
+      DBP_CHECK(272 * (t >> 4) + 272 <= Shm<LOGN>::plane_len());
       for (int k = 0; k < 16; ++k) tile[l + 17 * k] = v[k];
       __syncwarp();
 #pragma unroll
@@ -423,14 +447,20 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
     {
       float2* plane = sh.plane();
 #pragma unroll
-      for (int m = 0; m < 16; ++m) plane[side_index<LOGN, P>(t, m)] = v[m];
+      for (int m = 0; m < 16; ++m) {
+        DBP_CHECK(side_index<LOGN, P>(t, m) < Shm<LOGN>::plane_len());
+        plane[side_index<LOGN, P>(t, m)] = v[m];
+      }
     }
     sh.after_write();
     {
       const float2* plane = sh.plane();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
+      for (int e = 0; e < 16; ++e) {
+        DBP_CHECK(xchg_index<LOGN, P>(base + (e << LS1)) < Shm<LOGN>::plane_len());
+        v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
+      }
     }
 
     conv_pass<LOGN, P + 1>(v, sh, tab, tw, t);
@@ -521,12 +551,13 @@ __device__ __forceinline__ void store_factors8(float2* __restrict__ csbuf, int p
 // intensity buffer, turned into rotation factors and stored to csbuf.
 template <int NC>
 __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
-                                           int p0, float a, float g, const KernelParams& kp) {
+                                           int p0, float a, float g, const KernelParams& kp, int n_blk) {
   constexpr int PW = (NC + 3) & ~3;
   constexpr int W = 8 + 2 * PW;
   float w[W];
 #pragma unroll
   for (int m = 0; m < W / 4; ++m) {
+    DBP_CHECK(fir_phys(p0 + 4 * m) + 3 < fir_phys(n_blk + 2 * PW) + 4);
     const float4 q = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
     w[4 * m] = q.x; w[4 * m + 1] = q.y; w[4 * m + 2] = q.z; w[4 * m + 3] = q.w;
   }
@@ -645,11 +676,11 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
     sh.after_write();
     const int p0 = 16 * t + 8 * pol;
     switch (kp.coeff_stride ? -1 : kp.nc) {
-      case 1: fir8_fixed<1>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
-      case 9: fir8_fixed<9>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
-      case 17: fir8_fixed<17>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
-      case 32: fir8_fixed<32>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
-      case 33: fir8_fixed<33>(ibuf, csbuf, p0, sg.x, sg.y, kp); break;
+      case 1: fir8_fixed<1>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 9: fir8_fixed<9>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 17: fir8_fixed<17>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 32: fir8_fixed<32>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 33: fir8_fixed<33>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
       default: fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp, cptr, c0); break;
     }
     __syncthreads();
@@ -698,6 +729,8 @@ dbp_block_kernel(const KernelParams kp) {
     if (!kp.cyclic || (s0 >= 0 && s0 + N <= kp.n_total)) {
       // interior block (or pre-extended chunk): one contiguous window, immediate offsets
       const float2* src = pin + (kp.cyclic ? s0 : s0 - kp.in_origin) + t;
+      DBP_CHECK((kp.cyclic ? s0 : s0 - kp.in_origin) >= 0);
+      DBP_CHECK((kp.cyclic ? s0 : s0 - kp.in_origin) + N <= kp.in_pol_stride);
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = ld_stream(src + m * T);
     } else {
@@ -709,6 +742,7 @@ dbp_block_kernel(const KernelParams kp) {
           gi %= kp.n_total;
           if (gi < 0) gi += kp.n_total;
         }
+        DBP_CHECK(gi >= 0 && gi < kp.n_total);
         v[m] = ld_stream(pin + gi);
       }
     }
@@ -760,7 +794,10 @@ dbp_block_kernel(const KernelParams kp) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
       const int j = m * T + t;
-      if (j >= kp.lead && j < hi) __stcs(dst + m * T, v[m]);
+      if (j >= kp.lead && j < hi) {
+        DBP_CHECK(ob + j >= 0 && ob + j < kp.out_pol_stride);
+        __stcs(dst + m * T, v[m]);
+      }
     }
   }
 }

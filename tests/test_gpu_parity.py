@@ -311,3 +311,34 @@ def test_coeff_batch_items_match_single_runs(rng):
     for i in range(3):
         single = _run(x, pb.DbpConfig("essfm", plan, link, num_steps=2, coeffs=pb.EssfmCoefficients(sets[i])))[0]
         assert rel_l2(out[i], single) < 1e-6
+
+
+def test_random_configurations_match_oracle():
+    # seeded sweep of random geometries / programs (cf. the reference's hypothesis
+    # properties, test_dbp.py:90-114): every block length 16..8192, any overlap,
+    # ragged lengths (n < N included), 1..6 steps, gains != 1, every arrangement,
+    # N_c up to min(64, (N-1)/2) -- per-block rel-L2 <= 1e-5 against the oracle
+    gen = np.random.default_rng(2718)
+    for case in range(40):
+        logn = int(gen.integers(4, 14))
+        n_blk = 1 << logn
+        m = int(gen.integers(0, n_blk))
+        n = int(gen.integers(1, 3 * n_blk + 2))
+        alg = ("ffe", "ssfm", "essfm")[case % 3]
+        steps = int(gen.integers(1, 7))
+        spans = int(gen.integers(1, 6))
+        arr = pb.ARRANGEMENTS[int(gen.integers(0, 3))]
+        coeffs = None
+        if alg == "essfm":
+            nc = int(gen.integers(0, min(64, (n_blk - 1) // 2) + 1))
+            c = gen.normal(size=nc + 1) * 0.1
+            c[0] = 1.0
+            coeffs = pb.EssfmCoefficients(c)
+        span = pb.FiberParams(-21.68, 1.3, 0.2, float(gen.uniform(20.0, 100.0)))
+        cfg = pb.DbpConfig(alg, pb.OverlapPlan(n_blk, m), quiet_link(spans, span), num_steps=steps,
+                           coeffs=coeffs, arrangement=arr)
+        x = (0.02 * (gen.normal(size=(2, n)) + 1j * gen.normal(size=(2, n)))).astype(np.complex64)
+        got = _run(x, cfg)[0]
+        want = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(cfg))
+        err = dbp_port.per_block_rel_l2(got, want, n_blk, m).max()
+        assert err <= TOL_BLOCK, (case, alg, n_blk, m, n, steps, spans, arr, err)

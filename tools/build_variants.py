@@ -13,6 +13,7 @@ VARIANTS = {
     "v2_cta64": ["-DDBP_CTA_POSITIONS=64", "-DDBP_THREADS_PER_SM=768"],
     "single": ["-DDBP_DOUBLE_BUFFER=0"],
     "aliasfir": ["-DDBP_SEPARATE_FIR=0"],
+    "bounds": ["-DDBP_DEBUG_BOUNDS=1"],
     "pw1": ["-DDBP_TW_POWERS=1"],
     "pw2": ["-DDBP_TW_POWERS=2"],
     "pw3": ["-DDBP_TW_POWERS=3"],
