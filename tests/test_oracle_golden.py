@@ -113,3 +113,18 @@ def test_framing_identity(rng, n_total):                       # test_spectral.p
 def test_frequency_grid():                                     # test_spectral.py:47-53
     np.testing.assert_allclose(dbp_port.bin_frequencies(8, 8e9),
                                np.array([0, 1, 2, 3, -4, -3, -2, -1]) * 1e9)
+
+
+def test_training_port_matches_reference(golden):
+    # train.py:86-188 restated on the oracle port, pinned to the reference's own fit
+    from oracle import train_port
+    from oracle.waveforms import d_to_beta2
+    cfg = dbp_port.PortConfig("essfm", 2048, 700, d_to_beta2(17.0), 1.3, 0.2, 80.0, 40, 1,
+                              np.array([1.0, 0, 0, 0, 0]), "symmetric")
+    c, err, initial, _, iters = train_port.fit(golden["link_rx"].astype(np.complex128), 56e9, cfg,
+                                               n_coeffs=4, target_steps_per_span=2, train_samples=8192,
+                                               max_iterations=6)
+    ref_initial, ref_final, ref_iters, _ = golden["train_mse"]
+    assert iters == ref_iters
+    np.testing.assert_allclose([initial, err], [ref_initial, ref_final], rtol=1e-9)
+    np.testing.assert_allclose(c, golden["train_c"], rtol=0, atol=1e-9)
