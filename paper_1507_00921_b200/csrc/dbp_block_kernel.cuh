@@ -86,7 +86,7 @@ struct Geo {
   // default: measured -0.7% (ESSFM) / -3% (FFE) at N = 2048, the larger
   // shared carve-out costs more L1 table hits than the barriers cost.
   static constexpr bool SEP_FIR = DBP_SEPARATE_FIR && (16 * (N + N / 16) + 10 * N + 2048) * BPC <= 72 * 1024;
-  // first exchange with 16-byte paired accesses (see conv_pass)
+  // first exchange with 16-byte paired accesses (see fft_fwd)
   static constexpr bool X01_PAIRED = (NP == 3 && R0 == 8);
   // log2 of the pass stride S_p = N / (L_p r_p)
   __host__ __device__ static constexpr int log_s(int p) { return LOGN - LOGR0 - 4 * p; }
@@ -161,7 +161,7 @@ inline int slice_floats(int n, int pw, bool separate_fir) {
 //  * NP >= 3: the exchange INTO pass NP-2 uses one pad of 16 elements per
 //    256 ("pad256"), so half-warp h gathers exactly [272 h, 272 h + 256); the
 //    exchange into the last pass then stays inside half-warp h's own
-//    272-element tile (see conv_pass) and needs only __syncwarp.
+//    272-element tile (see fft_fwd) and needs only __syncwarp.
 //  * all other exchanges: plain.
 // Every form is linear in the register index, so accesses are base + immediates.
 __host__ __device__ constexpr int pad16(int i) { return i + (i >> 4); }
@@ -303,20 +303,19 @@ __device__ __forceinline__ void apply_table(float2 (&v)[16], const float2* __res
 }
 
 // ---------------------------------------------------------------------------
-// FFT -> x table -> IFFT on one polarisation, recursive over passes.
-// On entry and exit v[m] holds block position t + T m.
+// Block FFT on one polarisation: fft_fwd walks the decimation-in-frequency
+// passes 0 .. NP-1 (register m of thread t holds block position t + T m on
+// entry; on exit register e holds bin last_pass_bin(t, e)); fft_inv is the
+// exact adjoint walk back (bins in that distribution -> positions t + T m,
+// unscaled).  conv_block = fft_fwd, x table, fft_inv.
 // ---------------------------------------------------------------------------
 template <int LOGN, int P>
-__device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
-                                          const float2* __restrict__ tab,
-                                          const float2* __restrict__ tw, int t) {
+__device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tw,
+                                        int t) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T, NP = G::NP;
   if constexpr (NP == 1) {
-    // N == 16: a single radix-16 pass, bins k = e
-    dft<16, false>(v);
-    apply_table<LOGN>(v, tab, 0);
-    dft<16, true>(v);
+    dft<16, false>(v);  // N == 16: a single radix-16 pass, bins k = e
   } else if constexpr (P == 0) {
     // radix R0 over G0 groups: group q = registers q + G0 e, g = t + T q
     constexpr int R0 = G::R0, G0 = G::G0, S0 = N / R0;
@@ -340,6 +339,7 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       // pad256(256 (i >> 8) + 2 (i & 127) + ((i >> 7) & 1)) -- and every
       // access is a conflict-free 16-byte vector: half the LDS/STS.
       float2* plane = sh.plane() + 2 * t;
+      DBP_CHECK(2 * t + 272 * 7 + 1 < Shm<LOGN>::plane_len());
 #pragma unroll
       for (int m = 0; m < 16; m += 2) st_pair(plane + 272 * (m >> 1), v[m], v[m + 1]);
     } else {
@@ -364,10 +364,66 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
         v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
       }
     }
+    fft_fwd<LOGN, 1>(v, sh, tw, t);
+  } else if constexpr (NP >= 3 && P == NP - 2) {
+    // second-to-last pass (S = 16) + last pass, joined by a half-warp-local
+    // 16 x 16 transpose: half-warp h = t >> 4 owns sub-problem h, lane
+    // ns = t & 15 holds its register k; the last pass's group (h, k) goes to
+    // lane k of the same half-warp.  The tile [272 h, 272 h + 272) is the
+    // region this half-warp alone read in the previous (pad256) exchange.
+    dft<16, false>(v);
+    twiddle<16, false, false>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
+    float2* tile = sh.plane() + 272 * (t >> 4);
+    const int l = t & 15;
+    DBP_CHECK(272 * (t >> 4) + 272 <= Shm<LOGN>::plane_len());
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) tile[l + 17 * k] = v[k];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = tile[17 * l + e];
+    dft<16, false>(v);  // last pass: group (h, l)
+  } else if constexpr (P < NP - 1) {
+    // middle radix-16 pass: group g = t, ns = t mod S_P
+    constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
+    dft<16, false>(v);
+    twiddle<16, false, false>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
+    sh.before_write();
+    {
+      float2* plane = sh.plane();
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        DBP_CHECK(side_index<LOGN, P>(t, m) < Shm<LOGN>::plane_len());
+        plane[side_index<LOGN, P>(t, m)] = v[m];
+      }
+    }
+    sh.after_write();
+    {
+      const float2* plane = sh.plane();
+      const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        DBP_CHECK(xchg_index<LOGN, P>(base + (e << LS1)) < Shm<LOGN>::plane_len());
+        v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
+      }
+    }
+    fft_fwd<LOGN, P + 1>(v, sh, tw, t);
+  } else {
+    dft<16, false>(v);  // last pass: S = 1, group g = t, bins t + T e
+  }
+}
 
-    conv_pass<LOGN, 1>(v, sh, tab, tw, t);
-    t = opaque(t);
-
+template <int LOGN, int P>
+__device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tw,
+                                        int t) {
+  using G = Geo<LOGN>;
+  constexpr int N = G::N, T = G::T, NP = G::NP;
+  if constexpr (NP == 1) {
+    dft<16, true>(v);
+  } else if constexpr (P == 0) {
+    constexpr int R0 = G::R0, G0 = G::G0, S0 = N / R0;
+    constexpr int LS1 = G::log_s(1);
+    fft_inv<LOGN, 1>(v, sh, tw, t);
     sh.before_write();
     if constexpr (G::X01_PAIRED) {
       float2* plane = sh.plane() + 272 * (t >> 4) + 2 * (t & 15);
@@ -400,73 +456,20 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
   } else if constexpr (NP >= 3 && P == NP - 2) {
-    // second-to-last pass (S = 16) + last pass, joined by a half-warp-local
-    // 16 x 16 transpose: half-warp h = t >> 4 owns sub-problem h, lane
-    // ns = t & 15 holds its register k; the last pass's group (h, k) goes to
-    // lane k of the same half-warp.  The tile [272 h, 272 h + 272) is the
-    // region this half-warp alone read in the previous (pad256) exchange.
-    const float2* twp = tw + G::tw_offset(P) + 2 * (t & 15);
-    dft<16, false>(v);
-    twiddle<16, false, false>(v, twp, 2 * 16);
-    {
-      float2* tile = sh.plane() + 272 * (t >> 4);
-      const int l = t & 15;
-      __syncwarp();
+    dft<16, true>(v);  // last pass
+    float2* tile = sh.plane() + 272 * (t >> 4);
+    const int l = t & 15;
+    __syncwarp();
 #pragma unroll
-      DBP_CHECK(272 * (t >> 4) + 272 <= Shm<LOGN>::plane_len());
-      for (int k = 0; k < 16; ++k) tile[l + 17 * k] = v[k];
-      __syncwarp();
+    for (int e = 0; e < 16; ++e) tile[17 * l + e] = v[e];
+    __syncwarp();
 #pragma unroll
-      for (int e = 0; e < 16; ++e) v[e] = tile[17 * l + e];
-    }
-    // last pass: group (h, l), bins last_pass_bin(t, e) (table pre-permuted)
-    dft<16, false>(v);
-    apply_table<LOGN>(v, tab, t);
-    dft<16, true>(v);
-    t = opaque(t);
-    {
-      float2* tile = sh.plane() + 272 * (t >> 4);
-      const int l = t & 15;
-      __syncwarp();
-#pragma unroll
-      for (int e = 0; e < 16; ++e) tile[17 * l + e] = v[e];
-      __syncwarp();
-#pragma unroll
-      for (int k = 0; k < 16; ++k) v[k] = tile[l + 17 * k];
-    }
-    twp = tw + G::tw_offset(P) + 2 * (t & 15);
-    twiddle<16, true, false>(v, twp, 2 * 16);
+    for (int k = 0; k < 16; ++k) v[k] = tile[l + 17 * k];
+    twiddle<16, true, false>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
     dft<16, true>(v);
   } else if constexpr (P < NP - 1) {
-    // middle radix-16 pass: group g = t, ns = t mod S_P
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
-    const float2* twp = tw + G::tw_offset(P) + 2 * (t & (S - 1));
-    dft<16, false>(v);
-    twiddle<16, false, false>(v, twp, 2 * S);
-    sh.before_write();
-    {
-      float2* plane = sh.plane();
-#pragma unroll
-      for (int m = 0; m < 16; ++m) {
-        DBP_CHECK(side_index<LOGN, P>(t, m) < Shm<LOGN>::plane_len());
-        plane[side_index<LOGN, P>(t, m)] = v[m];
-      }
-    }
-    sh.after_write();
-    {
-      const float2* plane = sh.plane();
-      const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
-#pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        DBP_CHECK(xchg_index<LOGN, P>(base + (e << LS1)) < Shm<LOGN>::plane_len());
-        v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
-      }
-    }
-
-    conv_pass<LOGN, P + 1>(v, sh, tab, tw, t);
-    t = opaque(t);
-    twp = tw + G::tw_offset(P) + 2 * (t & (S - 1));
-
+    fft_inv<LOGN, P + 1>(v, sh, tw, t);
     sh.before_write();
     {
       float2* plane = sh.plane();
@@ -480,14 +483,22 @@ __device__ __forceinline__ void conv_pass(float2 (&v)[16], Shm<LOGN>& sh,
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
-    twiddle<16, true, false>(v, twp, 2 * S);
+    twiddle<16, true, false>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
     dft<16, true>(v);
   } else {
-    // last pass: S = 1, group g = t, bin k = t + T e
-    dft<16, false>(v);
-    apply_table<LOGN>(v, tab, t);
-    dft<16, true>(v);
+    dft<16, true>(v);  // last pass
   }
+}
+
+// FFT -> x table (bins in register order, 1/N folded in) -> IFFT
+template <int LOGN>
+__device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tab,
+                                           const float2* __restrict__ tw, int t) {
+  fft_fwd<LOGN, 0>(v, sh, tw, t);
+  apply_table<LOGN>(v, tab, Geo<LOGN>::NP == 1 ? 0 : t);
+  // value barrier: the inverse recomputes its indices instead of holding the
+  // forward ones (and reloading twiddles) across the last pass
+  fft_inv<LOGN, 0>(v, sh, tw, opaque(t));
 }
 
 // ---------------------------------------------------------------------------
@@ -778,7 +789,7 @@ dbp_block_kernel(const KernelParams kp) {
       sidx = op >> 1;
     }
     if (is_conv) {
-      conv_pass<LOGN, 0>(v, sh, tab, kp.twiddle, t);
+      conv_block<LOGN>(v, sh, tab, kp.twiddle, t);
     } else {
       rotate<LOGN>(v, sh, kp, sidx, t, pol, cptr);
     }

@@ -1,6 +1,6 @@
 """Executable numpy model of the fused kernel's FFT data movement.
 
-A line-by-line restatement of ``conv_pass`` / ``side_index`` /
+A line-by-line restatement of ``fft_fwd`` / ``fft_inv`` / ``side_index`` /
 ``xchg_index`` in paper_1507_00921_b200/csrc/dbp_block_kernel.cuh (thread
 registers, shared-memory exchange addresses, the twiddle table layout of
 ``make_twiddles``), evaluated in complex128.  The CPU tests use it to prove
@@ -85,7 +85,7 @@ def last_pass_bin(g: Geo2, t: int, e: int) -> int:
 
 
 def conv_model2(block: np.ndarray, table: np.ndarray, logn: int, trace=None) -> np.ndarray:
-    """Emulate the kernel's conv_pass<LOGN,0> on one polarisation (table: natural order, 1/N folded)."""
+    """Emulate the kernel's conv_block<LOGN> on one polarisation (table: natural order, 1/N folded)."""
     g = Geo2(logn)
     N, T = g.N, g.T
     tw = twiddles2(g)
