@@ -157,6 +157,33 @@ int64_t dbp_launch_count(void);
  * bench.py uses it as the FP32 roofline denominator.                        */
 int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms);
 
+/* ------------------------------------------------------------------------
+ * Whole-waveform split-step link simulator: the reference's
+ * propagate_span / amplify_with_ase / apply_jones_matrix
+ * (pkg/src/fiberdbp/channel.py:74-153) for a batch of circular waveforms of
+ * n = 2^log2_n samples (n in [2^8, 2^26]).  The simulator owns the device
+ * waveform buffer [item][pol][n] complex64; all calls are synchronous.
+ * ------------------------------------------------------------------------ */
+typedef struct dbp_sim dbp_sim;
+
+int dbp_sim_create(dbp_sim** out, int device, int log2_n, int max_batch);
+int dbp_sim_destroy(dbp_sim* sim);
+int dbp_sim_length(const dbp_sim* sim, int64_t* n);
+int dbp_sim_upload(dbp_sim* sim, const void* h_in, int batch);     /* [batch][2][n] complex64 */
+int dbp_sim_download(dbp_sim* sim, void* h_out, int batch);
+
+/* ``steps`` SSFM steps of one span (channel.py:74-94): per step
+ * x <- ifft(fft(x) exp(-j 2 pi^2 beta2 1e-24 f^2 dz)), then (nonlinear != 0)
+ * x <- x exp(-j gamma dz_eff (|x|^2 + |y|^2)), then x <- x * loss.          */
+int dbp_sim_span(dbp_sim* sim, int batch, double sample_rate, double beta2, double gamma, double dz,
+                 double dz_eff, double loss, int steps, int nonlinear);
+
+/* Span-end amplifier (channel.py:97-153): x <- J (g_amp x + noise) with
+ * ``h_noise`` a host [batch][2][n] complex64 noise realisation (NULL: none)
+ * and ``jones`` one row-major 2x2 complex matrix per waveform, [batch][2][2]
+ * complex as 8 * batch doubles (NULL: no rotation).                         */
+int dbp_sim_amplify(dbp_sim* sim, int batch, double g_amp, const void* h_noise, const double* jones);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,6 +34,16 @@ from .backprop import (
     nonlinear_substep_ssfm,
 )
 
+from .forward import (
+    SsfmStepConfig,
+    amplify_with_ase,
+    apply_jones_matrix,
+    haar_random_unitary,
+    propagate_link,
+    propagate_link_batch,
+    propagate_span,
+    random_polarization_rotation,
+)
 from .training import TrainConfig, TrainResult, load_coefficients, mse, optimize_coefficients, save_coefficients
 
 __version__ = "0.1.0"
@@ -45,5 +55,7 @@ __all__ = [
     "ALGORITHMS", "ARRANGEMENTS", "DbpConfig", "DbpEngine", "backpropagate", "backpropagate_batch",
     "channel_memory_samples", "estimate_channel_memory", "get_engine", "nonlinear_substep_essfm",
     "nonlinear_substep_ssfm", "TrainConfig", "TrainResult", "load_coefficients", "mse",
-    "optimize_coefficients", "save_coefficients", "__version__",
+    "optimize_coefficients", "save_coefficients", "SsfmStepConfig", "amplify_with_ase",
+    "apply_jones_matrix", "haar_random_unitary", "propagate_link", "propagate_link_batch", "propagate_span",
+    "random_polarization_rotation", "__version__",
 ]

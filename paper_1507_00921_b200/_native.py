@@ -48,6 +48,14 @@ SIGNATURES = {
     "dbp_run_coeff_batch": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int64, _c_int64,
                                      _c_void_p]),
     "dbp_run_host_coeff_batch": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64]),
+    "dbp_sim_create": (_c_int, [ctypes.POINTER(_c_void_p), _c_int, _c_int, _c_int]),
+    "dbp_sim_destroy": (_c_int, [_c_void_p]),
+    "dbp_sim_length": (_c_int, [_c_void_p, ctypes.POINTER(_c_int64)]),
+    "dbp_sim_upload": (_c_int, [_c_void_p, _c_void_p, _c_int]),
+    "dbp_sim_download": (_c_int, [_c_void_p, _c_void_p, _c_int]),
+    "dbp_sim_span": (_c_int, [_c_void_p, _c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                              ctypes.c_double, ctypes.c_double, ctypes.c_double, _c_int, _c_int]),
+    "dbp_sim_amplify": (_c_int, [_c_void_p, _c_int, ctypes.c_double, _c_void_p, _c_double_p]),
 }
 
 _lib = None
@@ -239,3 +247,52 @@ class PinnedBuffer:
             self.free()
         except Exception:
             pass
+
+
+class NativeSim:
+    """Owner of one ``dbp_sim`` (whole-waveform SSFM simulator) on one device."""
+
+    def __init__(self, device: int, log2_n: int, max_batch: int):
+        lib = load_library()
+        if device_count() == 0:
+            raise RuntimeError("no CUDA device visible: the B200 simulator has no CPU fallback")
+        h = ctypes.c_void_p()
+        _check(lib.dbp_sim_create(ctypes.byref(h), int(device), int(log2_n), int(max_batch)), "dbp_sim_create")
+        self._h, self._lib = h, lib
+        self.device, self.n, self.max_batch = int(device), 1 << int(log2_n), int(max_batch)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.dbp_sim_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def upload(self, x: np.ndarray):
+        x = np.ascontiguousarray(x, dtype=np.complex64)
+        _check(self._lib.dbp_sim_upload(self._h, x.ctypes.data, int(x.shape[0])), "dbp_sim_upload")
+
+    def download(self, batch: int) -> np.ndarray:
+        out = np.empty((batch, 2, self.n), dtype=np.complex64)
+        _check(self._lib.dbp_sim_download(self._h, out.ctypes.data, int(batch)), "dbp_sim_download")
+        return out
+
+    def span(self, batch, sample_rate, beta2, gamma, dz, dz_eff, loss, steps, nonlinear):
+        _check(self._lib.dbp_sim_span(self._h, int(batch), float(sample_rate), float(beta2), float(gamma),
+                                      float(dz), float(dz_eff), float(loss), int(steps), int(bool(nonlinear))),
+               "dbp_sim_span")
+
+    def amplify(self, batch, g_amp, noise=None, jones=None):
+        nz = None if noise is None else np.ascontiguousarray(noise, dtype=np.complex64)
+        if noise is not None and np.shape(noise) != (batch, 2, self.n):
+            raise ValueError(f"noise must have shape ({batch}, 2, {self.n})")
+        if jones is not None and np.shape(jones) != (batch, 2, 2):
+            raise ValueError(f"jones must have shape ({batch}, 2, 2)")
+        jj = None if jones is None else np.ascontiguousarray(np.asarray(jones, dtype=np.complex128)).view(np.float64)
+        _check(self._lib.dbp_sim_amplify(self._h, int(batch), float(g_amp),
+                                         None if nz is None else nz.ctypes.data,
+                                         None if jj is None else _dptr(jj)), "dbp_sim_amplify")

@@ -105,14 +105,41 @@ struct Geo {
 // pass 0 W_N^{g k} (g < N/R0, k < R0), pass p >= 1 W_{16 S_p}^{ns k}
 // (ns < S_p, k < 16); entry [r][c] = (W^{(2r+1) c}, W^{(2r+2) c}), the
 // second half zero when 2r+2 reaches the radix.
+//
+// Unit complex numbers are rounded to the float pair (within +-1 ulp per
+// component of the nearest) whose squared magnitude is closest to 1, the
+// phase error held to <= 1.5 ulp: a forward twiddle and its conjugate in the
+// inverse transform compose to |w|^2, so the magnitude rounding -- not the
+// phase -- is what a long chain of transform pairs (the 10^3 - 10^4 split
+// steps of a link simulation) accumulates systematically.
+inline float2 unit_float2(double ang) {
+  const double c = std::cos(ang), s = std::sin(ang);
+  const float c0 = (float)c, s0 = (float)s;
+  float2 best = make_float2(c0, s0);
+  double best_mag = std::fabs((double)c0 * c0 + (double)s0 * s0 - 1.0);
+  const double phase_tol = 1.5 * 5.9604644775390625e-8;
+  for (int dc = -1; dc <= 1; ++dc)
+    for (int ds = -1; ds <= 1; ++ds) {
+      float cc = c0, ss = s0;
+      if (dc) cc = std::nextafter(cc, dc > 0 ? 2.f : -2.f);
+      if (ds) ss = std::nextafter(ss, ds > 0 ? 2.f : -2.f);
+      const double mag = std::fabs((double)cc * cc + (double)ss * ss - 1.0);
+      const double dphi = std::fabs(std::atan2(ss * c - cc * s, cc * c + ss * s));
+      if (dphi <= phase_tol && mag < best_mag) {
+        best_mag = mag;
+        best = make_float2(cc, ss);
+      }
+    }
+  return best;
+}
+
 inline std::vector<float2> make_twiddles(int logn) {
   const int np = (logn + 3) / 4;
   const int logr0 = logn - 4 * (np - 1);
   const long long n = 1LL << logn, r0 = 1LL << logr0;
   std::vector<float2> tw;
   auto w = [](long long m, long long period) {
-    const double ang = -2.0 * M_PI * (double)(m % period) / (double)period;
-    return make_float2((float)std::cos(ang), (float)std::sin(ang));
+    return unit_float2(-2.0 * M_PI * (double)(m % period) / (double)period);
   };
   auto table = [&](long long radix, long long cols, long long period) {
     for (long long r = 0; r < radix / 2; ++r)
@@ -284,9 +311,9 @@ __device__ __forceinline__ void twiddle_powers(float2* u, const float2* col) {
 #define DBP_TW_POWERS 1
 #endif
 
-template <int R, bool CONJ, bool FIRST>
+template <int R, bool CONJ, bool FIRST, int TWP>
 __device__ __forceinline__ void twiddle(float2* u, const float2* col, int row_stride) {
-  if constexpr ((DBP_TW_POWERS & (FIRST ? 1 : 2)) != 0) twiddle_powers<R, CONJ>(u, col);
+  if constexpr ((TWP & (FIRST ? 1 : 2)) != 0) twiddle_powers<R, CONJ>(u, col);
   else twiddle_paired<R, CONJ>(u, col, row_stride);
 }
 
@@ -302,6 +329,23 @@ __device__ __forceinline__ void apply_table(float2 (&v)[16], const float2* __res
   }
 }
 
+// v[e] *= (hi + lo) of a double-float table pair (same layout as apply_table):
+// the table's own rounding drops to ~2^-48, for operators applied 10^3+ times
+template <int LOGN>
+__device__ __forceinline__ void apply_table_df(float2 (&v)[16], const float2* __restrict__ hi,
+                                               const float2* __restrict__ lo, int t) {
+#pragma unroll
+  for (int e = 0; e < 16; e += 2) {
+    float2 h0, h1, l0, l1;
+    ldg_table_pair(hi + tab_index(LOGN, t, e), h0, h1);
+    ldg_table_pair(lo + tab_index(LOGN, t, e), l0, l1);
+    const float2 a0 = c_mul(v[e], l0), a1 = c_mul(v[e + 1], l1);
+    v[e] = make_float2(fmaf(v[e].x, h0.x, fmaf(-v[e].y, h0.y, a0.x)), fmaf(v[e].x, h0.y, fmaf(v[e].y, h0.x, a0.y)));
+    v[e + 1] = make_float2(fmaf(v[e + 1].x, h1.x, fmaf(-v[e + 1].y, h1.y, a1.x)),
+                           fmaf(v[e + 1].x, h1.y, fmaf(v[e + 1].y, h1.x, a1.y)));
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Block FFT on one polarisation: fft_fwd walks the decimation-in-frequency
 // passes 0 .. NP-1 (register m of thread t holds block position t + T m on
@@ -309,7 +353,9 @@ __device__ __forceinline__ void apply_table(float2 (&v)[16], const float2* __res
 // exact adjoint walk back (bins in that distribution -> positions t + T m,
 // unscaled).  conv_block = fft_fwd, x table, fft_inv.
 // ---------------------------------------------------------------------------
-template <int LOGN, int P>
+// TWP: which passes build twiddles by powers (DBP_TW_POWERS bits); the link
+// simulator passes 0 (table loads only: powers compound the magnitude error)
+template <int LOGN, int P, int TWP = DBP_TW_POWERS>
 __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
@@ -325,7 +371,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
       dft<R0, false>(u);
-      twiddle<R0, false, true>(u, tw + 2 * (t + T * q), 2 * S0);
+      twiddle<R0, false, true, TWP>(u, tw + 2 * (t + T * q), 2 * S0);
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
@@ -364,7 +410,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
         v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
       }
     }
-    fft_fwd<LOGN, 1>(v, sh, tw, t);
+    fft_fwd<LOGN, 1, TWP>(v, sh, tw, t);
   } else if constexpr (NP >= 3 && P == NP - 2) {
     // second-to-last pass (S = 16) + last pass, joined by a half-warp-local
     // 16 x 16 transpose: half-warp h = t >> 4 owns sub-problem h, lane
@@ -372,7 +418,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
     // lane k of the same half-warp.  The tile [272 h, 272 h + 272) is the
     // region this half-warp alone read in the previous (pad256) exchange.
     dft<16, false>(v);
-    twiddle<16, false, false>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
+    twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
     float2* tile = sh.plane() + 272 * (t >> 4);
     const int l = t & 15;
     DBP_CHECK(272 * (t >> 4) + 272 <= Shm<LOGN>::plane_len());
@@ -387,7 +433,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
     // middle radix-16 pass: group g = t, ns = t mod S_P
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
     dft<16, false>(v);
-    twiddle<16, false, false>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
+    twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
     sh.before_write();
     {
       float2* plane = sh.plane();
@@ -407,13 +453,13 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
         v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
       }
     }
-    fft_fwd<LOGN, P + 1>(v, sh, tw, t);
+    fft_fwd<LOGN, P + 1, TWP>(v, sh, tw, t);
   } else {
     dft<16, false>(v);  // last pass: S = 1, group g = t, bins t + T e
   }
 }
 
-template <int LOGN, int P>
+template <int LOGN, int P, int TWP = DBP_TW_POWERS>
 __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
@@ -423,7 +469,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
   } else if constexpr (P == 0) {
     constexpr int R0 = G::R0, G0 = G::G0, S0 = N / R0;
     constexpr int LS1 = G::log_s(1);
-    fft_inv<LOGN, 1>(v, sh, tw, t);
+    fft_inv<LOGN, 1, TWP>(v, sh, tw, t);
     sh.before_write();
     if constexpr (G::X01_PAIRED) {
       float2* plane = sh.plane() + 272 * (t >> 4) + 2 * (t & 15);
@@ -450,7 +496,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
       float2 u[R0];
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
-      twiddle<R0, true, true>(u, tw + 2 * (t + T * q), 2 * S0);
+      twiddle<R0, true, true, TWP>(u, tw + 2 * (t + T * q), 2 * S0);
       dft<R0, true>(u);
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
@@ -465,11 +511,11 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[l + 17 * k];
-    twiddle<16, true, false>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
+    twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
     dft<16, true>(v);
   } else if constexpr (P < NP - 1) {
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
-    fft_inv<LOGN, P + 1>(v, sh, tw, t);
+    fft_inv<LOGN, P + 1, TWP>(v, sh, tw, t);
     sh.before_write();
     {
       float2* plane = sh.plane();
@@ -483,7 +529,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
-    twiddle<16, true, false>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
+    twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
     dft<16, true>(v);
   } else {
     dft<16, true>(v);  // last pass

@@ -81,6 +81,11 @@ const Dispatch& dispatch() {
 
 }  // namespace
 
+namespace dbp_capi_internal {
+// shared with ssfm_capi.cu: set the thread-local message, return the code
+int fail(int code, const std::string& msg) { return ::fail(code, msg); }
+}  // namespace dbp_capi_internal
+
 struct dbp_plan {
   int device = 0;
   int N = 0, M = 0, logn = 0, step = 0, lead = 0;

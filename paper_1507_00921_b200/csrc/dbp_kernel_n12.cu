@@ -1,5 +1,6 @@
 // Instantiation of the fused DBP block kernel for N = 2^12.
 #include "launch.h"
+#include "ssfm_kernels.cuh"
 
 namespace dbp {
 
@@ -14,6 +15,18 @@ cudaError_t launch_block_kernel<12>(const KernelParams& kp, long long n_ctas, si
     if (e != cudaSuccess) return e;
   }
   dbp_block_kernel<12><<<dim3((unsigned)n_ctas), dim3(launch_shape<12>().threads_x, launch_shape<12>().threads_y), smem_bytes, stream>>>(kp);
+  return cudaGetLastError();
+}
+
+template <>
+cudaError_t launch_ssfm_row<12>(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream) {
+  using G = Geo<12>;
+  if (smem_bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+  }
+  ssfm_row_kernel<12><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
   return cudaGetLastError();
 }
 

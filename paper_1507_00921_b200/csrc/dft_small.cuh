@@ -46,14 +46,28 @@ __device__ __forceinline__ void dft4(float2& a0, float2& a1, float2& a2, float2&
   a3 = c_sub(t1, t3);
 }
 
-// W_16^M of the forward kernel (conjugate for INV) as a compile-time constant
+// W_16^M of the forward kernel (conjugate for INV) as a compile-time constant.
+// The float pairs are not the nearest roundings of (cos, sin): each is within
+// 1 ulp per component (phase error <= 7.3e-8 rad) and chosen for |w|^2, since
+// a transform and its adjoint (the inverse uses conj of the same constants,
+// so phase errors cancel) scale the energy routed through w by |w|^4.  The
+// nearest roundings are all low (|w|^2 - 1 = -5.7e-8 at 22.5 deg, -3.4e-8 at
+// 45 deg): a split-step simulation applying ~10^4 transform pairs drifted by
+// -1e-7 per step in amplitude.  Here M = 1, 5 are +7.5e-9, M = 3, 7 -1.1e-8,
+// M = 2 -3.4e-8 and M = 6 +5.0e-8 (M = 2 and 6 occur equally often in dft8
+// and dft16), so the bias averages to ~1e-9 per use.
 template <bool INV, int M>
 __device__ __forceinline__ float2 w16() {
   constexpr int m = M & 15;
-  constexpr float C1 = 0.92387953251128674f, S1 = 0.38268343236508978f, R2 = 0.70710678118654752f;
-  constexpr float tab_re[16] = {1.f, C1, R2, S1, 0.f, -S1, -R2, -C1, -1.f, -C1, -R2, -S1, 0.f, S1, R2, C1};
-  constexpr float tab_im[16] = {0.f, -S1, -R2, -C1, -1.f, -C1, -R2, -S1, 0.f, S1, R2, C1, 1.f, C1, R2, S1};
-  return make_float2(tab_re[m], INV ? -tab_im[m] : tab_im[m]);
+  constexpr float CA = 0.9238795638084412f, SA = 0.3826833665370941f;   // M = 1, 5: |w|^2 - 1 = +7.5e-9
+  constexpr float CB = 0.9238795042037964f, SB = 0.38268348574638367f;  // M = 3, 7: -1.1e-8
+  constexpr float R2 = 0.7071067690849304f, R2U = 0.7071068286895752f; // M = 2: (R2, R2); M = 6: (R2, R2U)
+  constexpr float tab_re[8] = {1.f, CA, R2, SB, 0.f, -SA, -R2, -CB};
+  constexpr float tab_im[8] = {0.f, -SA, -R2, -CB, -1.f, -CA, -R2U, -SB};
+  // W^(m + 8) = -W^m
+  constexpr float re = m < 8 ? tab_re[m & 7] : -tab_re[m & 7];
+  constexpr float im = m < 8 ? tab_im[m & 7] : -tab_im[m & 7];
+  return make_float2(re, INV ? -im : im);
 }
 
 // (p + w q, p - w q) for w = W_16^M: plain adds for the four trivial roots,

@@ -21,6 +21,11 @@ template <int LOGN>
 cudaError_t launch_block_kernel(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                 cudaStream_t stream);
 
+struct SimParams;
+
+template <int LOGN>
+cudaError_t launch_ssfm_row(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream);
+
 template <int LOGN>
 LaunchShape launch_shape() {
   return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::SEP_FIR};

@@ -1,0 +1,132 @@
+// Whole-waveform split-step Fourier link simulator on sm_100a.
+//
+// Reference: pkg/src/fiberdbp/channel.py:74-94 propagate_span -- per step
+// x <- ifft(fft(x) * exp(-j 2 pi^2 beta2 f^2 dz)); x <- x exp(-j gamma
+// dz_eff (|x|^2 + |y|^2)); x <- x exp(-alpha dz / 2) -- on ONE circular
+// block of n = 2^k samples (2^17 .. 2^21 in the reference experiments), and
+// channel.py:97-153 (amplifier with ASE, Jones rotation) at span ends.
+//
+// n = N1 N2 four-step FFT built from the DBP kernel's block-FFT halves
+// (fft_fwd / fft_inv: radix-16 register DFTs + shared-memory exchanges):
+//
+//   At[n2][n1] = x[n1 N2 + n2]   (N2 rows of length N1)
+//   K_a  row of At : fft_fwd over n1, x W_n^{k1 n2}, store in register order
+//                    (W_n from full tables in both layouts, rounded for |w| ~ 1)
+//   transpose      -> B[p][n2]  (row p = register position of bin k1)
+//   K_b  row of B  : fft_fwd over n2, x Lin[k1 + N1 k2] (1/n folded in),
+//                    fft_inv, x W_n^{-k1 n2}, store natural
+//   transpose      -> At'
+//   K_c  row of At': fft_inv over n1, x e^{-j gamma dz_eff I} x loss, and
+//                    for every step but the last K_a again (fused, mode CA)
+//
+// One SSFM step = two row kernels + two transposes over the waveform, which
+// stays L2-resident for n <= 2^21 (32 MB dual-pol complex64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "dbp_block_kernel.cuh"
+
+namespace dbp {
+
+enum SimMode : int { kSimA = 0, kSimCA = 1, kSimC = 2, kSimB = 3 };
+
+struct SimParams {
+  float2* data;             // rows of row_len samples, [item][pol][rows][row_len]
+  long long pol_stride;     // n
+  long long total_rows;     // rows * items (both polarisations handled per row)
+  int rows;                 // rows per polarisation
+  int log_n;                // log2 n
+  int log_n1;               // log2 N1 (At row length)
+  int mode;                 // SimMode
+  const float2* tw;         // block-FFT twiddles of this row length
+  const float2* wtab;       // W_n^{k1 n2} by row and position (A/CA: [n2][p], B: [p][n2])
+  const float2* lin;        // kSimB: per-row permuted linear table [row][tab_index] ...
+  const float2* lin_lo;     // ... as a double-float pair (hi, lo)
+  float nl_a;               // rotation exp(+j nl_a I) (= -gamma dz_eff)
+  float loss;               // amplitude factor per step ...
+  float loss_last;          // ... and on the span's last step (kSimC), absorbing the
+                            // float rounding of loss^(steps-1): the span gain is then
+                            // exact to one rounding instead of drifting by steps ulp
+  int nonlinear;
+  int slice_floats;
+};
+
+// x e^{-j gamma dz_eff (|x|^2 + |y|^2)} x loss (channel.py:61-71, 93); the
+// partner lane (lane ^ 16) holds the other polarisation of the same sample
+__device__ __forceinline__ void sim_nonlinear(float2 (&v)[16], const SimParams& sp, int pol) {
+  const float loss = sp.mode == kSimC ? sp.loss_last : sp.loss;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const float own = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
+    const float other = __shfl_xor_sync(0xffffffffu, own, 16);
+    const float inten = pol ? other + own : own + other;
+    v[m] = sp.nonlinear ? c_mul(v[m], rot_factor<true>(sp.nl_a, loss, inten))
+                        : make_float2(v[m].x * loss, v[m].y * loss);
+  }
+}
+
+// after fft_fwd over the At row n2: position p = t + T e holds bin k1(p)
+template <int LOGN>
+__device__ __forceinline__ void sim_twiddle_rows(float2 (&v)[16], const float2* __restrict__ w, int t) {
+  constexpr int T = Geo<LOGN>::T;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(w + t + T * e));
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
+ssfm_row_kernel(const SimParams sp) {
+  using G = Geo<LOGN>;
+  constexpr int N = G::N, T = G::T;
+  extern __shared__ float4 smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int pol = lane >> 4;
+  const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);
+  const int t = q % T;
+  const int slice = q / T;
+  Shm<LOGN> sh;
+  sh.base = reinterpret_cast<float*>(smem_raw) + slice * sp.slice_floats;
+  sh.pol = pol;
+
+  const long long gr = (long long)blockIdx.x * G::BPC + slice;
+  const bool active = gr < sp.total_rows;
+  const long long item = active ? gr / sp.rows : 0;
+  const int row = active ? (int)(gr - item * sp.rows) : 0;
+  float2* rp = sp.data + (item * 2 + pol) * sp.pol_stride + (long long)row * N + t;
+
+  // natural (A, B) or register order (CA, C): both are position t + T m
+  float2 v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) v[m] = active ? rp[T * m] : make_float2(0.f, 0.f);
+
+  if (sp.mode == kSimB) {
+    fft_fwd<LOGN, 0, 0>(v, sh, sp.tw, t);
+    apply_table_df<LOGN>(v, sp.lin + (long long)row * N, sp.lin_lo + (long long)row * N, G::NP == 1 ? 0 : t);
+    const int ti = opaque(t);
+    fft_inv<LOGN, 0, 0>(v, sh, sp.tw, ti);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = c_mulc(v[m], ldg_table(sp.wtab + (long long)row * N + ti + T * m));
+  } else {
+    if (sp.mode != kSimA) {
+      fft_inv<LOGN, 0, 0>(v, sh, sp.tw, t);
+      sim_nonlinear(v, sp, pol);
+    }
+    if (sp.mode != kSimC) {
+      // fft_fwd's first exchange skips its leading barrier when the FIR region
+      // is separate (Geo::SEP_FIR); here it follows fft_inv's plane reads
+      if constexpr (G::SEP_FIR) {
+        if (sp.mode == kSimCA) __syncthreads();
+      }
+      const int tf = opaque(t);
+      fft_fwd<LOGN, 0, 0>(v, sh, sp.tw, tf);
+      sim_twiddle_rows<LOGN>(v, sp.wtab + (long long)row * N, tf);
+    }
+  }
+  if (active) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) rp[T * m] = v[m];
+  }
+}
+
+}  // namespace dbp

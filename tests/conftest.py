@@ -28,6 +28,18 @@ def manifest():
     return json.loads((REPO / "tests" / "golden" / "golden_v1.json").read_text())
 
 
+@pytest.fixture(scope="session")
+def golden_fwd():
+    data = np.load(REPO / "tests" / "golden" / "golden_fwd_v1.npz")
+    return {k: data[k] for k in data.files}
+
+
+@pytest.fixture(scope="session")
+def manifest_fwd():
+    import json
+    return json.loads((REPO / "tests" / "golden" / "golden_fwd_v1.json").read_text())
+
+
 @pytest.fixture
 def rng():
     return np.random.default_rng(1234)

@@ -128,3 +128,26 @@ def test_training_port_matches_reference(golden):
     assert iters == ref_iters
     np.testing.assert_allclose([initial, err], [ref_initial, ref_final], rtol=1e-9)
     np.testing.assert_allclose(c, golden["train_c"], rtol=0, atol=1e-9)
+
+
+def test_channel_port_matches_reference_forward_fixtures(golden_fwd, manifest_fwd):
+    # channel.py:74-207 restated in oracle/channel_port.py, pinned to the reference's own outputs
+    from oracle import channel_port as cp
+    for case in manifest_fwd["cases"]:
+        name, x = case["name"], golden_fwd[f"{case['name']}_in"].astype(np.complex128)
+        if case["kind"] == "span":
+            got = cp.span(x, case["sample_rate"], case["beta2"], case["gamma"], case["alpha_db_per_km"],
+                          case["length"], case["steps_per_span"], case["nonlinear"])
+        else:
+            got = cp.link(x, case["sample_rate"], case["beta2"], case["gamma"], case["alpha_db_per_km"],
+                          case["length"], case["num_spans"], case["steps_per_span"], case["amp_gain_db"],
+                          case["amp_noise_figure_db"], case["pol_rotation"], case["center_wavelength_nm"],
+                          case["rng"], case["nonlinear"])
+        want = golden_fwd[f"{name}_out"]
+        tol = 1e-6 if want.dtype == np.complex64 else 1e-12
+        np.testing.assert_allclose(got, want, rtol=0, atol=tol * np.max(np.abs(want)), err_msg=name)
+    x = golden_fwd["amp_in"].astype(np.complex128)
+    np.testing.assert_allclose(cp.amplify(x, 56e9, 16.0, 5.0, 1550.0, 3), golden_fwd["amp_out"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(cp.amplify(x, 56e9, 16.0, None), golden_fwd["amp_quiet_out"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(cp.haar(11), golden_fwd["haar11"], rtol=0, atol=1e-14)
+    np.testing.assert_allclose(cp.haar(5) @ x, golden_fwd["rot_out"], rtol=0, atol=1e-13)

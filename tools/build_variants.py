@@ -14,6 +14,7 @@ VARIANTS = {
     "single": ["-DDBP_DOUBLE_BUFFER=0"],
     "aliasfir": ["-DDBP_SEPARATE_FIR=0"],
     "bounds": ["-DDBP_DEBUG_BOUNDS=1"],
+    "pw0": ["-DDBP_TW_POWERS=0"],
     "pw1": ["-DDBP_TW_POWERS=1"],
     "pw2": ["-DDBP_TW_POWERS=2"],
     "pw3": ["-DDBP_TW_POWERS=3"],

@@ -1,0 +1,89 @@
+"""Throughput of the GPU link simulator against the CPU oracle.
+
+python tools/sim_bench.py [--out profiles/r1/sim_bench.json]
+
+Metric: dual-polarisation sample-steps per second (one SSFM step over one
+complex sample of both polarisations), 80 km spans of 80 steps (1 km, the
+reference experiments' step size), batch 1 waveform, fully device resident;
+each ``dbp_sim_span`` call is timed on the host around the blocking call
+(the call ends with a stream synchronize).  Algorithmic traffic per
+single-polarisation sample per step: 96 bytes (row kernel B: data r+w 16,
+double-float dispersion table 16, W_n table 8; row kernel CA: 16 + W_n 8;
+two transposes 32).  CPU baseline: oracle/channel_port.span (numpy
+complex128 pocketfft, one thread) on a bounded sample.
+"""
+import argparse
+import json
+import math
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--logs", default="14,17,20,21,22")
+    ap.add_argument("--steps", type=int, default=80)
+    ap.add_argument("--reps", type=int, default=5)
+    args = ap.parse_args()
+    import paper_1507_00921_b200 as pb
+    from paper_1507_00921_b200 import _native
+    from paper_1507_00921_b200.forward import _SimCache
+    from oracle import channel_port as cp
+    from oracle.waveforms import d_to_beta2
+
+    beta2 = d_to_beta2(17.0)
+    fiber = pb.FiberParams(beta2, 1.3, 0.2, 80.0)
+    cfg = pb.SsfmStepConfig(args.steps)
+    from paper_1507_00921_b200.forward import _span_args
+    dz, dz_eff, loss = _span_args(fiber, cfg)
+    rows = []
+    peaks = json.loads(Path("MEASURED_PEAKS.json").read_text()) if Path("MEASURED_PEAKS.json").exists() else {}
+    for lg in [int(v) for v in args.logs.split(",")]:
+        n = 1 << lg
+        rng = np.random.default_rng(lg)
+        x = ((rng.normal(size=(1, 2, n)) + 1j * rng.normal(size=(1, 2, n))) * 0.02).astype(np.complex64)
+        sim = _SimCache.get(0, lg, 1)
+        sim.upload(x)
+        launches0 = _native.launch_count()
+        sim.span(1, 56e9, beta2, 1.3, dz, dz_eff, loss, args.steps, True)   # warm-up + tables
+        times = []
+        for _ in range(args.reps):
+            t0 = time.perf_counter()
+            sim.span(1, 56e9, beta2, 1.3, dz, dz_eff, loss, args.steps, True)
+            times.append(time.perf_counter() - t0)
+        t = float(np.median(times))
+        per_step = t / args.steps
+        rate = n * args.steps / t
+        traffic = 96.0 * 2 * n
+        rows.append(dict(log2_n=lg, ms_per_span=t * 1e3, us_per_step=per_step * 1e6,
+                         sample_steps_per_s=rate, effective_GBps=traffic / per_step / 1e9))
+        print(json.dumps(rows[-1]))
+    # CPU oracle on a bounded sample: 2^17 samples, 4 steps
+    n = 1 << 17
+    rng = np.random.default_rng(0)
+    x = (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n))) * 0.02
+    t0 = time.perf_counter()
+    reps = 0
+    while time.perf_counter() - t0 < 10.0:
+        cp.span(x, 56e9, beta2, 1.3, 0.2, 80.0 * 4 / args.steps, 4)
+        reps += 1
+    tc = (time.perf_counter() - t0) / reps
+    cpu = dict(value=n * 4 / tc, unit="sample-steps/s", cores=1, kind="port",
+               sample=f"oracle/channel_port.span, 2^17 samples x 4 steps, {reps} reps")
+    print(json.dumps(dict(cpu_baseline=cpu)))
+    out = dict(metric="link simulator throughput", unit="dual-pol sample-steps/s", steps_per_span=args.steps,
+               span_km=80.0, rows=rows, cpu_baseline=cpu,
+               hbm_peak_GBps=peaks.get("hbm_gbs"))
+    if args.out:
+        Path(args.out).write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
