@@ -184,6 +184,52 @@ int dbp_sim_span(dbp_sim* sim, int batch, double sample_rate, double beta2, doub
  * complex as 8 * batch doubles (NULL: no rotation).                         */
 int dbp_sim_amplify(dbp_sim* sim, int batch, double g_amp, const void* h_noise, const double* jones);
 
+/* ------------------------------------------------------------------------
+ * Post-DBP receiver DSP: pkg/src/fiberdbp/modem.py
+ * butterfly_equalize (:207-271), carrier_recover (:283-351), qpsk_decide
+ * (:116-125) and the counting core of measure_ber (:358-413), in float64,
+ * for a batch of waveforms of 2 n_symbols samples (2 samples/symbol).
+ * Buffers are host memory; every call is synchronous.
+ * ------------------------------------------------------------------------ */
+typedef struct dbp_rx dbp_rx;
+
+int dbp_rx_create(dbp_rx** out, int device, int64_t n_symbols, int max_batch);
+int dbp_rx_destroy(dbp_rx* rx);
+
+/* CMA 2x2 butterfly, T/2 spaced, centre-spike start, ``passes`` circular
+ * sweeps with the collapse re-initialisation of modem.py:259-266.
+ * h_in [batch][2][2 n_symbols] complex128 -> h_out [batch][2][n_symbols]
+ * complex128; reinits[batch] and h_taps [batch][4][taps] (hxx, hxy, hyx,
+ * hyy) complex128 may be NULL.  taps odd, <= 64.                           */
+int dbp_rx_equalize(dbp_rx* rx, const void* h_in, int batch, int taps, double step_size, int passes,
+                    void* h_out, int* reinits, void* h_taps);
+
+/* 4th-power frequency-offset removal, sliding-window phase tracking and (with
+ * h_ref [2][n_symbols] complex128, else NULL) the 90-degree rotation search.
+ * h_sym -> h_out [batch][2][n_symbols] complex128; f_off[batch] (may be NULL);
+ * status[batch] = 1 where the offset sits at the aliasing edge (the
+ * reference's FrequencyOffsetError), else 0.                                */
+int dbp_rx_carrier_recover(dbp_rx* rx, const void* h_sym, int batch, double symbol_rate, const void* h_ref,
+                           int window, void* h_out, double* f_off, int* status);
+
+/* Hard decisions: h_bits [batch][2][2 n_symbols], I and Q bits interleaved. */
+int dbp_rx_decide(dbp_rx* rx, const void* h_sym, int batch, uint8_t* h_bits);
+
+/* Bit errors at the best circular alignment and polarisation pairing:
+ * h_dec [batch][2][2 n_symbols], h_ref [2][2 n_symbols]; errors[batch];
+ * *counted = 2 (n_symbols - ceil(skip_bits / 2)) (BER = errors / (2 counted)). */
+int dbp_rx_count_errors(dbp_rx* rx, const uint8_t* h_dec, int batch, const uint8_t* h_ref, int64_t skip_bits,
+                        int64_t* errors, int64_t* counted);
+
+/* The whole receiver of cli.py:677-685 device-resident: h_in [batch][2][2
+ * n_symbols] complex64 (in_is_c64) or complex128, h_ref_sym [2][n_symbols]
+ * complex128.  metrics[batch][6] = (ber, errors, bits counted, evm %,
+ * frequency offset Hz, re-initialisations); status[batch] = 0 ok, 1
+ * frequency offset at the aliasing edge, 2 no alignment below BER 0.4.     */
+int dbp_rx_chain(dbp_rx* rx, const void* h_in, int in_is_c64, int batch, int taps, double step_size, int passes,
+                 double symbol_rate, const void* h_ref_sym, int window, int64_t skip_bits, double* metrics,
+                 int* status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -44,6 +44,20 @@ from .forward import (
     propagate_span,
     random_polarization_rotation,
 )
+from .rx import (
+    AlignmentError,
+    FrequencyOffsetError,
+    RxMetrics,
+    butterfly_equalize,
+    butterfly_equalize_batch,
+    carrier_recover,
+    carrier_recover_batch,
+    evm_percent,
+    measure_ber,
+    qpsk_decide,
+    qpsk_map,
+    receive_batch,
+)
 from .training import TrainConfig, TrainResult, load_coefficients, mse, optimize_coefficients, save_coefficients
 
 __version__ = "0.1.0"
@@ -57,5 +71,7 @@ __all__ = [
     "nonlinear_substep_ssfm", "TrainConfig", "TrainResult", "load_coefficients", "mse",
     "optimize_coefficients", "save_coefficients", "SsfmStepConfig", "amplify_with_ase",
     "apply_jones_matrix", "haar_random_unitary", "propagate_link", "propagate_link_batch", "propagate_span",
-    "random_polarization_rotation", "__version__",
+    "random_polarization_rotation", "AlignmentError", "FrequencyOffsetError", "RxMetrics", "butterfly_equalize",
+    "butterfly_equalize_batch", "carrier_recover", "carrier_recover_batch", "evm_percent", "measure_ber",
+    "qpsk_decide", "qpsk_map", "receive_batch", "__version__",
 ]

@@ -56,6 +56,17 @@ SIGNATURES = {
     "dbp_sim_span": (_c_int, [_c_void_p, _c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                               ctypes.c_double, ctypes.c_double, ctypes.c_double, _c_int, _c_int]),
     "dbp_sim_amplify": (_c_int, [_c_void_p, _c_int, ctypes.c_double, _c_void_p, _c_double_p]),
+    "dbp_rx_create": (_c_int, [ctypes.POINTER(_c_void_p), _c_int, _c_int64, _c_int]),
+    "dbp_rx_destroy": (_c_int, [_c_void_p]),
+    "dbp_rx_equalize": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, ctypes.c_double, _c_int, _c_void_p,
+                                 ctypes.POINTER(_c_int), _c_void_p]),
+    "dbp_rx_carrier_recover": (_c_int, [_c_void_p, _c_void_p, _c_int, ctypes.c_double, _c_void_p, _c_int,
+                                        _c_void_p, _c_double_p, ctypes.POINTER(_c_int)]),
+    "dbp_rx_decide": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_void_p]),
+    "dbp_rx_count_errors": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_void_p, _c_int64,
+                                     ctypes.POINTER(_c_int64), ctypes.POINTER(_c_int64)]),
+    "dbp_rx_chain": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, _c_int, ctypes.c_double, _c_int,
+                              ctypes.c_double, _c_void_p, _c_int, _c_int64, _c_double_p, ctypes.POINTER(_c_int)]),
 }
 
 _lib = None
@@ -296,3 +307,84 @@ class NativeSim:
         _check(self._lib.dbp_sim_amplify(self._h, int(batch), float(g_amp),
                                          None if nz is None else nz.ctypes.data,
                                          None if jj is None else _dptr(jj)), "dbp_sim_amplify")
+
+
+def _iptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_int))
+
+
+class NativeRx:
+    """Owner of one ``dbp_rx`` (float64 receiver DSP) for waveforms of 2 n_symbols samples."""
+
+    def __init__(self, device: int, n_symbols: int, max_batch: int):
+        lib = load_library()
+        if device_count() == 0:
+            raise RuntimeError("no CUDA device visible: the B200 receiver has no CPU fallback")
+        h = ctypes.c_void_p()
+        _check(lib.dbp_rx_create(ctypes.byref(h), int(device), int(n_symbols), int(max_batch)), "dbp_rx_create")
+        self._h, self._lib = h, lib
+        self.device, self.n_symbols, self.max_batch = int(device), int(n_symbols), int(max_batch)
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.dbp_rx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def equalize(self, x: np.ndarray, taps: int, step_size: float, passes: int, want_taps: bool = False):
+        x = np.ascontiguousarray(x, dtype=np.complex128)
+        b = x.shape[0]
+        out = np.empty((b, 2, self.n_symbols), dtype=np.complex128)
+        reinits = np.zeros(b, dtype=np.int32)
+        tp = np.empty((b, 4, taps), dtype=np.complex128) if want_taps else None
+        _check(self._lib.dbp_rx_equalize(self._h, x.ctypes.data, b, int(taps), float(step_size), int(passes),
+                                          out.ctypes.data, _iptr(reinits), None if tp is None else tp.ctypes.data),
+               "dbp_rx_equalize")
+        return out, reinits, tp
+
+    def carrier_recover(self, s: np.ndarray, symbol_rate: float, reference, window: int):
+        s = np.ascontiguousarray(s, dtype=np.complex128)
+        b = s.shape[0]
+        ref = None if reference is None else np.ascontiguousarray(reference, dtype=np.complex128)
+        out = np.empty_like(s)
+        f_off = np.zeros(b)
+        status = np.zeros(b, dtype=np.int32)
+        _check(self._lib.dbp_rx_carrier_recover(self._h, s.ctypes.data, b, float(symbol_rate),
+                                                None if ref is None else ref.ctypes.data, int(window),
+                                                out.ctypes.data, _dptr(f_off), _iptr(status)),
+               "dbp_rx_carrier_recover")
+        return out, f_off, status
+
+    def decide(self, s: np.ndarray) -> np.ndarray:
+        s = np.ascontiguousarray(s, dtype=np.complex128)
+        bits = np.empty(s.shape[:-1] + (2 * s.shape[-1],), dtype=np.uint8)
+        _check(self._lib.dbp_rx_decide(self._h, s.ctypes.data, s.shape[0], bits.ctypes.data), "dbp_rx_decide")
+        return bits
+
+    def count_errors(self, dec: np.ndarray, ref: np.ndarray, skip_bits: int):
+        dec = np.ascontiguousarray(dec, dtype=np.uint8)
+        ref = np.ascontiguousarray(ref, dtype=np.uint8)
+        b = dec.shape[0]
+        errors = np.zeros(b, dtype=np.int64)
+        counted = ctypes.c_int64()
+        _check(self._lib.dbp_rx_count_errors(self._h, dec.ctypes.data, b, ref.ctypes.data, int(skip_bits),
+                                              errors.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                              ctypes.byref(counted)), "dbp_rx_count_errors")
+        return errors, counted.value
+
+    def chain(self, x: np.ndarray, taps, step_size, passes, symbol_rate, ref_symbols, window, skip_bits):
+        c64 = np.asarray(x).dtype == np.complex64
+        x = np.ascontiguousarray(x, dtype=np.complex64 if c64 else np.complex128)
+        b = x.shape[0]
+        ref = np.ascontiguousarray(ref_symbols, dtype=np.complex128)
+        metrics = np.zeros((b, 6))
+        status = np.zeros(b, dtype=np.int32)
+        _check(self._lib.dbp_rx_chain(self._h, x.ctypes.data, int(c64), b, int(taps), float(step_size), int(passes),
+                                      float(symbol_rate), ref.ctypes.data, int(window), int(skip_bits),
+                                      _dptr(metrics), _iptr(status)), "dbp_rx_chain")
+        return metrics, status

@@ -72,6 +72,7 @@ __global__ void __launch_bounds__(256) ssfm_amplify_kernel(float2* __restrict__ 
 
 namespace dbp_capi_internal {
 int fail(int code, const std::string& msg);
+void add_launches(long long n);
 }
 
 namespace {
@@ -181,6 +182,7 @@ int launch_row(dbp_sim* s, int logn_row, int mode, float2* buf, int batch, const
   const long long ctas = (sp.total_rows + sh.slices - 1) / sh.slices;
   const size_t smem = (size_t)sp.slice_floats * sizeof(float) * sh.slices;
   cudaError_t e = d.row[logn_row](sp, ctas, smem, st);
+  dbp_capi_internal::add_launches(1);
   if (e != cudaSuccess) return fail(DBP_ECUDA, std::string("ssfm_row_kernel: ") + cudaGetErrorString(e));
   return DBP_OK;
 }
@@ -188,6 +190,7 @@ int launch_row(dbp_sim* s, int logn_row, int mode, float2* buf, int batch, const
 int transpose(const float2* in, float2* out, int rows, int cols, int planes, cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32, planes);
   dbp::ssfm_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(in, out, rows, cols);
+  dbp_capi_internal::add_launches(1);
   SIM_CUDA(cudaGetLastError(), "ssfm_transpose_kernel");
   return DBP_OK;
 }
@@ -376,6 +379,7 @@ int dbp_sim_amplify(dbp_sim* s, int batch, double g_amp, const void* h_noise, co
   const long long total = s->n * batch;
   dbp::ssfm_amplify_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(
       s->data, s->n, batch, (float)g_amp, h_noise ? s->noise : nullptr, jones ? s->jones : nullptr);
+  dbp_capi_internal::add_launches(1);
   SIM_CUDA(cudaGetLastError(), "ssfm_amplify_kernel");
   SIM_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   return DBP_OK;

@@ -40,6 +40,18 @@ def manifest_fwd():
     return json.loads((REPO / "tests" / "golden" / "golden_fwd_v1.json").read_text())
 
 
+@pytest.fixture(scope="session")
+def golden_rx():
+    data = np.load(REPO / "tests" / "golden" / "golden_rx_v1.npz")
+    return {k: data[k] for k in data.files}
+
+
+@pytest.fixture(scope="session")
+def manifest_rx():
+    import json
+    return json.loads((REPO / "tests" / "golden" / "golden_rx_v1.json").read_text())
+
+
 @pytest.fixture
 def rng():
     return np.random.default_rng(1234)

@@ -151,3 +151,24 @@ def test_channel_port_matches_reference_forward_fixtures(golden_fwd, manifest_fw
     np.testing.assert_allclose(cp.amplify(x, 56e9, 16.0, None), golden_fwd["amp_quiet_out"], rtol=1e-13, atol=0)
     np.testing.assert_allclose(cp.haar(11), golden_fwd["haar11"], rtol=0, atol=1e-14)
     np.testing.assert_allclose(cp.haar(5) @ x, golden_fwd["rot_out"], rtol=0, atol=1e-13)
+
+
+def test_rx_port_matches_reference_receiver_fixtures(golden_rx, manifest_rx):
+    # modem.py:183-413 restated in oracle/rx_port.py, pinned to the reference's own outputs
+    from oracle import rx_port
+    for case in manifest_rx["cases"]:
+        name = case["name"]
+        eq, reinits, taps = rx_port.equalize(golden_rx[f"{name}_in"])
+        assert reinits == case["reinits"], name
+        np.testing.assert_allclose(eq, golden_rx[f"{name}_eq"], rtol=0, atol=1e-12, err_msg=name)
+        np.testing.assert_allclose(np.stack(taps), golden_rx[f"{name}_taps"], rtol=0, atol=1e-12, err_msg=name)
+        if case.get("equalize_only"):
+            continue
+        rec, _, edge = rx_port.carrier(golden_rx[f"{name}_cr_in"], case["symbol_rate"], golden_rx[f"{name}_ref"],
+                                       case["window"])
+        assert not edge
+        np.testing.assert_allclose(rec, golden_rx[f"{name}_rec"], rtol=0, atol=1e-12, err_msg=name)
+        dec = rx_port.decide(rec)
+        np.testing.assert_array_equal(dec, golden_rx[f"{name}_dec"])
+        errors, counted = rx_port.count_errors(dec, rx_port.decide(golden_rx[f"{name}_ref"]), case["skip_bits"])
+        assert errors / (2 * counted) == case["ber"] and 2 * counted == case["bits_counted"], name
