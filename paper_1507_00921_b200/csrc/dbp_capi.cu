@@ -85,6 +85,7 @@ namespace dbp_capi_internal {
 // shared with ssfm_capi.cu: set the thread-local message, return the code
 int fail(int code, const std::string& msg) { return ::fail(code, msg); }
 void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_total() { return g_launches.load(); }
 }  // namespace dbp_capi_internal
 
 struct dbp_plan {

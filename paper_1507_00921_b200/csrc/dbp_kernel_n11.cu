@@ -19,14 +19,16 @@ cudaError_t launch_block_kernel<11>(const KernelParams& kp, long long n_ctas, si
 }
 
 template <>
-cudaError_t launch_ssfm_row<11>(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream) {
+cudaError_t launch_ssfm_row<11>(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream,
+                                bool column) {
   using G = Geo<11>;
+  if (column) return cudaErrorInvalidValue;   // column tiles only for N1 <= 512
   if (smem_bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<11, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_bytes);
     if (e != cudaSuccess) return e;
   }
-  ssfm_row_kernel<11><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
+  ssfm_row_kernel<11, false><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
   return cudaGetLastError();
 }
 

@@ -19,14 +19,25 @@ cudaError_t launch_block_kernel<5>(const KernelParams& kp, long long n_ctas, siz
 }
 
 template <>
-cudaError_t launch_ssfm_row<5>(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream) {
+cudaError_t launch_ssfm_row<5>(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream,
+                                bool column) {
   using G = Geo<5>;
+  if (column) {
+    smem_bytes = col_smem_bytes<5>(smem_bytes);
+    if (smem_bytes > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem_bytes);
+      if (e != cudaSuccess) return e;
+    }
+    ssfm_row_kernel<5, true><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
+    return cudaGetLastError();
+  }
   if (smem_bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<5, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_bytes);
     if (e != cudaSuccess) return e;
   }
-  ssfm_row_kernel<5><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
+  ssfm_row_kernel<5, false><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
   return cudaGetLastError();
 }
 

@@ -19,14 +19,25 @@ cudaError_t launch_block_kernel<6>(const KernelParams& kp, long long n_ctas, siz
 }
 
 template <>
-cudaError_t launch_ssfm_row<6>(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream) {
+cudaError_t launch_ssfm_row<6>(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream,
+                                bool column) {
   using G = Geo<6>;
+  if (column) {
+    smem_bytes = col_smem_bytes<6>(smem_bytes);
+    if (smem_bytes > 48 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<6, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem_bytes);
+      if (e != cudaSuccess) return e;
+    }
+    ssfm_row_kernel<6, true><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
+    return cudaGetLastError();
+  }
   if (smem_bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(ssfm_row_kernel<6, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem_bytes);
     if (e != cudaSuccess) return e;
   }
-  ssfm_row_kernel<6><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
+  ssfm_row_kernel<6, false><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,8 @@ cudaError_t launch_block_kernel(const KernelParams& kp, long long n_ctas, size_t
 struct SimParams;
 
 template <int LOGN>
-cudaError_t launch_ssfm_row(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream);
+cudaError_t launch_ssfm_row(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream,
+                            bool column);
 
 template <int LOGN>
 LaunchShape launch_shape() {

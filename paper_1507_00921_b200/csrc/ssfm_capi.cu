@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -73,6 +74,7 @@ __global__ void __launch_bounds__(256) ssfm_amplify_kernel(float2* __restrict__ 
 namespace dbp_capi_internal {
 int fail(int code, const std::string& msg);
 void add_launches(long long n);
+long long launch_total();
 }
 
 namespace {
@@ -85,7 +87,7 @@ using dbp_capi_internal::fail;
     if (e_ != cudaSuccess) return fail(DBP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-using RowFn = cudaError_t (*)(const dbp::SimParams&, long long, size_t, cudaStream_t);
+using RowFn = cudaError_t (*)(const dbp::SimParams&, long long, size_t, cudaStream_t, bool);
 using ShapeFn = dbp::LaunchShape (*)();
 
 template <int L>
@@ -121,6 +123,11 @@ struct Guard {
 
 struct dbp_sim {
   int device = 0, log_n = 0, log_n1 = 0, log_n2 = 0, max_batch = 0;
+  // column mode (n <= 2^22): the waveform stays in natural [N1][N2] order,
+  // column kernels with shared-memory tiles do the N1-point transforms, no
+  // global transposes.  Otherwise (or DBP_SIM_TRANSPOSE=1) the transposed
+  // four-step layout with 32 x 33 tile transposes.
+  bool column = false;
   long long n = 0;
   float2* data = nullptr;
   float2* scratch = nullptr;
@@ -135,6 +142,15 @@ struct dbp_sim {
   double lin_key[3] = {0, 0, 0};
   bool lin_valid = false;
   cudaStream_t stream = nullptr;
+  // one CUDA graph per span configuration: a span is 4 launches per step, so
+  // small waveforms are launch-bound; the graph replays the whole span
+  struct SpanGraph {
+    int batch, steps, nonlinear;
+    float nl_a, loss, loss_last;
+    cudaGraphExec_t exec;
+    long long launches;
+  };
+  std::vector<SpanGraph> graphs;
 };
 
 namespace {
@@ -168,7 +184,7 @@ void make_four_step_twiddles(int log_n, int log_n1, std::vector<float2>& wa, std
 }
 
 int launch_row(dbp_sim* s, int logn_row, int mode, float2* buf, int batch, const dbp::SimParams& base,
-               cudaStream_t st) {
+               cudaStream_t st, bool column = false) {
   const SimDispatch& d = sim_dispatch();
   const dbp::LaunchShape sh = d.shape[logn_row]();
   dbp::SimParams sp = base;
@@ -176,12 +192,14 @@ int launch_row(dbp_sim* s, int logn_row, int mode, float2* buf, int batch, const
   sp.mode = mode;
   sp.rows = (int)(s->n >> logn_row);
   sp.total_rows = (long long)sp.rows * batch;
+  sp.n2 = 1 << s->log_n2;
   sp.tw = logn_row == s->log_n1 ? s->tw1 : s->tw2;
   sp.wtab = mode == dbp::kSimB ? s->wb : s->wa;
   sp.slice_floats = dbp::slice_floats(1 << logn_row, 0, false);
-  const long long ctas = (sp.total_rows + sh.slices - 1) / sh.slices;
+  // row kernels: one row per slice; column kernels: one tile of ``slices`` columns per CTA
+  const long long ctas = column ? (long long)batch * (sp.n2 / sh.slices) : (sp.total_rows + sh.slices - 1) / sh.slices;
   const size_t smem = (size_t)sp.slice_floats * sizeof(float) * sh.slices;
-  cudaError_t e = d.row[logn_row](sp, ctas, smem, st);
+  cudaError_t e = d.row[logn_row](sp, ctas, smem, st, column);
   dbp_capi_internal::add_launches(1);
   if (e != cudaSuccess) return fail(DBP_ECUDA, std::string("ssfm_row_kernel: ") + cudaGetErrorString(e));
   return DBP_OK;
@@ -247,11 +265,26 @@ int dbp_sim_create(dbp_sim** out, int device, int log2_n, int max_batch) {
   s->device = device;
   s->log_n = log2_n;
   s->n = 1LL << log2_n;
-  s->log_n2 = (log2_n + 1) / 2;
-  s->log_n1 = log2_n - s->log_n2;
-  if (s->log_n2 > dbp::kMaxLogN) {
-    s->log_n2 = dbp::kMaxLogN;
+  const char* force_t = std::getenv("DBP_SIM_TRANSPOSE");
+  // Column tiles are BPC(N1) = 2048 / N1 columns wide, so N2 >= 2048 / N1,
+  // i.e. n >= 2^11.  Split measured on B200 (tools/sim_sweep.sh,
+  // profiles/r1/sim_sweep.txt): N1 = 2^7 up to 2^14, 2^8 up to 2^20, 2^9 at
+  // 2^21; from 2^22 the transposed layout is faster (32-byte column rows).
+  s->column = log2_n >= 11 && log2_n <= 21 && !(force_t && force_t[0] == '1');
+  const char* force_l1 = std::getenv("DBP_SIM_LOGN1");   // tuning experiments
+  if (s->column) {
+    s->log_n1 = log2_n <= 14 ? std::min(7, log2_n - 4) : log2_n <= 20 ? 8 : 9;
+    if (force_l1 && std::atoi(force_l1) >= dbp::kMinLogN && std::atoi(force_l1) <= 9 &&
+        log2_n - std::atoi(force_l1) <= dbp::kMaxLogN && log2_n - std::atoi(force_l1) >= 11 - std::atoi(force_l1))
+      s->log_n1 = std::atoi(force_l1);
+    s->log_n2 = log2_n - s->log_n1;
+  } else {
+    s->log_n2 = (log2_n + 1) / 2;
     s->log_n1 = log2_n - s->log_n2;
+    if (s->log_n2 > dbp::kMaxLogN) {
+      s->log_n2 = dbp::kMaxLogN;
+      s->log_n1 = log2_n - s->log_n2;
+    }
   }
   s->max_batch = max_batch;
   const size_t bytes = (size_t)max_batch * 2 * s->n * sizeof(float2);
@@ -260,7 +293,8 @@ int dbp_sim_create(dbp_sim** out, int device, int log2_n, int max_batch) {
     dbp_sim_destroy(s);
     return code;
   };
-  if (cudaMalloc(&s->data, bytes) != cudaSuccess || cudaMalloc(&s->scratch, bytes) != cudaSuccess ||
+  if (cudaMalloc(&s->data, bytes) != cudaSuccess ||
+      (!s->column && cudaMalloc(&s->scratch, bytes) != cudaSuccess) ||
       cudaMalloc(&s->noise, bytes) != cudaSuccess ||
       cudaMalloc(&s->jones, (size_t)max_batch * 4 * sizeof(float2)) != cudaSuccess)
     return cleanup(fail(DBP_ENOMEM, "device allocation of the waveform buffers failed"));
@@ -292,6 +326,7 @@ int dbp_sim_destroy(dbp_sim* s) {
   cudaFree(s->wb);
   cudaFree(s->lin);
   cudaFree(s->lin_lo);
+  for (auto& gr : s->graphs) cudaGraphExecDestroy(gr.exec);
   if (s->stream) cudaStreamDestroy(s->stream);
   delete s;
   return DBP_OK;
@@ -341,18 +376,61 @@ int dbp_sim_span(dbp_sim* s, int batch, double sample_rate, double beta2, double
   base.nonlinear = nonlinear ? 1 : 0;
   const int n1 = 1 << s->log_n1, n2 = 1 << s->log_n2, planes = 2 * batch;
   cudaStream_t st = s->stream;
-  // natural [N1][N2] -> At [N2][N1], first column FFT
-  if ((rc = transpose(s->data, s->scratch, n1, n2, planes, st))) return rc;
-  if ((rc = launch_row(s, s->log_n1, dbp::kSimA, s->scratch, batch, base, st))) return rc;
-  for (int k = 0; k < steps; ++k) {
-    if ((rc = transpose(s->scratch, s->data, n2, n1, planes, st))) return rc;   // -> B [N1][N2]
-    if ((rc = launch_row(s, s->log_n2, dbp::kSimB, s->data, batch, base, st))) return rc;
-    if ((rc = transpose(s->data, s->scratch, n1, n2, planes, st))) return rc;   // -> At
-    if ((rc = launch_row(s, s->log_n1, k + 1 < steps ? dbp::kSimCA : dbp::kSimC, s->scratch, batch, base,
-                         st)))
+  auto enqueue = [&]() -> int {
+    int r;
+    if (s->column) {   // natural layout throughout: column (N1) and row (N2) kernels in place
+      if ((r = launch_row(s, s->log_n1, dbp::kSimA, s->data, batch, base, st, true))) return r;
+      for (int k = 0; k < steps; ++k) {
+        if ((r = launch_row(s, s->log_n2, dbp::kSimB, s->data, batch, base, st))) return r;
+        if ((r = launch_row(s, s->log_n1, k + 1 < steps ? dbp::kSimCA : dbp::kSimC, s->data, batch, base, st,
+                            true)))
+          return r;
+      }
+      return DBP_OK;
+    }
+    // natural [N1][N2] -> At [N2][N1], first column FFT
+    if ((r = transpose(s->data, s->scratch, n1, n2, planes, st))) return r;
+    if ((r = launch_row(s, s->log_n1, dbp::kSimA, s->scratch, batch, base, st))) return r;
+    for (int k = 0; k < steps; ++k) {
+      if ((r = transpose(s->scratch, s->data, n2, n1, planes, st))) return r;   // -> B [N1][N2]
+      if ((r = launch_row(s, s->log_n2, dbp::kSimB, s->data, batch, base, st))) return r;
+      if ((r = transpose(s->data, s->scratch, n1, n2, planes, st))) return r;   // -> At
+      if ((r = launch_row(s, s->log_n1, k + 1 < steps ? dbp::kSimCA : dbp::kSimC, s->scratch, batch, base, st)))
+        return r;
+    }
+    return transpose(s->scratch, s->data, n2, n1, planes, st);                 // -> natural
+  };
+  dbp_sim::SpanGraph* gr = nullptr;
+  for (auto& g2 : s->graphs)
+    if (g2.batch == batch && g2.steps == steps && g2.nonlinear == base.nonlinear && g2.nl_a == base.nl_a &&
+        g2.loss == base.loss && g2.loss_last == base.loss_last)
+      gr = &g2;
+  if (!gr) {
+    if (s->graphs.size() >= 8) {
+      cudaGraphExecDestroy(s->graphs.front().exec);
+      s->graphs.erase(s->graphs.begin());
+    }
+    SIM_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    const long long before = dbp_capi_internal::launch_total();
+    rc = enqueue();
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(st, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
       return rc;
+    }
+    SIM_CUDA(ce, "cudaStreamEndCapture");
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    SIM_CUDA(ie, "cudaGraphInstantiate");
+    const long long launches = dbp_capi_internal::launch_total() - before;
+    dbp_capi_internal::add_launches(-launches);   // counted when the graph runs
+    s->graphs.push_back({batch, steps, base.nonlinear, base.nl_a, base.loss, base.loss_last, exec, launches});
+    gr = &s->graphs.back();
   }
-  if ((rc = transpose(s->scratch, s->data, n2, n1, planes, st))) return rc;     // -> natural
+  SIM_CUDA(cudaGraphLaunch(gr->exec, st), "cudaGraphLaunch");
+  dbp_capi_internal::add_launches(gr->launches);
   SIM_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   return DBP_OK;
 }

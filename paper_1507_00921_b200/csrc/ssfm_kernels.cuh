@@ -50,6 +50,7 @@ struct SimParams {
                             // exact to one rounding instead of drifting by steps ulp
   int nonlinear;
   int slice_floats;
+  int n2;                   // column kernels: row stride / number of columns (N2)
 };
 
 // x e^{-j gamma dz_eff (|x|^2 + |y|^2)} x loss (channel.py:61-71, 93); the
@@ -74,11 +75,18 @@ __device__ __forceinline__ void sim_twiddle_rows(float2 (&v)[16], const float2* 
   for (int e = 0; e < 16; ++e) v[e] = c_mul(v[e], ldg_table(w + t + T * e));
 }
 
-template <int LOGN>
+// Row kernels (COL = false): slice s of a CTA owns one contiguous row of
+// ``row_len`` = 2^LOGN samples.  Column kernels (COL = true): the CTA owns a
+// tile of BPC adjacent columns of the natural [N1][N2] layout (column length
+// 2^LOGN = N1, row stride N2), loaded and stored with coalesced row
+// segments through a padded shared-memory tile; slice s then holds column
+// c0 + s in the same register layout as a row, so the four-step FFT needs no
+// global transposes.
+template <int LOGN, bool COL>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
 ssfm_row_kernel(const SimParams sp) {
   using G = Geo<LOGN>;
-  constexpr int N = G::N, T = G::T;
+  constexpr int N = G::N, T = G::T, C = G::BPC;
   extern __shared__ float4 smem_raw[];
   const int lane = threadIdx.x & 31;
   const int pol = lane >> 4;
@@ -89,16 +97,40 @@ ssfm_row_kernel(const SimParams sp) {
   sh.base = reinterpret_cast<float*>(smem_raw) + slice * sp.slice_floats;
   sh.pol = pol;
 
-  const long long gr = (long long)blockIdx.x * G::BPC + slice;
-  const bool active = gr < sp.total_rows;
-  const long long item = active ? gr / sp.rows : 0;
-  const int row = active ? (int)(gr - item * sp.rows) : 0;
-  float2* rp = sp.data + (item * 2 + pol) * sp.pol_stride + (long long)row * N + t;
-
-  // natural (A, B) or register order (CA, C): both are position t + T m
   float2 v[16];
+  bool active;
+  int row;            // W-table row: n2 (A/CA/C) or the register position p (B)
+  float2* rp = nullptr;
+  long long item = 0;
+  int c0 = 0;
+  if constexpr (COL) {
+    // tile = (item, column group); columns c0 .. c0 + C - 1 of both polarisations
+    const long long groups = sp.n2 / C;
+    item = blockIdx.x / groups;
+    c0 = (int)(blockIdx.x - item * groups) * C;
+    active = true;
+    row = c0 + slice;
+    float2* tile = reinterpret_cast<float2*>(smem_raw);
+    const float2* src = sp.data + item * 2 * sp.pol_stride + c0;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < 2 * N * C; i += G::THREADS) {
+      const int c = i % C, r = (i / C) % N, pl = i / (N * C);
+      tile[(pl * N + r) * (C + 1) + c] = src[pl * sp.pol_stride + (long long)r * sp.n2 + c];
+    }
+    __syncthreads();
 #pragma unroll
-  for (int m = 0; m < 16; ++m) v[m] = active ? rp[T * m] : make_float2(0.f, 0.f);
+    for (int m = 0; m < 16; ++m) v[m] = tile[(pol * N + t + T * m) * (C + 1) + slice];
+    __syncthreads();   // the tile region is reused by the FFT exchange planes
+  } else {
+    const long long gr = (long long)blockIdx.x * G::BPC + slice;
+    active = gr < sp.total_rows;
+    item = active ? gr / sp.rows : 0;
+    row = active ? (int)(gr - item * sp.rows) : 0;
+    rp = sp.data + (item * 2 + pol) * sp.pol_stride + (long long)row * N + t;
+    // natural (A, B) or register order (CA, C): both are position t + T m
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = active ? rp[T * m] : make_float2(0.f, 0.f);
+  }
 
   if (sp.mode == kSimB) {
     fft_fwd<LOGN, 0, 0>(v, sh, sp.tw, t);
@@ -123,10 +155,30 @@ ssfm_row_kernel(const SimParams sp) {
       sim_twiddle_rows<LOGN>(v, sp.wtab + (long long)row * N, tf);
     }
   }
-  if (active) {
+  if constexpr (COL) {
+    float2* tile = reinterpret_cast<float2*>(smem_raw);
+    __syncthreads();   // exchange planes -> tile
+#pragma unroll
+    for (int m = 0; m < 16; ++m) tile[(pol * N + t + T * m) * (C + 1) + slice] = v[m];
+    __syncthreads();
+    float2* dst = sp.data + item * 2 * sp.pol_stride + c0;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < 2 * N * C; i += G::THREADS) {
+      const int c = i % C, r = (i / C) % N, pl = i / (N * C);
+      dst[pl * sp.pol_stride + (long long)r * sp.n2 + c] = tile[(pl * N + r) * (C + 1) + c];
+    }
+  } else if (active) {
 #pragma unroll
     for (int m = 0; m < 16; ++m) rp[T * m] = v[m];
   }
+}
+
+// shared memory of a column-kernel CTA: the padded tile or the exchange planes
+template <int LOGN>
+inline size_t col_smem_bytes(size_t planes_bytes) {
+  using G = Geo<LOGN>;
+  const size_t tile = (size_t)2 * G::N * (G::BPC + 1) * sizeof(float2);
+  return tile > planes_bytes ? tile : planes_bytes;
 }
 
 }  // namespace dbp

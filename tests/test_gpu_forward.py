@@ -15,6 +15,7 @@ reference; the GPU is 1.4e-4.
 """
 
 import math
+from pathlib import Path
 
 import numpy as np
 import pytest
@@ -144,3 +145,39 @@ def test_simulator_validation():
                           pb.SsfmStepConfig(2), rng=np.random.default_rng(0))
     with pytest.raises(ValueError):
         pb.SsfmStepConfig(0)
+
+
+def test_transpose_layout_matches_oracle_2_23():
+    # n > 2^22 uses the transposed four-step layout (tile transposes); a 2-step span vs the oracle
+    n = 1 << 23
+    rng = np.random.default_rng(23)
+    amp = math.sqrt(10 ** ((3.0 - 30) / 10) / 4.0)
+    x = (amp * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))).astype(np.complex64)
+    fiber = pb.FiberParams(beta2=-21.7, gamma=1.3, alpha_db_per_km=0.2, length=80.0)
+    got = pb.propagate_span(_sig(x), fiber, pb.SsfmStepConfig(2)).stack()
+    want = cp.span(x.astype(np.complex128), 56e9, -21.7, 1.3, 0.2, 80.0, 2)
+    assert rel_l2(got, want) <= tol(2)
+
+
+def test_forced_transpose_layout_equals_column_layout(tmp_path):
+    # DBP_SIM_TRANSPOSE=1 selects the transposed layout at any n: same results to rounding
+    import subprocess, sys, textwrap
+    script = textwrap.dedent('''
+        import sys, numpy as np
+        sys.path.insert(0, sys.argv[1])
+        import paper_1507_00921_b200 as pb
+        rng = np.random.default_rng(4)
+        x = ((rng.normal(size=(2, 1 << 16)) + 1j * rng.normal(size=(2, 1 << 16))) * 0.02).astype(np.complex64)
+        f = pb.FiberParams(-21.7, 1.3, 0.2, 80.0)
+        y = pb.propagate_span(pb.DualPolSignal(x[0], x[1], 56e9), f, pb.SsfmStepConfig(5)).stack()
+        np.save(sys.argv[2], y)
+    ''')
+    import os
+    root = str(Path(__file__).resolve().parent.parent)
+    outs = []
+    for flag in ("0", "1"):
+        out = tmp_path / f"y{flag}.npy"
+        env = dict(os.environ, DBP_SIM_TRANSPOSE=flag)
+        subprocess.run([sys.executable, "-c", script, root, str(out)], check=True, env=env)
+        outs.append(np.load(out))
+    assert rel_l2(outs[0], outs[1]) <= tol(5)

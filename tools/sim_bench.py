@@ -7,9 +7,10 @@ complex sample of both polarisations), 80 km spans of 80 steps (1 km, the
 reference experiments' step size), batch 1 waveform, fully device resident;
 each ``dbp_sim_span`` call is timed on the host around the blocking call
 (the call ends with a stream synchronize).  Algorithmic traffic per
-single-polarisation sample per step: 96 bytes (row kernel B: data r+w 16,
-double-float dispersion table 16, W_n table 8; row kernel CA: 16 + W_n 8;
-two transposes 32).  CPU baseline: oracle/channel_port.span (numpy
+single-polarisation sample per step: column layout (2^11 <= n <= 2^21) 64
+bytes (row kernel B: data r+w 16, double-float dispersion table 16, W_n
+table 8; column kernel CA: 16 + W_n 8); transposed layout 96 bytes (the
+same plus two transposes, 32).  CPU baseline: oracle/channel_port.span (numpy
 complex128 pocketfft, one thread) on a bounded sample.
 """
 import argparse
@@ -31,6 +32,7 @@ def main():
     ap.add_argument("--logs", default="14,17,20,21,22")
     ap.add_argument("--steps", type=int, default=80)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--batches", default="1")
     args = ap.parse_args()
     import paper_1507_00921_b200 as pb
     from paper_1507_00921_b200 import _native
@@ -46,23 +48,27 @@ def main():
     rows = []
     peaks = json.loads(Path("MEASURED_PEAKS.json").read_text()) if Path("MEASURED_PEAKS.json").exists() else {}
     for lg in [int(v) for v in args.logs.split(",")]:
+      for batch in [int(v) for v in args.batches.split(",")]:
         n = 1 << lg
+        if batch * n > (1 << 24):
+            continue
         rng = np.random.default_rng(lg)
-        x = ((rng.normal(size=(1, 2, n)) + 1j * rng.normal(size=(1, 2, n))) * 0.02).astype(np.complex64)
-        sim = _SimCache.get(0, lg, 1)
+        x = ((rng.normal(size=(batch, 2, n)) + 1j * rng.normal(size=(batch, 2, n))) * 0.02).astype(np.complex64)
+        sim = _SimCache.get(0, lg, batch)
         sim.upload(x)
-        launches0 = _native.launch_count()
-        sim.span(1, 56e9, beta2, 1.3, dz, dz_eff, loss, args.steps, True)   # warm-up + tables
+        sim.span(batch, 56e9, beta2, 1.3, dz, dz_eff, loss, args.steps, True)   # warm-up + tables
         times = []
         for _ in range(args.reps):
             t0 = time.perf_counter()
-            sim.span(1, 56e9, beta2, 1.3, dz, dz_eff, loss, args.steps, True)
+            sim.span(batch, 56e9, beta2, 1.3, dz, dz_eff, loss, args.steps, True)
             times.append(time.perf_counter() - t0)
         t = float(np.median(times))
         per_step = t / args.steps
-        rate = n * args.steps / t
-        traffic = 96.0 * 2 * n
-        rows.append(dict(log2_n=lg, ms_per_span=t * 1e3, us_per_step=per_step * 1e6,
+        rate = batch * n * args.steps / t
+        column = 11 <= lg <= 21 and os.environ.get("DBP_SIM_TRANSPOSE") != "1"
+        traffic = (64.0 if column else 96.0) * 2 * n * batch
+        rows.append(dict(log2_n=lg, batch=batch, layout="column" if column else "transposed",
+                         bytes_per_pol_sample_step=64 if column else 96, ms_per_span=t * 1e3, us_per_step=per_step * 1e6,
                          sample_steps_per_s=rate, effective_GBps=traffic / per_step / 1e9))
         print(json.dumps(rows[-1]))
     # CPU oracle on a bounded sample: 2^17 samples, 4 steps
