@@ -156,6 +156,9 @@ int64_t dbp_launch_count(void);
  * ``iters`` x 16 x 8 FMAs per thread; ``ms`` receives the kernel time.
  * bench.py uses it as the FP32 roofline denominator.                        */
 int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms);
+/* The same with sm_100a's packed FFMA2 (fma.rn.f32x2: two float32 FMAs per
+ * lane per instruction); the FP32 roofline uses the larger of the two.      */
+int dbp_probe_fp32x2_peak(int device, int iters, double* tflops, double* ms);
 
 /* ------------------------------------------------------------------------
  * Whole-waveform split-step link simulator: the reference's

@@ -44,6 +44,8 @@ SIGNATURES = {
     "dbp_launch_count": (_c_int64, []),
     "dbp_probe_fp32_peak": (_c_int, [_c_int, _c_int, ctypes.POINTER(ctypes.c_double),
                                      ctypes.POINTER(ctypes.c_double)]),
+    "dbp_probe_fp32x2_peak": (_c_int, [_c_int, _c_int, ctypes.POINTER(ctypes.c_double),
+                                       ctypes.POINTER(ctypes.c_double)]),
     "dbp_plan_set_coeff_batch": (_c_int, [_c_void_p, _c_double_p, _c_int, _c_int]),
     "dbp_run_coeff_batch": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int64, _c_int64,
                                      _c_void_p]),
@@ -118,6 +120,14 @@ def probe_fp32_peak(device: int = 0, iters: int = 4096) -> tuple[float, float]:
     tf, ms = ctypes.c_double(), ctypes.c_double()
     _check(load_library().dbp_probe_fp32_peak(int(device), int(iters), ctypes.byref(tf), ctypes.byref(ms)),
            "dbp_probe_fp32_peak")
+    return tf.value, ms.value
+
+
+def probe_fp32x2_peak(device: int = 0, iters: int = 4096) -> tuple[float, float]:
+    """(TFLOP/s, ms) of the packed FFMA2 throughput probe on ``device``."""
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    _check(load_library().dbp_probe_fp32x2_peak(int(device), int(iters), ctypes.byref(tf), ctypes.byref(ms)),
+           "dbp_probe_fp32x2_peak")
     return tf.value, ms.value
 
 

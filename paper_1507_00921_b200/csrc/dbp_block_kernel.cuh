@@ -282,9 +282,7 @@ __device__ __forceinline__ void twiddle_paired(float2* u, const float2* col, int
 // pass, bit 1: later passes).  Default 1: the first pass's table is the big
 // one (N/R0 columns); measured +3% (ESSFM) / +3% (FFE) at N = 2048, worst
 // golden-case error 3.4e-6 -> 3.6e-6.  Later passes keep table loads.
-__device__ __forceinline__ float2 c_sqr(float2 a) {
-  return make_float2(fmaf(a.x, a.x, -a.y * a.y), fmaf(a.x, a.y, a.x * a.y));
-}
+__device__ __forceinline__ float2 c_sqr(float2 a) { return c_mul(a, a); }
 
 template <int R, bool CONJ>
 __device__ __forceinline__ void twiddle_powers(float2* u, const float2* col) {

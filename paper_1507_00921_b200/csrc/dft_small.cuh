@@ -11,16 +11,73 @@
 
 namespace dbp {
 
-__device__ __forceinline__ float2 c_add(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 c_sub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// Complex arithmetic on sm_100a's packed FP32 pipe (FADD2 / FMUL2 / FFMA2:
+// one instruction, two lanes of float32, with operand swap / broadcast /
+// half-negate modifiers that ptxas folds from the register pairs below).
+// The kernels are issue-bound, so halving the FP instruction count is the
+// lever; every operation keeps the exact rounding of the scalar form
+// (DBP_F32X2=0), so results are bit-identical either way.
+#ifndef DBP_F32X2
+#define DBP_F32X2 1
+#endif
 
-// a * w (4 FP32 instructions: 2 FMUL + 2 FFMA)
-__device__ __forceinline__ float2 c_mul(float2 a, float2 w) {
-  return make_float2(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x));
+__device__ __forceinline__ unsigned long long f2_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
 }
-// a * conj(w)
+__device__ __forceinline__ float2 f2_unpack(unsigned long long v) {
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+  return make_float2(lo, hi);
+}
+__device__ __forceinline__ unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+__device__ __forceinline__ float2 c_add(float2 a, float2 b) {
+#if DBP_F32X2
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a.x, a.y)), "l"(f2_pack(b.x, b.y)));
+  return f2_unpack(r);
+#else
+  return make_float2(a.x + b.x, a.y + b.y);
+#endif
+}
+__device__ __forceinline__ float2 c_sub(float2 a, float2 b) {
+#if DBP_F32X2
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2_pack(a.x, a.y)), "l"(f2_pack(b.x, b.y)));
+  return f2_unpack(r);
+#else
+  return make_float2(a.x - b.x, a.y - b.y);
+#endif
+}
+
+// a * w = (fma(ax, wx, -(ay wy)), fma(ax, wy, ay wx)): FMUL2 + FFMA2
+__device__ __forceinline__ float2 c_mul(float2 a, float2 w) {
+#if DBP_F32X2
+  const float2 u = f2_unpack(f2_mul(f2_pack(w.y, -w.x), f2_pack(a.y, a.y)));   // (ay wy, -ay wx)
+  return f2_unpack(f2_fma(f2_pack(a.x, a.x), f2_pack(w.x, w.y), f2_pack(-u.x, -u.y)));
+#else
+  return make_float2(fmaf(a.x, w.x, -a.y * w.y), fmaf(a.x, w.y, a.y * w.x));
+#endif
+}
+// a * conj(w) = (fma(ax, wx, ay wy), fma(ay, wx, -(ax wy)))
 __device__ __forceinline__ float2 c_mulc(float2 a, float2 w) {
+#if DBP_F32X2
+  const unsigned long long u = f2_mul(f2_pack(a.y, -a.x), f2_pack(w.y, w.y));   // (ay wy, -ax wy)
+  return f2_unpack(f2_fma(f2_pack(a.x, a.y), f2_pack(w.x, w.x), u));
+#else
   return make_float2(fmaf(a.x, w.x, a.y * w.y), fmaf(a.y, w.x, -a.x * w.y));
+#endif
 }
 
 // multiply by -j (forward kernel) or +j (inverse kernel): a pure register swap
@@ -87,8 +144,15 @@ __device__ __forceinline__ void pm_w16(float2 p, float2 q, float2& plus, float2&
     plus = c_add(p, r); minus = c_sub(p, r);
   } else {
     const float2 w = w16<INV, M>();
+#if DBP_F32X2
+    // inner = (fma(-wy, qy, px), fma(wy, qx, py)); plus = fma(wx, q, inner); minus = 2 p - plus
+    const unsigned long long in = f2_fma(f2_pack(-q.y, q.x), f2_pack(w.y, w.y), f2_pack(p.x, p.y));
+    plus = f2_unpack(f2_fma(f2_pack(q.x, q.y), f2_pack(w.x, w.x), in));
+    minus = f2_unpack(f2_fma(f2_pack(p.x, p.y), f2_pack(2.0f, 2.0f), f2_pack(-plus.x, -plus.y)));
+#else
     plus = make_float2(fmaf(w.x, q.x, fmaf(-w.y, q.y, p.x)), fmaf(w.x, q.y, fmaf(w.y, q.x, p.y)));
     minus = make_float2(fmaf(2.0f, p.x, -plus.x), fmaf(2.0f, p.y, -plus.y));
+#endif
   }
 }
 

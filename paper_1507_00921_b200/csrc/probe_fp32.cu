@@ -13,6 +13,12 @@
 
 namespace {
 
+__device__ __forceinline__ unsigned long long dbp_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+
 __global__ void __launch_bounds__(256) fma_probe_kernel(float* sink, int iters, float a, float b) {
   float r0 = threadIdx.x * 1e-7f, r1 = r0 + 1e-7f, r2 = r0 + 2e-7f, r3 = r0 + 3e-7f;
   float r4 = r0 + 4e-7f, r5 = r0 + 5e-7f, r6 = r0 + 6e-7f, r7 = r0 + 7e-7f;
@@ -27,9 +33,30 @@ __global__ void __launch_bounds__(256) fma_probe_kernel(float* sink, int iters, 
   if (s == 1234.5f) sink[threadIdx.x] = s;  // keep the chain alive
 }
 
-}  // namespace
+// the same with sm_100a's packed FFMA2 (two float32 FMAs per lane per instruction)
+__global__ void __launch_bounds__(256) fma2_probe_kernel(float* sink, int iters, float a, float b) {
+  unsigned long long r[8];
+  const unsigned long long av = dbp_pack(a, a), bv = dbp_pack(b, b);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = dbp_pack(threadIdx.x * 1e-7f + k * 1e-7f, threadIdx.x * 1e-7f + k * 2e-7f);
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(r[k]) : "l"(av), "l"(bv));
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r[k]));
+    s += lo + hi;
+  }
+  if (s == 1234.5f) sink[threadIdx.x] = s;
+}
 
-extern "C" int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms) {
+int probe(int device, int iters, bool packed, double* tflops, double* ms) {
   if (!tflops || iters < 1) return DBP_EINVAL;
   if (cudaSetDevice(device) != cudaSuccess) return DBP_ECUDA;
   int sms = 0;
@@ -40,9 +67,13 @@ extern "C" int dbp_probe_fp32_peak(int device, int iters, double* tflops, double
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int blocks = sms * 8;
-  fma_probe_kernel<<<blocks, 256>>>(sink, iters / 8 + 1, 0.9999f, 1e-7f);  // warm-up
+  auto launch = [&](int it) {
+    if (packed) fma2_probe_kernel<<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
+    else fma_probe_kernel<<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
+  };
+  launch(iters / 8 + 1);  // warm-up
   cudaEventRecord(e0);
-  fma_probe_kernel<<<blocks, 256>>>(sink, iters, 0.9999f, 1e-7f);
+  launch(iters);
   cudaEventRecord(e1);
   cudaError_t err = cudaEventSynchronize(e1);
   float t = 0.f;
@@ -51,8 +82,18 @@ extern "C" int dbp_probe_fp32_peak(int device, int iters, double* tflops, double
   cudaEventDestroy(e1);
   cudaFree(sink);
   if (err != cudaSuccess) return DBP_ECUDA;
-  const double flops = 2.0 * 8.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
+  const double flops = 2.0 * (packed ? 2.0 : 1.0) * 8.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
   *tflops = flops / (t * 1e-3) / 1e12;
   if (ms) *ms = t;
   return DBP_OK;
+}
+
+}  // namespace
+
+extern "C" int dbp_probe_fp32x2_peak(int device, int iters, double* tflops, double* ms) {
+  return probe(device, iters, true, tflops, ms);
+}
+
+extern "C" int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms) {
+  return probe(device, iters, false, tflops, ms);
 }

@@ -15,6 +15,7 @@ VARIANTS = {
     "aliasfir": ["-DDBP_SEPARATE_FIR=0"],
     "bounds": ["-DDBP_DEBUG_BOUNDS=1"],
     "pw0": ["-DDBP_TW_POWERS=0"],
+    "scalar": ["-DDBP_F32X2=0"],
     "pw1": ["-DDBP_TW_POWERS=1"],
     "pw2": ["-DDBP_TW_POWERS=2"],
     "pw3": ["-DDBP_TW_POWERS=3"],
