@@ -279,9 +279,11 @@ __device__ __forceinline__ void twiddle_paired(float2* u, const float2* col, int
 // Same twiddles from ONE 8-byte load of W (row 0 first half) and complex
 // products of depth <= 4 (W^2, W^4, W^8 by squaring): trades L1 table
 // traffic for FP32 work.  Selected per pass by DBP_TW_POWERS (bit 0: first
-// pass, bit 1: later passes).  Default 1: the first pass's table is the big
-// one (N/R0 columns); measured +3% (ESSFM) / +3% (FFE) at N = 2048, worst
-// golden-case error 3.4e-6 -> 3.6e-6.  Later passes keep table loads.
+// pass, bit 1: later passes).  Default 3 since the packed-FP32 complex
+// arithmetic (dft_small.cuh) made the L1 data pipe the co-limiter: +1.3%
+// (ESSFM) / +2.8% (FFE) over 1 at N = 2048, worst golden-case per-block
+// error 1.2e-6 -> 2.2e-6 (tolerance 1e-5).  The link simulator uses table
+// loads only (TWP = 0).
 __device__ __forceinline__ float2 c_sqr(float2 a) { return c_mul(a, a); }
 
 template <int R, bool CONJ>
@@ -306,7 +308,7 @@ __device__ __forceinline__ void twiddle_powers(float2* u, const float2* col) {
 }
 
 #ifndef DBP_TW_POWERS
-#define DBP_TW_POWERS 1
+#define DBP_TW_POWERS 3
 #endif
 
 template <int R, bool CONJ, bool FIRST, int TWP>
