@@ -43,7 +43,7 @@ def main():
     d_in = torch.randn((B, 2, n, 2), generator=gen, device="cuda:0") * amp
     d_out = torch.empty_like(d_in)
     stream = torch.cuda.Stream()
-    peak_tf, _ = _native.probe_fp32_peak(0, 8192)
+    peak_tf = max(_native.probe_fp32_peak(0, 8192)[0], _native.probe_fp32x2_peak(0, 8192)[0])
 
     points = []
     overl = {1024: 768, 2048: 1400, 4096: 1400, 8192: 1400}
