@@ -246,6 +246,25 @@ def test_decisions_and_q_match_oracle(golden, manifest):
         assert q_gpu == q_ref or abs(q_gpu - q_ref) <= 0.02
 
 
+def test_reference_receiver_on_gpu_dbp_output(golden, manifest, golden_rx, manifest_rx):
+    # identical qpsk_decide decisions and |dQ| <= 0.02 dB after the reference's own Rx
+    # chain (butterfly_equalize -> carrier_recover -> qpsk_decide -> measure_ber, cli.py:677-685).
+    # Reference side: the reference DBP output through the reference modem (golden_rx "link").
+    # GPU side: the GPU DBP of the same received waveform through the GPU receiver (rx.py).
+    case = next(c for c in manifest["cases"] if c["name"] == "c0_sym")
+    ref_case = next(c for c in manifest_rx["cases"] if c["name"] == "link")
+    x, c, _ = _case_inputs(golden, case)
+    got = _run(x, case_config(case, c))[0]
+    sym = golden["link_tx_symbols"]
+    eq = pb.butterfly_equalize(pb.DualPolSignal(got[0], got[1], 56e9))
+    rec = pb.carrier_recover(eq.stack(), 28e9, reference=sym)
+    dec = pb.qpsk_decide(rec)
+    np.testing.assert_array_equal(dec, golden_rx["link_dec"])
+    met = pb.measure_ber(dec, pb.qpsk_decide(sym), skip=ref_case["skip_bits"])
+    assert met.ber == ref_case["ber"] and met.bits_counted == ref_case["bits_counted"]
+    assert abs(met.q_factor_db - ref_case["q_db"]) <= 0.02
+
+
 def test_full_size_properties(rng):
     # BASELINE config-3 item size (2^18 samples): linearity of FFE and ESSFM(identity) == SSFM
     n = 1 << 18
