@@ -755,22 +755,13 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
+// One CTA-sized group of blocks (block slices) through the whole program.
 template <int LOGN>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
-dbp_block_kernel(const KernelParams kp) {
+__device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN>& sh, long long grp,
+                                              long long n_groups, int t, int slice, int pol) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
-  extern __shared__ float4 smem_raw[];
-  const int lane = threadIdx.x & 31;
-  const int pol = lane >> 4;
-  const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);  // position-thread index within the CTA
-  const int t = q % T;
-  const int slice = q / T;
-  Shm<LOGN> sh;
-  sh.base = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats;
-  sh.pol = pol;
-
-  const long long blk = (long long)blockIdx.x * G::BPC + slice;
+  const long long blk = grp * G::BPC + slice;
   const bool active = blk < kp.total_blocks;
   long long item = 0, b = 0;
   if (active) {
@@ -806,6 +797,20 @@ dbp_block_kernel(const KernelParams kp) {
   } else {
 #pragma unroll
     for (int m = 0; m < 16; ++m) v[m] = make_float2(0.f, 0.f);
+  }
+  if (grp + gridDim.x < n_groups) {
+    // L2 prefetch of the next group's block: one 128-byte line per thread and polarisation
+    const long long nblk = (grp + gridDim.x) * G::BPC + slice;
+    if (nblk < kp.total_blocks) {
+      const long long nitem = nblk / kp.blocks_per_item;
+      const long long nb = kp.block_begin + (nblk - nitem * kp.blocks_per_item);
+      const long long ns0 = nb * kp.step - kp.lead;
+      if (!kp.cyclic || (ns0 >= 0 && ns0 + N <= kp.n_total)) {
+        const float2* pn = kp.in + nitem * kp.in_item_stride + pol * kp.in_pol_stride +
+                           (kp.cyclic ? ns0 : ns0 - kp.in_origin) + 16 * t;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(pn));
+      }
+    }
   }
 
   // operator program (dbp.py:212-233)
@@ -856,6 +861,34 @@ dbp_block_kernel(const KernelParams kp) {
         __stcs(dst + m * T, v[m]);
       }
     }
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
+dbp_block_kernel(const KernelParams kp) {
+  using G = Geo<LOGN>;
+  constexpr int N = G::N, T = G::T;
+  extern __shared__ float4 smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int pol = lane >> 4;
+  const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);  // position-thread index within the CTA
+  const int t = q % T;
+  const int slice = q / T;
+  Shm<LOGN> sh;
+  sh.base = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats;
+  sh.pol = pol;
+
+  // N <= 4096: one group per CTA (full-size grid).  N = 8192: a persistent
+  // grid strides over the groups, prefetching the next group's input into L2
+  // meanwhile (the launcher sizes it; DBP_PERSISTENT).
+  // (compile-time split: the strided loop costs ~0.5% where it is not used)
+  const long long n_groups = (kp.total_blocks + G::BPC - 1) / G::BPC;
+  if constexpr (LOGN >= 13) {
+    for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x)
+      process_group<LOGN>(kp, sh, grp, n_groups, t, slice, pol);
+  } else {
+    process_group<LOGN>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
   }
 }
 

@@ -10,6 +10,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -159,7 +160,25 @@ int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
   if (ctas > 0x7fffffffLL) return fail(DBP_EINVAL, "too many blocks for one launch");
   const size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices;
   if (smem > 227 * 1024) return fail(DBP_EINVAL, "shared memory per CTA exceeds 227 KB for this block length");
-  cudaError_t e = d.launch[p->logn](kp, ctas, smem, s);
+  // Persistent grid (SMs x resident CTAs, each looping over block groups with
+  // an L2 prefetch of the next): only N = 8192 (one 1024-thread CTA per SM)
+  // gains, +3%; N <= 4096 loses ~10% against the hardware CTA scheduler
+  // (tools/ab_persist.sh).  DBP_PERSISTENT=k overrides (0 = off).
+  static const int env_persistent = [] {
+    const char* v = std::getenv("DBP_PERSISTENT");
+    return v ? std::atoi(v) : -1;
+  }();
+  // only the N = 8192 kernel loops; smaller N always get the full grid
+  const int persistent = p->logn < 13 ? 0 : env_persistent >= 0 ? env_persistent : 1;
+  long long grid = ctas;
+  if (persistent > 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long resident = (long long)sms * sh.min_ctas * persistent;
+    if (resident > 0 && resident < grid) grid = resident;
+  }
+  cudaError_t e = d.launch[p->logn](kp, grid, smem, s);
   if (e != cudaSuccess) return cuda_fail(e, "dbp_block_kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DBP_OK;

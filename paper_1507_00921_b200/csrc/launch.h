@@ -15,6 +15,7 @@ struct LaunchShape {
   int threads_y;  // along y
   int slices;     // block slices per CTA
   bool separate_fir;  // FIR buffers behind the exchange planes (Geo::SEP_FIR)
+  int min_ctas;       // resident CTAs per SM the kernel is built for (Geo::MIN_CTAS)
 };
 
 template <int LOGN>
@@ -29,7 +30,7 @@ cudaError_t launch_ssfm_row(const SimParams& sp, long long n_ctas, size_t smem_b
 
 template <int LOGN>
 LaunchShape launch_shape() {
-  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::SEP_FIR};
+  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::SEP_FIR, Geo<LOGN>::MIN_CTAS};
 }
 
 }  // namespace dbp
