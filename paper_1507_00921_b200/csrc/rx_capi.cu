@@ -104,62 +104,104 @@ __global__ void ext_kernel(const double2* __restrict__ in, long long n, int half
 // One CMA sweep (modem.py:183-204) over the waveforms listed in ``items``:
 // warp w owns waveform items[w]; half-warp h computes output h (x, y) with
 // taps (h_{h x}, h_{h y}); lane j holds taps j + 16 k, k < K.
+constexpr int kCmaChunk = 32;                     // symbols per staged chunk
+constexpr int kCmaWin = 2 * kCmaChunk + 64;       // samples per polarisation window (taps <= 64)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+
+// One CMA sweep (modem.py:183-204) over the waveforms listed in ``items``:
+// warp w owns waveform items[w]; half-warp h computes output h (x, y) with
+// taps (h_{h x}, h_{h y}); lane j holds taps j + 16 k, k < K.  The input
+// window of the next 32 symbols is staged into shared memory with cp.async
+// while the current chunk runs, so the per-symbol recursion only sees
+// shared-memory latency (an L2 round trip is longer than one symbol update).
 template <int K>
 __global__ void __launch_bounds__(128) cma_kernel(const double2* __restrict__ ext, long long ext_len,
                                                   double2* __restrict__ taps_buf, int taps, double mu,
                                                   long long m, double2* __restrict__ out,
                                                   const int* __restrict__ items, int n_items) {
+  __shared__ double2 win[4][2][2][kCmaWin];   // [warp][buffer][pol][sample]
   const int w = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
   if (w >= n_items) return;
   const int b = items[w];
-  const int lane = threadIdx.x & 31, h = lane >> 4, j = lane & 15;
+  const int lane = threadIdx.x & 31, h = lane >> 4, j = lane & 15, wl = threadIdx.x >> 5;
   const double2* ex = ext + (long long)b * 2 * ext_len;
-  const double2* ey = ex + ext_len;
   double2* tb = taps_buf + (long long)b * 4 * taps;
-  double2 h1[K], h2[K], ux[K], uy[K];
+  double2 h1[K], h2[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     const int i = j + 16 * k;
     const bool ok = i < taps;
     h1[k] = ok ? tb[(2 * h) * taps + i] : make_double2(0.0, 0.0);
     h2[k] = ok ? tb[(2 * h + 1) * taps + i] : make_double2(0.0, 0.0);
-    ux[k] = ok ? ex[i] : make_double2(0.0, 0.0);
-    uy[k] = ok ? ey[i] : make_double2(0.0, 0.0);
   }
   double2* o = out + ((long long)b * 2 + h) * m;
-  for (long long n = 0; n < m; ++n) {
-    double2 nx[K], ny[K];
-    const long long nb = 2 * (n + 1);
+  const long long nch = (m + kCmaChunk - 1) / kCmaChunk;
+  auto stage = [&](long long c) {   // ext[2 c CH, + 2 CH + taps - 1) of both polarisations -> buffer c & 1
+    const long long s0 = 2 * c * kCmaChunk;
+    long long len = 2 * kCmaChunk + taps - 1;
+    if (s0 + len > ext_len) len = ext_len - s0;
+    for (int e = lane; e < 2 * len; e += 32) {
+      const int pl = e >= len ? 1 : 0;
+      const int r = pl ? (int)(e - len) : e;
+      cp_async16(&win[wl][c & 1][pl][r], ex + pl * ext_len + s0 + r);
+    }
+  };
+  stage(0);
+  asm volatile("cp.async.commit_group;");
+  for (long long c = 0; c < nch; ++c) {
+    if (c + 1 < nch) stage(c + 1);
+    asm volatile("cp.async.commit_group;");
+    asm volatile("cp.async.wait_group 1;");
+    __syncwarp();
+    const double2(*wx) = win[wl][c & 1][0];
+    const double2(*wy) = win[wl][c & 1][1];
+    const long long n0 = c * kCmaChunk;
+    const int cnt = (int)(m - n0 < kCmaChunk ? m - n0 : kCmaChunk);
+    double2 ux[K], uy[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int i = j + 16 * k;
-      const bool ok = i < taps && n + 1 < m;
-      nx[k] = ok ? ex[nb + i] : make_double2(0.0, 0.0);
-      ny[k] = ok ? ey[nb + i] : make_double2(0.0, 0.0);
+      ux[k] = i < taps ? wx[i] : make_double2(0.0, 0.0);
+      uy[k] = i < taps ? wy[i] : make_double2(0.0, 0.0);
     }
-    double ar = 0.0, ai = 0.0;
+    for (int n = 0; n < cnt; ++n) {
+      double2 nx[K], ny[K];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      ar += (h1[k].x * ux[k].x - h1[k].y * ux[k].y) + (h2[k].x * uy[k].x - h2[k].y * uy[k].y);
-      ai += (h1[k].x * ux[k].y + h1[k].y * ux[k].x) + (h2[k].x * uy[k].y + h2[k].y * uy[k].x);
-    }
+      for (int k = 0; k < K; ++k) {
+        const int i = j + 16 * k;
+        const bool ok = i < taps && n + 1 < cnt;
+        nx[k] = ok ? wx[2 * (n + 1) + i] : make_double2(0.0, 0.0);
+        ny[k] = ok ? wy[2 * (n + 1) + i] : make_double2(0.0, 0.0);
+      }
+      double ar = 0.0, ai = 0.0;
 #pragma unroll
-    for (int off = 8; off; off >>= 1) {
-      ar += __shfl_xor_sync(0xffffffffu, ar, off);
-      ai += __shfl_xor_sync(0xffffffffu, ai, off);
-    }
-    const double a = mu * (1.0 - (ar * ar + ai * ai));
-    const double er = a * ar, ei = a * ai;
+      for (int k = 0; k < K; ++k) {
+        ar += (h1[k].x * ux[k].x - h1[k].y * ux[k].y) + (h2[k].x * uy[k].x - h2[k].y * uy[k].y);
+        ai += (h1[k].x * ux[k].y + h1[k].y * ux[k].x) + (h2[k].x * uy[k].y + h2[k].y * uy[k].x);
+      }
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      h1[k].x += er * ux[k].x + ei * ux[k].y;   // e * conj(u)
-      h1[k].y += ei * ux[k].x - er * ux[k].y;
-      h2[k].x += er * uy[k].x + ei * uy[k].y;
-      h2[k].y += ei * uy[k].x - er * uy[k].y;
-      ux[k] = nx[k];
-      uy[k] = ny[k];
+      for (int off = 8; off; off >>= 1) {
+        ar += __shfl_xor_sync(0xffffffffu, ar, off);
+        ai += __shfl_xor_sync(0xffffffffu, ai, off);
+      }
+      const double a = mu * (1.0 - (ar * ar + ai * ai));
+      const double er = a * ar, ei = a * ai;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        h1[k].x += er * ux[k].x + ei * ux[k].y;   // e * conj(u)
+        h1[k].y += ei * ux[k].x - er * ux[k].y;
+        h2[k].x += er * uy[k].x + ei * uy[k].y;
+        h2[k].y += ei * uy[k].x - er * uy[k].y;
+        ux[k] = nx[k];
+        uy[k] = ny[k];
+      }
+      if (j == 0) o[n0 + n] = make_double2(ar, ai);
     }
-    if (j == 0) o[n] = make_double2(ar, ai);
+    __syncwarp();   // every lane is done with this buffer before it is refilled
   }
 #pragma unroll
   for (int k = 0; k < K; ++k) {
