@@ -233,6 +233,24 @@ int dbp_rx_chain(dbp_rx* rx, const void* h_in, int in_is_c64, int batch, int tap
                  double symbol_rate, const void* h_ref_sym, int window, int64_t skip_bits, double* metrics,
                  int* status);
 
+/* ------------------------------------------------------------------------
+ * Device-side residual algebra of the coefficient fit (train.py:130-178).
+ * d_out: [sets][2][n_total] complex64 DBP outputs of coefficient sets,
+ * d_target / d_base: [2][n_total] complex64 (fine-step target, output of the
+ * current coefficients); residuals are (out - target) * scale on samples
+ * [w0, w1) of both polarisations, real and imaginary parts, in float64.
+ * Synchronous on ``stream``; results are host arrays.
+ * ------------------------------------------------------------------------ */
+/* h_sums[s] = || r_s ||^2 (line search). */
+int dbp_fit_sumsq(const void* d_out, int n_sets, int64_t n_total, const void* d_target, int64_t w0, int64_t w1,
+                  double scale, double* h_sums, void* stream);
+/* Gauss-Newton normal equations with central differences: sets i and
+ * n_params + i hold c + h e_i and c - h e_i; J_i = (r_{+i} - r_{-i}) / (2 h);
+ * h_ata [n_params][n_params] = J^T J, h_atr [n_params] = J^T r(base).       */
+int dbp_fit_normal(const void* d_out, int n_params, int64_t n_total, const void* d_target, const void* d_base,
+                   int64_t w0, int64_t w1, double scale, double fd_step, double* h_ata, double* h_atr,
+                   void* stream);
+
 #ifdef __cplusplus
 }
 #endif

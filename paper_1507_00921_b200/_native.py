@@ -58,6 +58,10 @@ SIGNATURES = {
     "dbp_sim_span": (_c_int, [_c_void_p, _c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                               ctypes.c_double, ctypes.c_double, ctypes.c_double, _c_int, _c_int]),
     "dbp_sim_amplify": (_c_int, [_c_void_p, _c_int, ctypes.c_double, _c_void_p, _c_double_p]),
+    "dbp_fit_sumsq": (_c_int, [_c_void_p, _c_int, _c_int64, _c_void_p, _c_int64, _c_int64, ctypes.c_double,
+                               _c_double_p, _c_void_p]),
+    "dbp_fit_normal": (_c_int, [_c_void_p, _c_int, _c_int64, _c_void_p, _c_void_p, _c_int64, _c_int64,
+                                ctypes.c_double, ctypes.c_double, _c_double_p, _c_double_p, _c_void_p]),
     "dbp_rx_create": (_c_int, [ctypes.POINTER(_c_void_p), _c_int, _c_int64, _c_int]),
     "dbp_rx_destroy": (_c_int, [_c_void_p]),
     "dbp_rx_equalize": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, ctypes.c_double, _c_int, _c_void_p,
@@ -239,6 +243,12 @@ class NativePlan:
         _check(self._lib.dbp_run_host_coeff_batch(self._h, h_in.ctypes.data, h_out.ctypes.data, int(n_total)),
                "dbp_run_host_coeff_batch")
 
+    def run_coeff_batch(self, d_in: int, d_out: int, n_total: int, stream: int = 0):
+        """Device buffers: d_in [2][n] complex64, d_out [n_sets][2][n] complex64 (async on ``stream``)."""
+        nb = self.num_blocks(n_total)
+        _check(self._lib.dbp_run_coeff_batch(self._h, d_in, d_out, int(n_total), 0, int(nb), stream or None),
+               "dbp_run_coeff_batch")
+
     def synchronize(self):
         _check(self._lib.dbp_plan_synchronize(self._h), "dbp_plan_synchronize")
 
@@ -398,3 +408,21 @@ class NativeRx:
                                       float(symbol_rate), ref.ctypes.data, int(window), int(skip_bits),
                                       _dptr(metrics), _iptr(status)), "dbp_rx_chain")
         return metrics, status
+
+
+def fit_sumsq(d_out: int, n_sets: int, n_total: int, d_target: int, w0: int, w1: int, scale: float,
+              stream: int = 0) -> np.ndarray:
+    out = np.zeros(n_sets)
+    _check(load_library().dbp_fit_sumsq(d_out, int(n_sets), int(n_total), d_target, int(w0), int(w1), float(scale),
+                                        _dptr(out), stream or None), "dbp_fit_sumsq")
+    return out
+
+
+def fit_normal(d_out: int, n_params: int, n_total: int, d_target: int, d_base: int, w0: int, w1: int,
+               scale: float, fd_step: float, stream: int = 0) -> tuple[np.ndarray, np.ndarray]:
+    ata = np.zeros((n_params, n_params))
+    atr = np.zeros(n_params)
+    _check(load_library().dbp_fit_normal(d_out, int(n_params), int(n_total), d_target, d_base, int(w0), int(w1),
+                                         float(scale), float(fd_step), _dptr(ata), _dptr(atr), stream or None),
+           "dbp_fit_normal")
+    return ata, atr

@@ -12,7 +12,11 @@ the same waveform (``dbp_run_host_coeff_batch``: per-item coefficient sets,
 shared input), the Jacobian uses all 2(N_c+1) central-difference
 perturbations at once and the line search evaluates eight step scales per
 launch, accepting the first improving scale in the reference's halving
-order.
+order.  The outputs of every coefficient set stay on the device: the
+squared residual norms (line search) and the Gauss-Newton normal equations
+J^T J, J^T r (float64) are reduced there (``dbp_fit_sumsq`` /
+``dbp_fit_normal``, csrc/fit_capi.cu), so an iteration moves (N_c+2)(N_c+1)
+numbers over PCIe instead of the outputs.
 
 Float32 note: the reference's forward difference with h = 1e-6
 (train.py:148) is below the float32 noise floor of a DBP output (~1e-7
@@ -28,6 +32,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from . import _native
 from .backprop import DbpConfig, backpropagate_batch, get_engine
 from .params import DualPolSignal, EssfmCoefficients
 
@@ -83,31 +88,67 @@ class TrainResult:
     iterations: int
 
 
-class _BatchEvaluator:
-    """Residuals of many coefficient vectors on one waveform, one launch per batch."""
+class _DeviceEvaluator:
+    """DBP outputs of many coefficient vectors on one waveform, kept on the device.
+
+    ``run`` is one launch for a batch of sets (dbp_run_coeff_batch); ``sumsq``
+    and ``normal`` reduce the residuals (out - target)[window] * scale on the
+    device (dbp_fit_sumsq / dbp_fit_normal); ``keep`` makes one set's output
+    the base the next Jacobian's residual r refers to.
+    """
 
     def __init__(self, prefix: np.ndarray, sample_rate: float, dbp_cfg: DbpConfig, n_coeffs: int,
-                 target: np.ndarray, window: slice, device: int):
+                 target: np.ndarray, window: slice, device: int, max_sets: int):
+        import torch
+
         geo = DbpConfig("essfm", dbp_cfg.plan, dbp_cfg.link, num_steps=dbp_cfg.num_steps,
                         coeffs=EssfmCoefficients.identity(n_coeffs), arrangement=dbp_cfg.arrangement)
         self.engine = get_engine(geo, sample_rate, device)
-        self.prefix = np.ascontiguousarray(prefix.astype(np.complex64))
         self.n = prefix.shape[1]
-        self.t_win = target[:, window]
-        self.scale = 1.0 / np.sqrt(np.sum(np.abs(self.t_win) ** 2))
-        self.window = window
+        dev = torch.device("cuda", device)
+
+        def upload(a):
+            return torch.from_numpy(np.ascontiguousarray(a.astype(np.complex64)).view(np.float32)).to(dev)
+
+        self.d_in = upload(prefix)
+        self.d_target = upload(target)
+        self.d_out = torch.empty((max_sets, 2, 2 * self.n), dtype=torch.float32, device=dev)
+        self.d_base = torch.empty((2, 2 * self.n), dtype=torch.float32, device=dev)
+        self.stream = torch.cuda.Stream(device=dev)
+        self.w0, self.w1 = window.start, window.stop
+        t_win = target[:, window].astype(np.complex128)
+        self.scale = 1.0 / np.sqrt(np.sum(np.abs(t_win) ** 2))
+        self.max_sets = max_sets
         self.launches = 0
 
-    def residuals(self, sets: np.ndarray) -> np.ndarray:
+    def run(self, sets: np.ndarray) -> int:
         sets = np.atleast_2d(np.asarray(sets, dtype=np.float64))
-        out = np.empty((sets.shape[0], 2, self.n), dtype=np.complex64)
+        if sets.shape[0] > self.max_sets:
+            raise ValueError("too many coefficient sets for the evaluator")
         plan = self.engine.native
         with plan.lock:
             plan.set_coeff_batch(sets)
-            plan.run_host_coeff_batch(self.prefix, out, self.n)
+            plan.run_coeff_batch(self.d_in.data_ptr(), self.d_out.data_ptr(), self.n, self.stream.cuda_stream)
         self.launches += 1
-        d = (out[:, :, self.window].astype(np.complex128) - self.t_win[None]) * self.scale
-        return np.concatenate([d.real.reshape(len(sets), -1), d.imag.reshape(len(sets), -1)], axis=1)
+        return sets.shape[0]
+
+    def sumsq(self, n_sets: int) -> np.ndarray:
+        return _native.fit_sumsq(self.d_out.data_ptr(), n_sets, self.n, self.d_target.data_ptr(), self.w0, self.w1,
+                                 self.scale, self.stream.cuda_stream)
+
+    def normal(self, n_params: int, fd_step: float):
+        return _native.fit_normal(self.d_out.data_ptr(), n_params, self.n, self.d_target.data_ptr(),
+                                  self.d_base.data_ptr(), self.w0, self.w1, self.scale, fd_step,
+                                  self.stream.cuda_stream)
+
+    def keep(self, k: int):
+        with torch_stream(self.stream):
+            self.d_base.copy_(self.d_out[k], non_blocking=True)
+
+
+def torch_stream(stream):
+    import torch
+    return torch.cuda.stream(stream)
 
 
 def optimize_coefficients(received: DualPolSignal, dbp_cfg: DbpConfig, train_cfg: TrainConfig, *,
@@ -132,19 +173,22 @@ def optimize_coefficients(received: DualPolSignal, dbp_cfg: DbpConfig, train_cfg
     if np.sum(np.abs(target[:, window]) ** 2) == 0.0:
         raise ValueError("fine-step target is identically zero on the fit window")
 
-    ev = _BatchEvaluator(prefix, received.sample_rate, dbp_cfg, train_cfg.n_coeffs, target, window, dev)
+    n_params = train_cfg.n_coeffs + 1
+    ev = _DeviceEvaluator(prefix, received.sample_rate, dbp_cfg, train_cfg.n_coeffs, target, window, dev,
+                          max_sets=max(2 * n_params, line_search_batch))
     c = EssfmCoefficients.identity(train_cfg.n_coeffs).c.copy()
-    r = ev.residuals(c)[0]
-    err = float(r @ r)
+    ev.run(c)
+    err = float(ev.sumsq(1)[0])
+    ev.keep(0)
     initial_err = err
     eye = np.eye(c.size) * fd_step
 
     converged = False
     iterations = 0
     for _ in range(train_cfg.max_iterations):
-        rr = ev.residuals(np.concatenate([c + eye, c - eye]))      # 2 (Nc+1) sets, one launch
-        jac = (rr[:c.size] - rr[c.size:]).T / (2.0 * fd_step)
-        step, *_ = np.linalg.lstsq(jac, -r, rcond=None)
+        ev.run(np.concatenate([c + eye, c - eye]))                  # 2 (Nc+1) sets, one launch
+        ata, atr = ev.normal(c.size, fd_step)                        # J^T J, J^T r on the device
+        step, *_ = np.linalg.lstsq(ata, -atr, rcond=None)
 
         scales = []
         s = 1.0
@@ -155,13 +199,14 @@ def optimize_coefficients(received: DualPolSignal, dbp_cfg: DbpConfig, train_cfg
         for i0 in range(0, len(scales), line_search_batch):
             trial = scales[i0:i0 + line_search_batch]
             cand = np.stack([c + sc * step for sc in trial])
-            r_cand = ev.residuals(cand)
-            errs = np.einsum("ij,ij->i", r_cand, r_cand)
+            ev.run(cand)
+            errs = ev.sumsq(len(trial))
             hit = np.nonzero(errs < err)[0]
             if hit.size:
                 k = int(hit[0])                      # first improving scale in halving order
                 improvement = (err - errs[k]) / err
-                c, r, err = cand[k], r_cand[k], float(errs[k])
+                c, err = cand[k], float(errs[k])
+                ev.keep(k)
                 iterations += 1
                 accepted = True
                 if improvement < train_cfg.tolerance:
