@@ -103,6 +103,12 @@ def main():
     arrays["bits8"] = ref_modem.qpsk_decide(ref)
     _, ref = modulate_pm_qpsk(TxConfig(num_symbols=2 ** 10, rng_seed=9))
     arrays["bits9"] = ref_modem.qpsk_decide(ref)
+    # transmitter and laser phase noise (modem.py:90-180, channel.py:156-171)
+    sig, ref = modulate_pm_qpsk(TxConfig(num_symbols=2 ** 8, rng_seed=8))
+    arrays["tx_nrz"], arrays["tx_nrz_ref"] = sig.stack(), ref
+    sig, ref = modulate_pm_qpsk(TxConfig(num_symbols=2 ** 8, rng_seed=9, pulse="rc", rolloff=0.2))
+    arrays["tx_rc"], arrays["tx_rc_ref"] = sig.stack(), ref
+    arrays["laser_out"] = apply_laser_phase_noise(sig, 100e3, rng=11).stack()
     np.savez_compressed(OUT, **arrays)
     MANIFEST.write_text(json.dumps(dict(generator="tests/golden/make_golden_rx.py",
                                         reference="fiberdbp " + fiberdbp.__version__,

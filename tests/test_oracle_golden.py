@@ -172,3 +172,17 @@ def test_rx_port_matches_reference_receiver_fixtures(golden_rx, manifest_rx):
         np.testing.assert_array_equal(dec, golden_rx[f"{name}_dec"])
         errors, counted = rx_port.count_errors(dec, rx_port.decide(golden_rx[f"{name}_ref"]), case["skip_bits"])
         assert errors / (2 * counted) == case["ber"] and 2 * counted == case["bits_counted"], name
+
+
+def test_modem_port_matches_reference_transmitter(golden_rx):
+    # modem.py:90-180 and channel.py:156-171 restated in oracle/modem_port.py
+    from oracle import modem_port as mp
+    wave, ref = mp.modulate_pm_qpsk(2 ** 8, 8)
+    np.testing.assert_array_equal(ref, golden_rx["tx_nrz_ref"])
+    np.testing.assert_array_equal(wave, golden_rx["tx_nrz"])
+    wave, ref = mp.modulate_pm_qpsk(2 ** 8, 9, pulse="rc", rolloff=0.2)
+    np.testing.assert_array_equal(ref, golden_rx["tx_rc_ref"])
+    np.testing.assert_allclose(wave, golden_rx["tx_rc"], rtol=0, atol=1e-15)
+    np.testing.assert_allclose(mp.laser_phase_noise(wave, 100e3, 56e9, rng=11), golden_rx["laser_out"],
+                               rtol=0, atol=1e-13)
+    assert mp.generate_prbs(7, 1).size == 127 and abs(int(mp.generate_prbs(7, 1).sum()) - 64) == 0
