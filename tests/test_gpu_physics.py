@@ -242,3 +242,78 @@ def test_single_step_enhanced_dbp_rivals_twenty_step_plain():         # test_acc
     for p in powers:
         assert med["essfm1"][p] <= med["ssfm1"][p] and med["essfm1"][p] <= med["ffe"][p], p
     assert min(med["essfm1"].values()) <= 1.5 * min(med["ssfm20"].values())
+
+
+# ---- test_train.py -------------------------------------------------------------------------
+
+TRAIN_PLAN = pb.OverlapPlan(2048, 512)
+
+
+def received(link, power_dbm=2.0, num_symbols=2 ** 12, seed=13):
+    x, _ = waveform(num_symbols, seed, power_dbm)
+    return x, pb.propagate_link(sig(x), link, pb.SsfmStepConfig(40), rng=None)
+
+
+def test_linear_link_needs_no_enhancement():                           # test_train.py:55-64
+    link = quiet_link(2, pb.FiberParams(beta2=-21.0, gamma=0.0, alpha_db_per_km=0.2, length=40.0))
+    _, rx = received(link)
+    res = pb.optimize_coefficients(rx, pb.DbpConfig("ssfm", TRAIN_PLAN, link, num_steps=2),
+                                   pb.TrainConfig(n_coeffs=4, train_samples=4096))
+    # float32 DBP of the same linear operator at two step counts: agreement at float32 rounding
+    assert res.initial_mse < 1e-11
+    assert res.final_mse <= res.initial_mse
+
+
+def test_single_coefficient_matches_scalar_search():                   # test_train.py:67-92
+    link = quiet_link(2)
+    _, rx = received(link, power_dbm=4.0)
+    res = pb.optimize_coefficients(rx, pb.DbpConfig("ssfm", TRAIN_PLAN, link, num_steps=2),
+                                   pb.TrainConfig(n_coeffs=0, train_samples=4096, target_steps_per_span=8))
+    prefix = rx.stack()[:, :4096]
+    target = dbp(prefix, pb.DbpConfig("ssfm", TRAIN_PLAN, link, num_steps=8 * link.num_spans)).astype(np.complex128)
+    window = slice(256, 4096 - 256)
+
+    def objective(c0):
+        out = dbp(prefix, pb.DbpConfig("essfm", TRAIN_PLAN, link, num_steps=2,
+                                       coeffs=pb.EssfmCoefficients([c0]))).astype(np.complex128)
+        return float(np.sum(np.abs((out - target)[:, window]) ** 2))
+
+    lo, hi = 0.0, 2.0                                                  # golden-section search (oracles.py)
+    g = (math.sqrt(5.0) - 1.0) / 2.0
+    a, b = hi - g * (hi - lo), lo + g * (hi - lo)
+    fa, fb = objective(a), objective(b)
+    while hi - lo > 1e-6:
+        if fa < fb:
+            hi, b, fb = b, a, fa
+            a = hi - g * (hi - lo)
+            fa = objective(a)
+        else:
+            lo, a, fa = a, b, fb
+            b = lo + g * (hi - lo)
+            fb = objective(b)
+    best = 0.5 * (lo + hi)
+    assert res.coefficients.c[0] == pytest.approx(best, abs=1e-4)
+    assert objective(res.coefficients.c[0]) <= objective(1.0)
+
+
+def test_training_never_hurts_and_usually_helps():                    # test_train.py:95-110
+    link = quiet_link(3)
+    x, rx = received(link, power_dbm=3.0)
+    cfg = pb.DbpConfig("ssfm", TRAIN_PLAN, link, num_steps=3)
+    res = pb.optimize_coefficients(rx, cfg, pb.TrainConfig(n_coeffs=8, train_samples=8192))
+    assert res.final_mse <= res.initial_mse
+    assert res.final_mse < 0.8 * res.initial_mse
+    assert res.iterations >= 1
+    plain = pb.backpropagate(rx, cfg).stack()
+    trained = pb.backpropagate(rx, pb.DbpConfig("essfm", TRAIN_PLAN, link, num_steps=3,
+                                                coeffs=res.coefficients)).stack()
+    assert pb.mse(trained, x) < pb.mse(plain, x)
+
+
+def test_training_respects_iteration_budget():                         # test_train.py:125-132
+    link = quiet_link(2)
+    _, rx = received(link, power_dbm=4.0)
+    res = pb.optimize_coefficients(rx, pb.DbpConfig("ssfm", TRAIN_PLAN, link, num_steps=2),
+                                   pb.TrainConfig(n_coeffs=4, train_samples=4096, max_iterations=1))
+    assert isinstance(res, pb.TrainResult)
+    assert res.iterations <= 1 and res.final_mse <= res.initial_mse
