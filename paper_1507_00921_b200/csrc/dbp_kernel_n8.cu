@@ -29,7 +29,8 @@ cudaError_t launch_ssfm_row<8>(const SimParams& sp, long long n_ctas, size_t sme
                                            (int)smem_bytes);
       if (e != cudaSuccess) return e;
     }
-    ssfm_row_kernel<8, true><<<dim3((unsigned)n_ctas), dim3(G::THREADS), smem_bytes, stream>>>(sp);
+    ssfm_row_kernel<8, true><<<dim3((unsigned)n_ctas), dim3(SimShape<8, true>::THREADS), smem_bytes,
+                                  stream>>>(sp);
     return cudaGetLastError();
   }
   if (smem_bytes > 48 * 1024) {

@@ -196,9 +196,10 @@ int launch_row(dbp_sim* s, int logn_row, int mode, float2* buf, int batch, const
   sp.tw = logn_row == s->log_n1 ? s->tw1 : s->tw2;
   sp.wtab = mode == dbp::kSimB ? s->wb : s->wa;
   sp.slice_floats = dbp::slice_floats(1 << logn_row, 0, false);
-  // row kernels: one row per slice; column kernels: one tile of ``slices`` columns per CTA
-  const long long ctas = column ? (long long)batch * (sp.n2 / sh.slices) : (sp.total_rows + sh.slices - 1) / sh.slices;
-  const size_t smem = (size_t)sp.slice_floats * sizeof(float) * sh.slices;
+  // row kernels: one row per slice; column kernels: one tile of col_width columns per CTA
+  const int slices = column ? dbp::col_width(logn_row) : sh.slices;
+  const long long ctas = column ? (long long)batch * (sp.n2 / slices) : (sp.total_rows + slices - 1) / slices;
+  const size_t smem = (size_t)sp.slice_floats * sizeof(float) * slices;
   cudaError_t e = d.row[logn_row](sp, ctas, smem, st, column);
   dbp_capi_internal::add_launches(1);
   if (e != cudaSuccess) return fail(DBP_ECUDA, std::string("ssfm_row_kernel: ") + cudaGetErrorString(e));
@@ -273,7 +274,7 @@ int dbp_sim_create(dbp_sim** out, int device, int log2_n, int max_batch) {
   s->column = log2_n >= 11 && log2_n <= 21 && !(force_t && force_t[0] == '1');
   const char* force_l1 = std::getenv("DBP_SIM_LOGN1");   // tuning experiments
   if (s->column) {
-    s->log_n1 = log2_n <= 14 ? std::min(7, log2_n - 4) : log2_n <= 20 ? 8 : 9;
+    s->log_n1 = log2_n <= 14 ? std::min(7, log2_n - 4) : log2_n <= 20 ? 8 : 9;   // N2 <= 2^13
     if (force_l1 && std::atoi(force_l1) >= dbp::kMinLogN && std::atoi(force_l1) <= 9 &&
         log2_n - std::atoi(force_l1) <= dbp::kMaxLogN && log2_n - std::atoi(force_l1) >= 11 - std::atoi(force_l1))
       s->log_n1 = std::atoi(force_l1);

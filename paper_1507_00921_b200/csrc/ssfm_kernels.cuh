@@ -82,11 +82,23 @@ __device__ __forceinline__ void sim_twiddle_rows(float2 (&v)[16], const float2* 
 // segments through a padded shared-memory tile; slice s then holds column
 // c0 + s in the same register layout as a row, so the four-step FFT needs no
 // global transposes.
+// Column tile width: the block-FFT slice count 2048 / N1.  (8 columns at
+// N1 = 512 -- 64-byte row segments, 512-thread CTAs -- measured no faster
+// than 4: 2^21 73.0 vs 68.6 us per step, tools/sim_sweep2.sh.)
+__host__ __device__ constexpr int col_width(int logn) { return 1 << (11 - logn); }
+
 template <int LOGN, bool COL>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
+struct SimShape {
+  static constexpr int C = COL ? col_width(LOGN) : Geo<LOGN>::BPC;   // slices per CTA
+  static constexpr int THREADS = 2 * Geo<LOGN>::T * C;
+  static constexpr int MIN_CTAS = threads_per_sm(LOGN) / THREADS > 0 ? threads_per_sm(LOGN) / THREADS : 1;
+};
+
+template <int LOGN, bool COL>
+__global__ void __launch_bounds__(SimShape<LOGN, COL>::THREADS, SimShape<LOGN, COL>::MIN_CTAS)
 ssfm_row_kernel(const SimParams sp) {
   using G = Geo<LOGN>;
-  constexpr int N = G::N, T = G::T, C = G::BPC;
+  constexpr int N = G::N, T = G::T, C = SimShape<LOGN, COL>::C, THREADS = SimShape<LOGN, COL>::THREADS;
   extern __shared__ float4 smem_raw[];
   const int lane = threadIdx.x & 31;
   const int pol = lane >> 4;
@@ -113,7 +125,7 @@ ssfm_row_kernel(const SimParams sp) {
     float2* tile = reinterpret_cast<float2*>(smem_raw);
     const float2* src = sp.data + item * 2 * sp.pol_stride + c0;
 #pragma unroll 4
-    for (int i = threadIdx.x; i < 2 * N * C; i += G::THREADS) {
+    for (int i = threadIdx.x; i < 2 * N * C; i += THREADS) {
       const int c = i % C, r = (i / C) % N, pl = i / (N * C);
       tile[(pl * N + r) * (C + 1) + c] = src[pl * sp.pol_stride + (long long)r * sp.n2 + c];
     }
@@ -163,7 +175,7 @@ ssfm_row_kernel(const SimParams sp) {
     __syncthreads();
     float2* dst = sp.data + item * 2 * sp.pol_stride + c0;
 #pragma unroll 4
-    for (int i = threadIdx.x; i < 2 * N * C; i += G::THREADS) {
+    for (int i = threadIdx.x; i < 2 * N * C; i += THREADS) {
       const int c = i % C, r = (i / C) % N, pl = i / (N * C);
       dst[pl * sp.pol_stride + (long long)r * sp.n2 + c] = tile[(pl * N + r) * (C + 1) + c];
     }
@@ -177,7 +189,7 @@ ssfm_row_kernel(const SimParams sp) {
 template <int LOGN>
 inline size_t col_smem_bytes(size_t planes_bytes) {
   using G = Geo<LOGN>;
-  const size_t tile = (size_t)2 * G::N * (G::BPC + 1) * sizeof(float2);
+  const size_t tile = (size_t)2 * G::N * (col_width(LOGN) + 1) * sizeof(float2);
   return tile > planes_bytes ? tile : planes_bytes;
 }
 
