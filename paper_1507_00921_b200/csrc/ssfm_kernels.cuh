@@ -127,11 +127,17 @@ ssfm_row_kernel(const SimParams sp) {
 #pragma unroll 4
     for (int i = threadIdx.x; i < 2 * N * C; i += THREADS) {
       const int c = i % C, r = (i / C) % N, pl = i / (N * C);
+      DBP_CHECK((pl * N + r) * (C + 1) + c < 2 * N * (C + 1));
+      DBP_CHECK(item * 2 * sp.pol_stride + c0 + pl * sp.pol_stride + (long long)r * sp.n2 + c <
+                (item + 1) * 2 * sp.pol_stride);
       tile[(pl * N + r) * (C + 1) + c] = src[pl * sp.pol_stride + (long long)r * sp.n2 + c];
     }
     __syncthreads();
 #pragma unroll
-    for (int m = 0; m < 16; ++m) v[m] = tile[(pol * N + t + T * m) * (C + 1) + slice];
+    for (int m = 0; m < 16; ++m) {
+      DBP_CHECK((pol * N + t + T * m) * (C + 1) + slice < 2 * N * (C + 1));
+      v[m] = tile[(pol * N + t + T * m) * (C + 1) + slice];
+    }
     __syncthreads();   // the tile region is reused by the FFT exchange planes
   } else {
     const long long gr = (long long)blockIdx.x * G::BPC + slice;
