@@ -110,3 +110,54 @@ def test_train_config_validation_and_coefficient_files(tmp_path):   # test_train
     with pytest.raises(ValueError):
         pb.load_coefficients(tmp_path / "bad.txt")
     assert pb.mse(np.ones((2, 4)), np.ones((2, 4))) == 0.0
+
+
+def test_receiver_and_simulator_validation_before_any_gpu_work():
+    # argument checks mirror modem.py / channel.py and raise before a device is touched
+    x = np.ones((2, 64), dtype=np.complex128)
+    s = pb.DualPolSignal(x[0], x[1], 56e9)
+    with pytest.raises(ValueError):
+        pb.butterfly_equalize(s, taps=14)
+    with pytest.raises(ValueError):
+        pb.butterfly_equalize(s, step_size=0.0)
+    with pytest.raises(ValueError):
+        pb.butterfly_equalize(s, passes=0)
+    with pytest.raises(ValueError):
+        pb.butterfly_equalize(pb.DualPolSignal(np.ones(15, complex), np.ones(15, complex), 2e9))
+    with pytest.raises(ValueError):
+        pb.carrier_recover(np.ones(16, dtype=complex), 28e9)
+    with pytest.raises(ValueError):
+        pb.carrier_recover(np.ones((2, 16), dtype=complex), 28e9, window=0)
+    with pytest.raises(ValueError):
+        pb.carrier_recover(np.ones((2, 16), dtype=complex), 0.0)
+    bits = np.zeros((2, 8), dtype=np.uint8)
+    with pytest.raises(ValueError):
+        pb.measure_ber(bits[:, :6], bits)
+    with pytest.raises(ValueError):
+        pb.measure_ber(bits, bits, skip=-1)
+    with pytest.raises(ValueError):
+        pb.SsfmStepConfig(0)
+    span = pb.FiberParams(-21.0, 1.3, 0.2, 40.0)
+    with pytest.raises(ValueError):
+        pb.propagate_span(pb.DualPolSignal(np.ones(1000, complex), np.ones(1000, complex), 56e9), span,
+                          pb.SsfmStepConfig(2))
+    with pytest.raises(ValueError):
+        pb.propagate_link(s, pb.LinkConfig(span=span, num_spans=1), pb.SsfmStepConfig(1),
+                          rng=np.random.default_rng(0))
+    with pytest.raises(ValueError):
+        pb.amplify_with_ase(s, -1.0, None)
+    u = pb.haar_random_unitary(3)
+    np.testing.assert_allclose(u @ u.conj().T, np.eye(2), atol=1e-12)
+
+
+def test_gpu_entry_points_fail_loudly_without_a_device():
+    # no CPU fallback: on a machine without a CUDA device the simulator / receiver refuse to run
+    from paper_1507_00921_b200 import _native
+    if _native.device_count() > 0:
+        pytest.skip("a CUDA device is visible")
+    x = np.ones((2, 1024), dtype=np.complex64)
+    with pytest.raises(RuntimeError):
+        pb.propagate_span(pb.DualPolSignal(x[0], x[1], 56e9), pb.FiberParams(-21.0, 1.3, 0.2, 40.0),
+                          pb.SsfmStepConfig(1))
+    with pytest.raises(RuntimeError):
+        pb.butterfly_equalize(pb.DualPolSignal(x[0], x[1], 56e9))
