@@ -48,6 +48,9 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
   return logn <= 10 ? 512 : (logn == 11 ? 768 : 1024);
 #endif
 }
+#ifndef DBP_EXPERIMENT_NOBAR
+#define DBP_EXPERIMENT_NOBAR 0
+#endif
 #ifndef DBP_CTA_POSITIONS
 #define DBP_CTA_POSITIONS 128
 #endif
@@ -255,11 +258,17 @@ struct Shm {
     constexpr int N = Geo<LOGN>::N;
     return base + (Geo<LOGN>::SEP_FIR ? 4 * (N + N / 16) : 0);
   }
+#if DBP_EXPERIMENT_NOBAR   // timing experiment only: exchange barriers removed (WRONG results)
+  __device__ __forceinline__ void before_first_write() const { __syncwarp(); }
+  __device__ __forceinline__ void before_write() const { __syncwarp(); }
+  __device__ __forceinline__ void after_write() const { __syncwarp(); }
+#else
   __device__ __forceinline__ void before_first_write() const {
     if constexpr (!Geo<LOGN>::SEP_FIR) __syncthreads();
   }
   __device__ __forceinline__ void before_write() const { __syncthreads(); }
   __device__ __forceinline__ void after_write() const { __syncthreads(); }
+#endif
 };
 
 // u[k] *= W (or conj W) for k = 1 .. R-1 from a k-paired table column
