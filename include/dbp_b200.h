@@ -251,6 +251,16 @@ int dbp_fit_normal(const void* d_out, int n_params, int64_t n_total, const void*
                    int64_t w0, int64_t w1, double scale, double fd_step, double* h_ata, double* h_atr,
                    void* stream);
 
+/* Float64 DFT along the last axis of a [batch][n] complex128 host array
+ * (spectral.py:37-48: forward unnormalised, inverse x 1/n; n a power of two),
+ * a cuFFT Z2Z library transform -- API completeness, not the DBP path.       */
+int dbp_fft_c2c(int device, const void* h_in, void* h_out, int64_t n, int64_t batch, int inverse);
+
+/* Laser phase noise (channel.py:156-171): out = in exp(j cumsum(incr)) for a
+ * [2][n] complex128 waveform; ``incr`` are the host-drawn Wiener increments
+ * (the reference's seeded normal draws), so a seeded run is reproduced.      */
+int dbp_phase_noise(int device, const void* h_in, const double* h_incr, void* h_out, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,8 @@ SIGNATURES = {
                                _c_double_p, _c_void_p]),
     "dbp_fit_normal": (_c_int, [_c_void_p, _c_int, _c_int64, _c_void_p, _c_void_p, _c_int64, _c_int64,
                                 ctypes.c_double, ctypes.c_double, _c_double_p, _c_double_p, _c_void_p]),
+    "dbp_fft_c2c": (_c_int, [_c_int, _c_void_p, _c_void_p, _c_int64, _c_int64, _c_int]),
+    "dbp_phase_noise": (_c_int, [_c_int, _c_void_p, _c_double_p, _c_void_p, _c_int64]),
     "dbp_rx_create": (_c_int, [ctypes.POINTER(_c_void_p), _c_int, _c_int64, _c_int]),
     "dbp_rx_destroy": (_c_int, [_c_void_p]),
     "dbp_rx_equalize": (_c_int, [_c_void_p, _c_void_p, _c_int, _c_int, ctypes.c_double, _c_int, _c_void_p,
@@ -426,3 +428,32 @@ def fit_normal(d_out: int, n_params: int, n_total: int, d_target: int, d_base: i
                                          float(scale), float(fd_step), _dptr(ata), _dptr(atr), stream or None),
            "dbp_fit_normal")
     return ata, atr
+
+
+def fft_c2c(x: np.ndarray, inverse: bool, device: int = 0) -> np.ndarray:
+    """Float64 DFT along the last axis on the GPU (cuFFT Z2Z); inverse scaled by 1/n."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+    n = a.shape[-1]
+    out = np.empty_like(a)
+    batch = a.size // n if n else 0
+    if batch == 0:
+        return out
+    if device_count() == 0:
+        raise RuntimeError("no CUDA device visible: the GPU FFT has no CPU fallback")
+    _check(load_library().dbp_fft_c2c(int(device), a.ctypes.data, out.ctypes.data, int(n), int(batch),
+                                      int(bool(inverse))), "dbp_fft_c2c")
+    return out
+
+
+def phase_noise(x: np.ndarray, increments: np.ndarray, device: int = 0) -> np.ndarray:
+    """(2, n) complex128 * exp(j cumsum(increments)) on the GPU."""
+    a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
+    inc = np.ascontiguousarray(np.asarray(increments, dtype=np.float64))
+    if a.ndim != 2 or a.shape[0] != 2 or inc.shape != (a.shape[1],):
+        raise ValueError("expected a (2, n) waveform and n increments")
+    if device_count() == 0:
+        raise RuntimeError("no CUDA device visible: the GPU phase-noise path has no CPU fallback")
+    out = np.empty_like(a)
+    _check(load_library().dbp_phase_noise(int(device), a.ctypes.data, _dptr(inc), out.ctypes.data,
+                                          int(a.shape[1])), "dbp_phase_noise")
+    return out

@@ -320,3 +320,67 @@ def nonlinear_substep_essfm(block, gamma: float, dz_eff: float, coeffs: EssfmCoe
 def nonlinear_substep_ssfm(block, gamma: float, dz_eff: float, *, device: int = 0) -> np.ndarray:
     """GPU plain rotation exp(-j gamma dz_eff (|x|^2 + |y|^2)) (channel.py:61-71)."""
     return _rotate_blocks(block, gamma, dz_eff, np.array([1.0]), device)
+
+
+BlockProcessor = "GpuBlockProcessor"   # spectral.py:84: the operator type overlap_save_run accepts
+
+
+class GpuBlockProcessor:
+    """The per-block operator of ``backpropagate`` (the closure ``process`` of
+    dbp.py:212-233) as a GPU object: callable on one (2, N) block or an
+    (nb, 2, N) stack (``dbp_process_blocks``), and recognised by
+    ``overlap_save_run``, which then frames and processes the whole signal in
+    the fused kernel."""
+
+    def __init__(self, cfg: DbpConfig, sample_rate: float, device: int = 0):
+        self.cfg = cfg
+        self.sample_rate = float(sample_rate)
+        self.device = int(device)
+        self.engine = get_engine(cfg, sample_rate, device)
+
+    @property
+    def plan(self):
+        return self.cfg.plan
+
+    def __call__(self, block):
+        import torch
+
+        b = np.asarray(block)
+        single = b.ndim == 2
+        blocks = np.ascontiguousarray((b[None] if single else b).astype(np.complex64))
+        n = self.cfg.plan.block_len
+        if blocks.ndim != 3 or blocks.shape[1:] != (2, n):
+            raise ValueError(f"expected (2, {n}) blocks")
+        dev = torch.device("cuda", self.device)
+        d_in = torch.from_numpy(blocks.view(np.float32)).to(dev)
+        d_out = torch.empty_like(d_in)
+        stream = torch.cuda.current_stream(dev)
+        with self.engine.native.lock:
+            self.engine.native.process_blocks(d_in.data_ptr(), d_out.data_ptr(), blocks.shape[0], stream.cuda_stream)
+        stream.synchronize()
+        out = d_out.cpu().numpy().view(np.complex64).astype(np.complex128)
+        return out[0] if single else out
+
+
+def block_processor(cfg: DbpConfig, sample_rate: float, *, device: int = 0) -> GpuBlockProcessor:
+    """The GPU block operator of ``cfg`` (dbp.py:193-233) for ``overlap_save_run``."""
+    return GpuBlockProcessor(cfg, sample_rate, device)
+
+
+def overlap_save_run(sig: DualPolSignal, plan, block_processor, jobs: int = 1) -> DualPolSignal:
+    """spectral.py:87-145 with a GPU block processor: cyclic extension, per-block
+    operator, keep the central ``plan.usable`` samples -- all inside the fused
+    kernel.  Arbitrary Python callables have no GPU path (and there is no CPU
+    fallback): pass ``block_processor(cfg, sample_rate)``."""
+    if jobs < 1:
+        raise ValueError("jobs must be >= 1")
+    if not isinstance(block_processor, GpuBlockProcessor):
+        raise TypeError("overlap_save_run needs a GPU block processor (paper_1507_00921_b200.block_processor); "
+                        "a Python callable cannot run on the GPU path")
+    if (plan.block_len, plan.overlap) != (block_processor.plan.block_len, block_processor.plan.overlap):
+        raise ValueError("plan does not match the block processor's plan")
+    if float(sig.sample_rate) != block_processor.sample_rate:
+        raise ValueError("signal sample rate does not match the block processor's")
+    out = block_processor.engine.run_host(np.stack([np.asarray(sig.x), np.asarray(sig.y)]))[0]
+    return DualPolSignal(out[0].astype(np.complex128), out[1].astype(np.complex128), sig.sample_rate)
+

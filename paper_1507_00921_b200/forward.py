@@ -40,6 +40,20 @@ class SsfmStepConfig:
             raise ValueError("steps_per_span must be >= 1")
 
 
+def linear_substep(spectrum, beta2: float, dz: float, freqs) -> np.ndarray:
+    """Dispersion operator exp(-j 2 pi^2 beta2 1e-24 f^2 dz) on a spectrum (channel.py:47-58).
+
+    The closed form the GPU tables are built from (float64, on the host, once
+    per configuration); the per-step multiply itself runs inside the kernels.
+    """
+    spectrum = np.asarray(spectrum)
+    freqs = np.asarray(freqs)
+    if spectrum.shape[-1] != freqs.shape[-1]:
+        raise ValueError("spectrum and frequency grid lengths differ")
+    phase = -2.0 * np.pi ** 2 * (beta2 * 1e-24) * freqs ** 2 * dz
+    return spectrum * np.exp(1j * phase)
+
+
 def _as_generator(rng) -> np.random.Generator:
     return rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
 
@@ -146,6 +160,21 @@ def apply_jones_matrix(sig: DualPolSignal, jones, *, device: int = 0) -> DualPol
 def random_polarization_rotation(sig: DualPolSignal, rng=None, *, device: int = 0) -> DualPolSignal:
     """Haar-random polarisation rotation of the whole block (channel.py:150-153)."""
     return apply_jones_matrix(sig, haar_random_unitary(rng), device=device)
+
+
+def apply_laser_phase_noise(sig: DualPolSignal, linewidth_hz: float, rng=None, *, device: int = 0) -> DualPolSignal:
+    """Common Wiener phase noise on both polarisations (channel.py:156-171): the
+    increments are the reference's seeded draws (host numpy), the running phase
+    and the rotation are computed on the GPU."""
+    if linewidth_hz < 0.0:
+        raise ValueError("linewidth must be non-negative")
+    if linewidth_hz == 0.0:
+        return sig
+    gen = _as_generator(rng)
+    sigma = np.sqrt(2.0 * np.pi * linewidth_hz / sig.sample_rate)
+    inc = gen.normal(scale=sigma, size=len(sig))
+    out = _native.phase_noise(np.stack([np.asarray(sig.x), np.asarray(sig.y)]), inc, device)
+    return DualPolSignal(out[0], out[1], sig.sample_rate)
 
 
 def propagate_link_batch(samples: np.ndarray, sample_rate: float, link: LinkConfig, cfg: SsfmStepConfig,

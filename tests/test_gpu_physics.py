@@ -317,3 +317,60 @@ def test_training_respects_iteration_budget():                         # test_tr
                                    pb.TrainConfig(n_coeffs=4, train_samples=4096, max_iterations=1))
     assert isinstance(res, pb.TrainResult)
     assert res.iterations <= 1 and res.final_mse <= res.initial_mse
+
+
+# ---- test_spectral.py / channel phase noise: the API utilities on the GPU ----------------------
+
+def test_fft_matches_direct_dft_and_round_trips():                    # test_spectral.py:13-36
+    rng = np.random.default_rng(0)
+    for n in (1, 2, 8, 64, 1024):
+        x = rng.normal(size=(3, n)) + 1j * rng.normal(size=(3, n))
+        k = np.arange(n)
+        direct = x @ np.exp(-2j * np.pi * np.outer(k, k) / n)
+        np.testing.assert_allclose(pb.fft(x), direct, rtol=0, atol=1e-11 * max(1, n))
+        np.testing.assert_allclose(pb.ifft(pb.fft(x)), x, rtol=0, atol=1e-13 * max(1, n))
+        np.testing.assert_allclose(np.sum(np.abs(pb.fft(x)) ** 2, axis=-1) / n, np.sum(np.abs(x) ** 2, axis=-1),
+                                   rtol=1e-12)
+    with pytest.raises(ValueError):
+        pb.fft(np.ones(12))
+    with pytest.raises(ValueError):
+        pb.ifft(np.ones(100))
+
+
+def test_overlap_save_run_with_gpu_block_processor(golden, manifest):
+    case = next(c for c in manifest["cases"] if c["name"] == "c0_sym")
+    from .helpers import case_config
+    cfg = case_config(case, golden["link_c17"])
+    x = golden["link_rx"]
+    proc = pb.block_processor(cfg, 56e9)
+    import warnings
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        via_run = pb.overlap_save_run(sig(x), cfg.plan, proc)
+        direct = pb.backpropagate(sig(x), cfg)
+    np.testing.assert_array_equal(via_run.stack(), direct.stack())
+    blocks = golden["link_c0_sym_blk_in"]
+    got = proc(blocks)
+    want = golden["link_c0_sym_blk_out"]
+    for b in range(blocks.shape[0]):
+        assert np.linalg.norm(got[b] - want[b]) / np.linalg.norm(want[b]) <= 1e-5
+    with pytest.raises(TypeError):
+        pb.overlap_save_run(sig(x), cfg.plan, lambda blk: blk)
+    with pytest.raises(ValueError):
+        pb.overlap_save_run(sig(x), cfg.plan, proc, jobs=0)
+
+
+def test_laser_phase_noise_matches_reference_and_statistics(golden_rx):  # test_channel.py:141-157
+    x = golden_rx["tx_rc"]
+    got = pb.apply_laser_phase_noise(sig(x), 100e3, rng=11).stack()
+    np.testing.assert_allclose(got, golden_rx["laser_out"], rtol=0, atol=1e-11)
+    n = 2 ** 19
+    const = pb.DualPolSignal(np.ones(n, dtype=complex), np.ones(n, dtype=complex), 56e9)
+    out = pb.apply_laser_phase_noise(const, 100e3, rng=7)
+    np.testing.assert_allclose(np.abs(out.x), 1.0, atol=1e-12)
+    np.testing.assert_array_equal(out.x, out.y)
+    dphi = np.angle(out.x[1:] * np.conj(out.x[:-1]))
+    assert np.var(dphi) == pytest.approx(2.0 * math.pi * 100e3 / 56e9, rel=0.02)
+    assert pb.apply_laser_phase_noise(const, 0.0) is const
+    with pytest.raises(ValueError):
+        pb.apply_laser_phase_noise(const, -1.0)
