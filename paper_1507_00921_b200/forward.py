@@ -178,9 +178,12 @@ def apply_laser_phase_noise(sig: DualPolSignal, linewidth_hz: float, rng=None, *
 
 
 def propagate_link_batch(samples: np.ndarray, sample_rate: float, link: LinkConfig, cfg: SsfmStepConfig,
-                         rngs, *, device: int = 0) -> np.ndarray:
+                         rngs, *, device: int = 0, devices=None) -> np.ndarray:
     """(B, 2, n) complex waveforms through every span; ``rngs[i]`` seeds item i like
-    ``propagate_link``'s ``rng`` (int or SeedSequence).  Returns (B, 2, n) complex64."""
+    ``propagate_link``'s ``rng`` (int or SeedSequence).  Returns (B, 2, n) complex64.
+    ``devices``: split the batch into contiguous waveform groups, one per GPU
+    (independent waveforms, no exchange); each item's result does not depend on
+    the split."""
     x = np.ascontiguousarray(samples, dtype=np.complex64)
     if x.ndim == 2:
         x = x[None]
@@ -188,6 +191,18 @@ def propagate_link_batch(samples: np.ndarray, sample_rate: float, link: LinkConf
     lg = _log2_length(n)
     if len(rngs) != b:
         raise ValueError("need one rng seed per waveform")
+    if devices is not None:
+        devs = list(dict.fromkeys(int(d) for d in devices))
+        if not devs:
+            raise ValueError("devices must not be empty")
+        if len(devs) > 1 and b > 1:
+            bounds = [round(i * b / len(devs)) for i in range(len(devs) + 1)]
+            parts = [(d, bounds[i], bounds[i + 1]) for i, d in enumerate(devs) if bounds[i + 1] > bounds[i]]
+            with ThreadPoolExecutor(max_workers=len(parts)) as pool:
+                futs = [pool.submit(propagate_link_batch, x[lo:hi], sample_rate, link, cfg, list(rngs[lo:hi]),
+                                    device=d) for d, lo, hi in parts]
+                return np.concatenate([f.result() for f in futs])
+        device = devs[0]
     children = []
     for r in rngs:
         if isinstance(r, np.random.Generator):

@@ -193,7 +193,7 @@ def measure_ber(decided_bits, reference_bits, skip: int = 0, evm: float = math.n
 
 def receive_batch(samples: np.ndarray, symbol_rate: float, reference_symbols: np.ndarray, taps: int = 15,
                   step_size: float = 1e-3, passes: int = 2, window: int = 32, skip_bits: int = 0, *,
-                  device: int = 0):
+                  device: int = 0, devices=None):
     """cli.py:677-685 for B waveforms on the GPU: equalise, recover the carrier
     against ``reference_symbols`` (2, m), decide, count.  Returns a list with one
     ``RxMetrics`` per waveform (EVM against the scaled nearest constellation
@@ -203,6 +203,20 @@ def receive_batch(samples: np.ndarray, symbol_rate: float, reference_symbols: np
         x = x[None]
     if x.dtype not in (np.complex64, np.complex128):
         x = x.astype(np.complex128)
+    if devices is not None:
+        devs = list(dict.fromkeys(int(d) for d in devices))
+        if not devs:
+            raise ValueError("devices must not be empty")
+        b = x.shape[0]
+        if len(devs) > 1 and b > 1:   # independent waveforms: contiguous groups, one per GPU
+            from concurrent.futures import ThreadPoolExecutor
+            bounds = [round(i * b / len(devs)) for i in range(len(devs) + 1)]
+            parts = [(d, bounds[i], bounds[i + 1]) for i, d in enumerate(devs) if bounds[i + 1] > bounds[i]]
+            with ThreadPoolExecutor(max_workers=len(parts)) as pool:
+                futs = [pool.submit(receive_batch, x[lo:hi], symbol_rate, reference_symbols, taps, step_size,
+                                    passes, window, skip_bits, device=d) for d, lo, hi in parts]
+                return [m for f in futs for m in f.result()]
+        device = devs[0]
     if taps < 1 or taps % 2 == 0:
         raise ValueError("taps must be odd and positive")
     n_samp = x.shape[-1]

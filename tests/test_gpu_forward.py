@@ -181,3 +181,14 @@ def test_forced_transpose_layout_equals_column_layout(tmp_path):
         subprocess.run([sys.executable, "-c", script, root, str(out)], check=True, env=env)
         outs.append(np.load(out))
     assert rel_l2(outs[0], outs[1]) <= tol(5)
+
+
+def test_batch_device_list_equals_single_device():
+    # devices=[...] splits independent waveforms across GPUs; on one GPU the list collapses
+    n = 1 << 12
+    rng = np.random.default_rng(8)
+    xs = (0.02 * (rng.normal(size=(3, 2, n)) + 1j * rng.normal(size=(3, 2, n)))).astype(np.complex64)
+    link = pb.LinkConfig(span=pb.FiberParams(-21.7, 1.3, 0.2, 80.0), num_spans=2)
+    a = pb.propagate_link_batch(xs, 56e9, link, pb.SsfmStepConfig(3), [1, 2, 3])
+    b = pb.propagate_link_batch(xs, 56e9, link, pb.SsfmStepConfig(3), [1, 2, 3], devices=[0, 0])
+    np.testing.assert_array_equal(a, b)
