@@ -361,3 +361,25 @@ def test_random_configurations_match_oracle():
         want = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(cfg))
         err = dbp_port.per_block_rel_l2(got, want, n_blk, m).max()
         assert err <= TOL_BLOCK, (case, alg, n_blk, m, n, steps, spans, arr, err)
+
+
+def test_integration_stub_runs_and_matches(golden, manifest, tmp_path):
+    # the ctypes binding INTEGRATION.md shows a fiberdbp maintainer adding, executed verbatim
+    # (its two relative imports pointed at this package's equivalents) against the same case
+    import re
+    from pathlib import Path
+    text = (Path(__file__).resolve().parent.parent / "INTEGRATION.md").read_text()
+    stub = re.search(r"```python\n(import ctypes, numpy as np.*?)```", text, re.S).group(1)
+    stub = stub.replace("from .dbp import _reverse_step_schedule",
+                        "from paper_1507_00921_b200.backprop import _reverse_step_schedule")
+    stub = stub.replace("from .spectral import fft_frequencies", "from paper_1507_00921_b200 import fft_frequencies")
+    stub = stub.replace('ctypes.CDLL("libdbp_b200.so")', f'ctypes.CDLL("{_native.LIB_PATH}")')
+    ns = {}
+    exec(compile(stub, "INTEGRATION.md", "exec"), ns)
+    case = next(c for c in manifest["cases"] if c["name"] == "c0_sym")
+    x, c, want = _case_inputs(golden, case)
+    cfg = case_config(case, c)
+    got = ns["backpropagate_b200"](pb.DualPolSignal(x[0], x[1], 56e9), cfg).stack()
+    errs = dbp_port.per_block_rel_l2(got, want, case["block_len"], case["overlap"])
+    assert errs.max() <= TOL_BLOCK
+    np.testing.assert_array_equal(got.astype(np.complex64), _run(x, cfg)[0])
