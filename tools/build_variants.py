@@ -19,6 +19,7 @@ VARIANTS = {
     "pw1": ["-DDBP_TW_POWERS=1"],
     "pw2": ["-DDBP_TW_POWERS=2"],
     "pw3": ["-DDBP_TW_POWERS=3"],
+    "xopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "sepfir": ["-DDBP_SEPARATE_FIR=1"],
     "nobar": ["-DDBP_EXPERIMENT_NOBAR=1"],   # timing ceiling only: wrong results
     "tps768": ["-DDBP_THREADS_PER_SM=768"],
