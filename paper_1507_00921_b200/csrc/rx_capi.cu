@@ -124,7 +124,10 @@ __global__ void __launch_bounds__(128) cma_kernel(const double2* __restrict__ ex
                                                   long long m, double2* __restrict__ out,
                                                   const int* __restrict__ items, int n_items) {
   __shared__ double2 win[4][2][2][kCmaWin];   // [warp][buffer][pol][sample]
+  __shared__ double2 zero_col[2 * kCmaChunk + 2];   // read by lanes beyond the tap count
   const int w = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  for (int e = threadIdx.x; e < 2 * kCmaChunk + 2; e += blockDim.x) zero_col[e] = make_double2(0.0, 0.0);
+  __syncthreads();
   if (w >= n_items) return;
   const int b = items[w];
   const int lane = threadIdx.x & 31, h = lane >> 4, j = lane & 15, wl = threadIdx.x >> 5;
@@ -157,25 +160,30 @@ __global__ void __launch_bounds__(128) cma_kernel(const double2* __restrict__ ex
     asm volatile("cp.async.commit_group;");
     asm volatile("cp.async.wait_group 1;");
     __syncwarp();
-    const double2(*wx) = win[wl][c & 1][0];
-    const double2(*wy) = win[wl][c & 1][1];
     const long long n0 = c * kCmaChunk;
     const int cnt = (int)(m - n0 < kCmaChunk ? m - n0 : kCmaChunk);
-    double2 ux[K], uy[K];
+    // per-tap column pointers: real taps read the window, the rest a zero column
+    // (no per-symbol predicates; the read one symbol past a chunk is never used)
+    const double2* px[K];
+    const double2* py[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       const int i = j + 16 * k;
-      ux[k] = i < taps ? wx[i] : make_double2(0.0, 0.0);
-      uy[k] = i < taps ? wy[i] : make_double2(0.0, 0.0);
+      px[k] = i < taps ? win[wl][c & 1][0] + i : zero_col;
+      py[k] = i < taps ? win[wl][c & 1][1] + i : zero_col;
+    }
+    double2 ux[K], uy[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      ux[k] = px[k][0];
+      uy[k] = py[k][0];
     }
     for (int n = 0; n < cnt; ++n) {
       double2 nx[K], ny[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const int i = j + 16 * k;
-        const bool ok = i < taps && n + 1 < cnt;
-        nx[k] = ok ? wx[2 * (n + 1) + i] : make_double2(0.0, 0.0);
-        ny[k] = ok ? wy[2 * (n + 1) + i] : make_double2(0.0, 0.0);
+        nx[k] = px[k][2 * (n + 1)];
+        ny[k] = py[k][2 * (n + 1)];
       }
       double ar = 0.0, ai = 0.0;
 #pragma unroll
