@@ -103,6 +103,17 @@ def work_per_sample(a, gains_not_one: bool = False) -> tuple[float, float]:
     return flops / (n - m), 16.0 * (2 * n - m) / (n - m)
 
 
+def cpu_model() -> str:
+    """The host CPU model (state the cores and the model beside the CPU figure)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def workload_config(a, world: int) -> dict:
     return {
         "workload": (f"configs[3] batch with configs[0] DBP: {a.waveforms} x 2^{a.log2_samples} dual-pol "
@@ -312,7 +323,7 @@ def run_ours(a) -> int:
         cpu = {"value": samples / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{waves} waveforms x 2^{a.log2_samples} samples of the same workload, "
                          f"oracle/dbp_port.py float64 numpy (pocketfft), {cores} single-threaded processes",
-               "seconds": secs}
+               "seconds": secs, "cpu_model": cpu_model()}
 
     if rank == 0:
         line = {
@@ -371,7 +382,7 @@ def run_reference(a) -> int:
         "config": workload_config(a, world), "impl": "reference",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"each step: {cores} waveforms x 2^{a.log2_samples} samples "
-                                   "(one per core) through oracle/dbp_port.py"},
+                                   "(one per core) through oracle/dbp_port.py", "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
