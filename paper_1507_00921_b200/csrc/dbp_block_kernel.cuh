@@ -1,4 +1,4 @@
-// Fused overlap-save DBP block kernel for sm_100a (v2: one polarisation per thread).
+// Fused overlap-save DBP block kernel for sm_100a (one polarisation per thread).
 //
 // One overlap-save block of N dual-polarisation samples per block slice of
 // 2T threads, T = N/16: lanes 0-15 of a warp carry polarisation x and lanes
@@ -19,12 +19,16 @@
 //
 // FFT: N = R0 * 16^(NP-1), passes radix R0 (2..16, G0 = 16/R0 groups per
 // thread) then radix 16.  Forward passes are decimation-in-frequency, so the
-// spectrum ends digit-reversed across threads; the dispersion table is read
-// at each register's natural bin index and the inverse is the exact adjoint
-// walk back (no reorder pass).  Every exchange writes register m to plane
-// position t + T m; reads gather a pass's 16 inputs.  Only the exchange into
-// the last pass (stride 1 reads) needs an XOR swizzle to stay conflict free
-// for 8-byte accesses (16 lanes per shared-memory phase).
+// spectrum ends digit-reversed across threads; the dispersion table is
+// permuted on the host to each register's bin and the inverse is the exact
+// adjoint walk back (no reorder pass).  Exchanges go through per-
+// polarisation shared-memory planes with padded layouts (pad16 / pad256,
+// conflict-free 8-byte accesses); the exchange into the last pass is a
+// 16 x 16 transpose inside each half-warp's own 272-element tile (only a
+// __syncwarp), and at N = 2048 the first exchange pairs positions i, i + T
+// into 16-byte accesses (Geo::X01_PAIRED).  Twiddles are built by powers of
+// one table load per group (DBP_TW_POWERS), and all complex arithmetic runs
+// on the packed FP32 pipe (FADD2 / FMUL2 / FFMA2, dft_small.cuh).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
