@@ -2,9 +2,10 @@
 //
 // The simulator owns its device buffers: the waveform batch
 // [item][pol][n] complex64, a scratch buffer of the same size (transposed
-// layout), the noise buffer of the span-end amplifier, the block-FFT
-// twiddles of both row lengths, the two-level W_n table and the permuted
-// linear-step table (cached per (sample rate, beta2, dz)).
+// layout only), the noise and Jones buffers of the span-end amplifier, the
+// block-FFT twiddles of both row lengths, the W_n^{k1 n2} tables in both
+// layouts and the permuted double-float linear-step table (cached per
+// (sample rate, beta2, dz)); spans run as cached CUDA graphs.
 #include <cuda_runtime.h>
 
 #include <algorithm>

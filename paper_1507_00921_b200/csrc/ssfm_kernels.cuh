@@ -19,8 +19,12 @@
 //   K_c  row of At': fft_inv over n1, x e^{-j gamma dz_eff I} x loss, and
 //                    for every step but the last K_a again (fused, mode CA)
 //
-// One SSFM step = two row kernels + two transposes over the waveform, which
-// stays L2-resident for n <= 2^21 (32 MB dual-pol complex64).
+// One SSFM step = two row kernels + two transposes over the waveform in this
+// transposed layout (n > 2^21).  For 2^11 <= n <= 2^21 the column layout
+// keeps the waveform in natural [N1][N2] order: K_a / K_c become column
+// kernels (COL = true: a tile of adjacent columns staged through shared
+// memory with coalesced row segments) and K_b runs on the natural rows --
+// two kernels per step, no transposes (ssfm_capi.cu).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
