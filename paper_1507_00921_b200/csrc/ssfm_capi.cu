@@ -129,6 +129,9 @@ struct dbp_sim {
   // global transposes.  Otherwise (or DBP_SIM_TRANSPOSE=1) the transposed
   // four-step layout with 32 x 33 tile transposes.
   bool column = false;
+  // block mode (n <= 2^13): the whole waveform is one block-FFT row; a span
+  // is ONE launch running every step on-chip (kSimFull)
+  bool block = false;
   long long n = 0;
   float2* data = nullptr;
   float2* scratch = nullptr;
@@ -221,7 +224,20 @@ int ensure_lin(dbp_sim* s, double fs, double beta2, double dz) {
   const int t1 = (int)(n1 / 16), t2 = (int)(n2 / 16);
   std::vector<float2> h(n), l(n);
   const double inv_n = 1.0 / (double)n;
-  for (long long p = 0; p < n1; ++p) {
+  auto entry = [&](long long k, long long slot) {
+    const double f = (k < n / 2 ? (double)k : (double)(k - n)) * (fs / (double)n);
+    const double ph = -2.0 * M_PI * M_PI * (beta2 * 1e-24) * f * f * dz;  // channel.py:57
+    const double re = std::cos(ph) * inv_n, im = std::sin(ph) * inv_n;
+    const float2 hi = make_float2((float)re, (float)im);
+    h[slot] = hi;
+    l[slot] = make_float2((float)(re - hi.x), (float)(im - hi.y));
+  };
+  if (s->block) {   // one row of n: bins in the block FFT's register order
+    const int tt = (int)(n / 16);
+    for (int t = 0; t < tt; ++t)
+      for (int e = 0; e < 16; ++e) entry(dbp::last_pass_bin(s->log_n, t, e), dbp::tab_index(s->log_n, t, e));
+  }
+  for (long long p = 0; !s->block && p < n1; ++p) {
     const long long k1 = dbp::last_pass_bin(s->log_n1, (int)(p % t1), (int)(p / t1));
     for (int t = 0; t < t2; ++t)
       for (int e = 0; e < 16; ++e) {
@@ -268,11 +284,15 @@ int dbp_sim_create(dbp_sim** out, int device, int log2_n, int max_batch) {
   s->log_n = log2_n;
   s->n = 1LL << log2_n;
   const char* force_t = std::getenv("DBP_SIM_TRANSPOSE");
+  const char* force_nb = std::getenv("DBP_SIM_NO_BLOCK");
+  // (measured: 2^8 2.7, 2^10 3.5, 2^12 10.0 us per step; at 2^13 one 1024-thread
+  // CTA per waveform is slower than the four-step split, 22 vs 11 us)
+  s->block = log2_n <= 12 && !(force_nb && force_nb[0] == '1') && !(force_t && force_t[0] == '1');
   // Column tiles are BPC(N1) = 2048 / N1 columns wide, so N2 >= 2048 / N1,
   // i.e. n >= 2^11.  Split measured on B200 (tools/sim_sweep.sh,
   // profiles/r1/sim_sweep.txt): N1 = 2^7 up to 2^14, 2^8 up to 2^20, 2^9 at
   // 2^21; from 2^22 the transposed layout is faster (32-byte column rows).
-  s->column = log2_n >= 11 && log2_n <= 21 && !(force_t && force_t[0] == '1');
+  s->column = !s->block && log2_n >= 11 && log2_n <= 21 && !(force_t && force_t[0] == '1');
   const char* force_l1 = std::getenv("DBP_SIM_LOGN1");   // tuning experiments
   if (s->column) {
     s->log_n1 = log2_n <= 14 ? std::min(7, log2_n - 4) : log2_n <= 20 ? 8 : 9;   // N2 <= 2^13
@@ -288,6 +308,10 @@ int dbp_sim_create(dbp_sim** out, int device, int log2_n, int max_batch) {
       s->log_n1 = log2_n - s->log_n2;
     }
   }
+  if (s->block) {
+    s->log_n1 = 0;
+    s->log_n2 = log2_n;
+  }
   s->max_batch = max_batch;
   const size_t bytes = (size_t)max_batch * 2 * s->n * sizeof(float2);
   int rc = DBP_OK;
@@ -296,13 +320,13 @@ int dbp_sim_create(dbp_sim** out, int device, int log2_n, int max_batch) {
     return code;
   };
   if (cudaMalloc(&s->data, bytes) != cudaSuccess ||
-      (!s->column && cudaMalloc(&s->scratch, bytes) != cudaSuccess) ||
+      (!s->column && !s->block && cudaMalloc(&s->scratch, bytes) != cudaSuccess) ||
       cudaMalloc(&s->noise, bytes) != cudaSuccess ||
       cudaMalloc(&s->jones, (size_t)max_batch * 4 * sizeof(float2)) != cudaSuccess)
     return cleanup(fail(DBP_ENOMEM, "device allocation of the waveform buffers failed"));
-  if ((rc = upload(&s->tw1, dbp::make_twiddles(s->log_n1)))) return cleanup(rc);
+  if (!s->block && (rc = upload(&s->tw1, dbp::make_twiddles(s->log_n1)))) return cleanup(rc);
   if ((rc = upload(&s->tw2, dbp::make_twiddles(s->log_n2)))) return cleanup(rc);
-  {
+  if (!s->block) {
     std::vector<float2> wa, wb;
     make_four_step_twiddles(log2_n, s->log_n1, wa, wb);
     if ((rc = upload(&s->wa, wa))) return cleanup(rc);
@@ -380,6 +404,11 @@ int dbp_sim_span(dbp_sim* s, int batch, double sample_rate, double beta2, double
   cudaStream_t st = s->stream;
   auto enqueue = [&]() -> int {
     int r;
+    if (s->block) {   // one launch: every step on-chip
+      dbp::SimParams full = base;
+      full.steps = steps;
+      return launch_row(s, s->log_n, dbp::kSimFull, s->data, batch, full, st);
+    }
     if (s->column) {   // natural layout throughout: column (N1) and row (N2) kernels in place
       if ((r = launch_row(s, s->log_n1, dbp::kSimA, s->data, batch, base, st, true))) return r;
       for (int k = 0; k < steps; ++k) {

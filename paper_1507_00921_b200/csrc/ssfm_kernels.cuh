@@ -33,7 +33,7 @@
 
 namespace dbp {
 
-enum SimMode : int { kSimA = 0, kSimCA = 1, kSimC = 2, kSimB = 3 };
+enum SimMode : int { kSimA = 0, kSimCA = 1, kSimC = 2, kSimB = 3, kSimFull = 4 };
 
 struct SimParams {
   float2* data;             // rows of row_len samples, [item][pol][rows][row_len]
@@ -55,12 +55,13 @@ struct SimParams {
   int nonlinear;
   int slice_floats;
   int n2;                   // column kernels: row stride / number of columns (N2)
+  int steps;                // kSimFull: SSFM steps of the span, all in one launch
 };
 
 // x e^{-j gamma dz_eff (|x|^2 + |y|^2)} x loss (channel.py:61-71, 93); the
 // partner lane (lane ^ 16) holds the other polarisation of the same sample
-__device__ __forceinline__ void sim_nonlinear(float2 (&v)[16], const SimParams& sp, int pol) {
-  const float loss = sp.mode == kSimC ? sp.loss_last : sp.loss;
+__device__ __forceinline__ void sim_nonlinear(float2 (&v)[16], const SimParams& sp, int pol, bool last) {
+  const float loss = last ? sp.loss_last : sp.loss;
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
     const float own = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
@@ -154,7 +155,19 @@ ssfm_row_kernel(const SimParams sp) {
     for (int m = 0; m < 16; ++m) v[m] = active ? rp[T * m] : make_float2(0.f, 0.f);
   }
 
-  if (sp.mode == kSimB) {
+  if (sp.mode == kSimFull) {
+    // whole waveform in this slice (n = row length <= 2^13): every step of
+    // the span on-chip -- FFT, dispersion (double-float table, bins in
+    // register order), inverse FFT, Manakov rotation and loss
+    for (int k = 0; k < sp.steps; ++k) {
+      if constexpr (G::SEP_FIR) __syncthreads();   // see kSimCA below
+      const int tf = opaque(t);
+      fft_fwd<LOGN, 0, 0>(v, sh, sp.tw, tf);
+      apply_table_df<LOGN>(v, sp.lin, sp.lin_lo, G::NP == 1 ? 0 : tf);
+      fft_inv<LOGN, 0, 0>(v, sh, sp.tw, opaque(t));
+      sim_nonlinear(v, sp, pol, k + 1 == sp.steps);
+    }
+  } else if (sp.mode == kSimB) {
     fft_fwd<LOGN, 0, 0>(v, sh, sp.tw, t);
     apply_table_df<LOGN>(v, sp.lin + (long long)row * N, sp.lin_lo + (long long)row * N, G::NP == 1 ? 0 : t);
     const int ti = opaque(t);
@@ -164,7 +177,7 @@ ssfm_row_kernel(const SimParams sp) {
   } else {
     if (sp.mode != kSimA) {
       fft_inv<LOGN, 0, 0>(v, sh, sp.tw, t);
-      sim_nonlinear(v, sp, pol);
+      sim_nonlinear(v, sp, pol, sp.mode == kSimC);
     }
     if (sp.mode != kSimC) {
       // fft_fwd's first exchange skips its leading barrier when the FIR region

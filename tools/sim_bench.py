@@ -65,10 +65,14 @@ def main():
         t = float(np.median(times))
         per_step = t / args.steps
         rate = batch * n * args.steps / t
-        column = 11 <= lg <= 21 and os.environ.get("DBP_SIM_TRANSPOSE") != "1"
-        traffic = (64.0 if column else 96.0) * 2 * n * batch
-        rows.append(dict(log2_n=lg, batch=batch, layout="column" if column else "transposed",
-                         bytes_per_pol_sample_step=64 if column else 96, ms_per_span=t * 1e3, us_per_step=per_step * 1e6,
+        forced_t = os.environ.get("DBP_SIM_TRANSPOSE") == "1"
+        block = lg <= 12 and not forced_t and os.environ.get("DBP_SIM_NO_BLOCK") != "1"
+        column = not block and 11 <= lg <= 21 and not forced_t
+        # block mode keeps the waveform on-chip for the whole span: 16 B per pol-sample per span
+        # (load + store) plus the 16-byte table per step
+        traffic = ((16.0 + 16.0 * args.steps) / args.steps if block else 64.0 if column else 96.0) * 2 * n * batch
+        rows.append(dict(log2_n=lg, batch=batch, layout="block" if block else "column" if column else "transposed",
+                         bytes_per_pol_sample_step=round(traffic / (2 * n * batch), 2), ms_per_span=t * 1e3, us_per_step=per_step * 1e6,
                          sample_steps_per_s=rate, effective_GBps=traffic / per_step / 1e9))
         print(json.dumps(rows[-1]))
     # CPU oracle on a bounded sample: 2^17 samples, 4 steps
