@@ -20,6 +20,7 @@ import json
 import math
 import os
 import sys
+import time
 import warnings
 from pathlib import Path
 
@@ -52,6 +53,9 @@ def main():
     ap.add_argument("--log2-samples", type=int, default=30)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--gather", action="store_true",
+                    help="after timing, assemble the whole output stream on rank 0 (NCCL point-to-point over "
+                         "NVLink; not part of the timed path) and report its digest and the gather time")
     a = ap.parse_args()
 
     import torch
@@ -105,6 +109,29 @@ def main():
         dist.all_gather_object(digests, (rank, olo, ohi, digest))
     else:
         digests = [(0, olo, ohi, digest)]
+    gather = None
+    if a.gather:
+        # optional final gather: rank r's output span [olo, ohi) -> rank 0, no data-path collective
+        spans = [None] * world
+        if world > 1:
+            dist.all_gather_object(spans, (olo, ohi))
+        else:
+            spans = [(olo, ohi)]
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        if rank == 0:
+            full = torch.empty((2, n, 2), device=dev)
+            full[:, olo:ohi] = out
+            for r in range(1, world):
+                rlo, rhi = spans[r]
+                buf = torch.empty((2, rhi - rlo, 2), device=dev)
+                dist.recv(buf, src=r)
+                full[:, rlo:rhi] = buf
+            torch.cuda.synchronize()
+            gather = {"seconds": time.perf_counter() - g0,
+                      "digest": hashlib.sha256(full.cpu().numpy().tobytes()).hexdigest()[:16]}
+        else:
+            dist.send(out.contiguous(), dst=0)
     if rank == 0:
         ms_max = float(t.item())
         print(json.dumps({
@@ -112,6 +139,7 @@ def main():
             "value": n / (ms_max * 1e-3) / 1e9, "n_gpus": world, "stream_samples": n, "blocks": nb,
             "chunk_latency_ms": ms_max, "halo_samples": [cfg.plan.lead, cfg.plan.overlap - cfg.plan.lead],
             "shards": [list(d) for d in digests], "device_resident": True,
+            "gather": gather,
         }), flush=True)
     if world > 1:
         dist.destroy_process_group()
