@@ -319,11 +319,12 @@ def run_ours(a) -> int:
         cb = CpuBaseline(port_kwargs(a), SAMPLE_RATE, n, POWER_DBM, cores)
         waves = max(16, 2 * cores)
         secs, samples = cb.step(waves)
+        one_core = cb.one_core_rate()
         cb.close()
         cpu = {"value": samples / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
                "sample": f"{waves} waveforms x 2^{a.log2_samples} samples of the same workload, "
                          f"oracle/dbp_port.py float64 numpy (pocketfft), {cores} single-threaded processes",
-               "seconds": secs, "cpu_model": cpu_model()}
+               "seconds": secs, "cpu_model": cpu_model(), "one_core_value": one_core / 1e9}
 
     if rank == 0:
         line = {

@@ -60,8 +60,12 @@ class CpuBaseline:
         """Process ``waveforms`` waveforms across the pool; returns (wall s, samples)."""
         jobs = [(seed0 + i, self.n, self.power_dbm, self.cfg_kwargs, self.rate) for i in range(waveforms)]
         t0 = time.perf_counter()
-        self.pool.map(_work, jobs, chunksize=1)
+        self.job_seconds = self.pool.map(_work, jobs, chunksize=1)
         return time.perf_counter() - t0, float(waveforms * self.n)
+
+    def one_core_rate(self) -> float:
+        """Samples/s of one core: the median per-waveform time of the last step (each job is one process)."""
+        return float(self.n / np.median(self.job_seconds))
 
     def close(self):
         self.pool.close()
