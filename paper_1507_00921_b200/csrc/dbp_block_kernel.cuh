@@ -42,21 +42,24 @@
 namespace dbp {
 
 // Resident threads per SM targeted by __launch_bounds__ (sets the register
-// budget 65536 / target).  Tuned per block length on B200 (tools/ab_sweep.sh):
-// N <= 1024: 512 (2 x 256-thread CTAs, 128 regs), N = 2048: 768 (3 CTAs,
-// 80 regs), N >= 4096: 1024 (64 regs).  -DDBP_THREADS_PER_SM overrides.
+// budget 65536 / target) and block positions per CTA (DBP_CTA_POSITIONS:
+// CTAs hold max(1, 32 / T) blocks, so every block of N >= 512 has its own
+// CTA and its own barrier domain).  Tuned on B200 with the packed-FP32
+// kernel (tools/ab_small_n.sh, profiles/r1/ab_small_n.txt): N <= 256: 512
+// threads/SM; N = 512, 1024, 2048: 768 (85 / 80 regs); N >= 4096: 1024
+// (64 regs).  -DDBP_THREADS_PER_SM overrides.
 __host__ __device__ constexpr int threads_per_sm(int logn) {
 #ifdef DBP_THREADS_PER_SM
   return DBP_THREADS_PER_SM + 0 * logn;
 #else
-  return logn <= 10 ? 512 : (logn == 11 ? 768 : 1024);
+  return logn <= 8 ? 512 : (logn <= 11 ? 768 : 1024);
 #endif
 }
 #ifndef DBP_EXPERIMENT_NOBAR
 #define DBP_EXPERIMENT_NOBAR 0
 #endif
 #ifndef DBP_CTA_POSITIONS
-#define DBP_CTA_POSITIONS 128
+#define DBP_CTA_POSITIONS 32
 #endif
 // Bounds checks for debug builds (compute-sanitizer is closed on the pool):
 // -DDBP_DEBUG_BOUNDS=1 asserts every shared-memory and global index against

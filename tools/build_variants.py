@@ -19,6 +19,11 @@ VARIANTS = {
     "pw1": ["-DDBP_TW_POWERS=1"],
     "pw2": ["-DDBP_TW_POWERS=2"],
     "pw3": ["-DDBP_TW_POWERS=3"],
+    "cta64": ["-DDBP_CTA_POSITIONS=64"],
+    "cta32": ["-DDBP_CTA_POSITIONS=32"],
+    "cta16": ["-DDBP_CTA_POSITIONS=16"],
+    "cta32_768": ["-DDBP_CTA_POSITIONS=32", "-DDBP_THREADS_PER_SM=768"],
+    "cta32_1024": ["-DDBP_CTA_POSITIONS=32", "-DDBP_THREADS_PER_SM=1024"],
     "xopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "sepfir": ["-DDBP_SEPARATE_FIR=1"],
     "nobar": ["-DDBP_EXPERIMENT_NOBAR=1"],   # timing ceiling only: wrong results
