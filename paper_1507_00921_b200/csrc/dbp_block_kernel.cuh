@@ -24,7 +24,7 @@
 // adjoint walk back (no reorder pass).  Exchanges go through per-
 // polarisation shared-memory planes with padded layouts (pad16 / pad256,
 // conflict-free 8-byte accesses); the exchange into the last pass is a
-// 16 x 16 transpose inside each half-warp's own 272-element tile (only a
+// 16 x 16 transpose inside each half-warp's own 288-element tile (only a
 // __syncwarp), and at N = 2048 the first exchange pairs positions i, i + T
 // into 16-byte accesses (Geo::X01_PAIRED).  Twiddles are built by powers of
 // one table load per group (DBP_TW_POWERS), and all complex arithmetic runs
@@ -55,6 +55,16 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
   return logn <= 8 ? 512 : (logn <= 11 ? 768 : 1024);
 #endif
 }
+// Block input through the TMA bulk-copy engine into the exchange planes
+// (Geo::TMA_LOAD): the loads bypass the L1 data path, so the kernel no
+// longer depends on the L1 share of the unified array (carve-out 86%: LDG
+// path -11%, TMA path -0.1%).  Off by default: at the default carve-out the
+// extra barrier and shared reads cost 1.9% (ESSFM) / +0.1% (FFE); with
+// double-buffered exchanges on top it is +2.9% (FFE) / -0.8% (ESSFM)
+// (tools/ab.sh, variants tma / tma_db / notma).
+#ifndef DBP_TMA_LOAD
+#define DBP_TMA_LOAD 0
+#endif
 #ifndef DBP_EXPERIMENT_NOBAR
 #define DBP_EXPERIMENT_NOBAR 0
 #endif
@@ -74,9 +84,24 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
 #define DBP_CHECK(...) ((void)0)
 #endif
 
-#ifndef DBP_SEPARATE_FIR
-#define DBP_SEPARATE_FIR 0
+// Double-buffered exchange regions (Geo::DB, see Shm).  Off: at N = 2048 the
+// 70 KB slices leave 28 KB of L1 and lose 10% (ESSFM) / 18% (FFE); at an equal
+// forced carve-out they gain only 0.8% (tools/ab_carveout.sh).
+#ifndef DBP_DOUBLE_BUFFER
+#define DBP_DOUBLE_BUFFER 0
 #endif
+
+// half-warp tile: 16 rows of kTilePitch; 18 keeps the rows 16-byte aligned
+// (8 LDS.128 / STS.128 on the row side), 17 is the minimal conflict-free pad
+#ifndef DBP_TILE_PITCH
+#define DBP_TILE_PITCH 18
+#endif
+constexpr int kTilePitch = DBP_TILE_PITCH;
+constexpr int kTileLen = 16 * kTilePitch;    // = 256 + the pad256 pad of its half-warp
+constexpr int kTilePad = kTileLen - 256;     // pad256: elements of pad per 256
+__host__ __device__ constexpr int pad256(int i) { return i + (i >> 8) * kTilePad; }
+// padded exchange plane (float2): pad256 for N >= 512, pad16 below
+__host__ __device__ constexpr int plane_elems(int n) { return n + (n >= 256 ? (n >> 8) * kTilePad : n / 16); }
 
 template <int LOGN>
 struct Geo {
@@ -89,13 +114,12 @@ struct Geo {
   static constexpr int BPC = T >= DBP_CTA_POSITIONS ? 1 : DBP_CTA_POSITIONS / T;
   static constexpr int THREADS = 2 * T * BPC;
   static constexpr int MIN_CTAS = threads_per_sm(LOGN) / THREADS > 0 ? threads_per_sm(LOGN) / THREADS : 1;
-  // FIR intensity / rotation-factor buffers in their own shared region (not
-  // aliased with the exchange planes) while a slice stays <= 72 KB: the
-  // first exchange of a conv and the intensity writes then need no
-  // barrier before writing (3 fewer CTA barriers per ESSFM block).  Off by
-  // default: measured -0.7% (ESSFM) / -3% (FFE) at N = 2048, the larger
-  // shared carve-out costs more L1 table hits than the barriers cost.
-  static constexpr bool SEP_FIR = DBP_SEPARATE_FIR && (16 * (N + N / 16) + 10 * N + 2048) * BPC <= 72 * 1024;
+  // two exchange regions per slice while MIN_CTAS CTAs still fit the SM's
+  // 228 KB (N = 128, 512 .. 2048): one CTA barrier per exchange instead of two
+  static constexpr bool DB =
+      DBP_DOUBLE_BUFFER && MIN_CTAS * (2 * 16 * plane_elems(N) * BPC + 1024) <= 228 * 1024;
+  // one block per CTA and one group per CTA (no persistent loop): input by TMA
+  static constexpr bool TMA_LOAD = DBP_TMA_LOAD && BPC == 1 && LOGN >= 9 && LOGN <= 12;
   // first exchange with 16-byte paired accesses (see fft_fwd)
   static constexpr bool X01_PAIRED = (NP == 3 && R0 == 8);
   // log2 of the pass stride S_p = N / (L_p r_p)
@@ -179,15 +203,23 @@ __host__ __device__ constexpr int tab_index(int logn, int t, int e) {
 __host__ __device__ inline int fir_phys(int u) { return u + ((u >> 4) << 2); }  // pad 4 per 16 floats
 __host__ __device__ inline int cs_phys(int j) { return j + ((j >> 4) << 1); }   // pad 2 per 16 float2
 
-// shared floats per block slice: max(exchange planes, FIR intensity + (cos, sin) buffers)
-inline int plane_elems(int n) { return n + n / 16; }  // padded exchange plane (float2)
+// shared floats per block slice.  Single region: max(exchange planes,
+// FIR intensity + (cos, sin) buffers).  Double-buffered: two regions, each
+// max(planes, intensity, (cos, sin)); the kernel's region 1 starts at
+// slice_floats / 2.
 
 inline int fir_floats(int n, int pw) { return fir_phys(n + 2 * pw) + 4 + 2 * (cs_phys(n) + 2); }
 
-inline int slice_floats(int n, int pw, bool separate_fir) {
-  const int fir = fir_floats(n, pw);
+inline int slice_floats(int n, int pw, bool double_buffer) {
   const int planes = 4 * plane_elems(n);
-  const int v = separate_fir ? planes + fir : (planes > fir ? planes : fir);
+  if (double_buffer) {
+    int r = planes;
+    if (fir_phys(n + 2 * pw) + 4 > r) r = fir_phys(n + 2 * pw) + 4;
+    if (2 * (cs_phys(n) + 2) > r) r = 2 * (cs_phys(n) + 2);
+    return 2 * ((r + 3) & ~3);
+  }
+  const int fir = fir_floats(n, pw);
+  const int v = planes > fir ? planes : fir;
   return (v + 3) & ~3;
 }
 
@@ -195,14 +227,14 @@ inline int slice_floats(int n, int pw, bool separate_fir) {
 //  * NP == 2 (N <= 256): the one exchange feeds the last pass, whose lanes
 //    gather 16 consecutive elements (128-byte lane stride): one pad element
 //    per 16 ("pad16") makes it conflict free.
-//  * NP >= 3: the exchange INTO pass NP-2 uses one pad of 16 elements per
-//    256 ("pad256"), so half-warp h gathers exactly [272 h, 272 h + 256); the
+//  * NP >= 3: the exchange INTO pass NP-2 uses one pad of 32 elements per
+//    256 ("pad256"), so half-warp h gathers exactly [288 h, 288 h + 256); the
 //    exchange into the last pass then stays inside half-warp h's own
-//    272-element tile (see fft_fwd) and needs only __syncwarp.
+//    288-element tile (16 rows of pitch 18, see fft_fwd) and needs only
+//    __syncwarp.
 //  * all other exchanges: plain.
 // Every form is linear in the register index, so accesses are base + immediates.
 __host__ __device__ constexpr int pad16(int i) { return i + (i >> 4); }
-__host__ __device__ constexpr int pad256(int i) { return i + ((i >> 8) << 4); }
 
 template <int LOGN, int P>
 __device__ __forceinline__ int xchg_index(int i) {
@@ -221,8 +253,8 @@ __device__ __forceinline__ int side_index(int t, int m) {
     else return pad16(t + T * m);
   } else if constexpr (NP >= 3 && P + 1 == NP - 2) {
     // t < T: for T <= 256, (t + T m) >> 8 == (T m) >> 8 (no carry); else linear
-    if constexpr (T <= 256) return t + T * m + (((T * m) >> 8) << 4);
-    else return pad256(t) + m * (T + T / 16);
+    if constexpr (T <= 256) return t + T * m + ((T * m) >> 8) * kTilePad;
+    else return pad256(t) + m * (T + (T >> 8) * kTilePad);
   } else {
     return t + T * m;
   }
@@ -244,36 +276,71 @@ __device__ __forceinline__ void ld_pair(const float2* p, float2& a, float2& b) {
   b = make_float2(q.z, q.w);
 }
 
-// Shared memory of one block slice: two exchange planes (x, y) and the FIR
-// buffers -- aliased with the planes, or behind them when Geo::SEP_FIR.
-// Exchanges are "barrier; write; barrier; read"; with separate FIR buffers
-// the leading barrier of a conv's first exchange is provably redundant (the
-// planes' previous readers finished before the rotation's barriers).
-template <int LOGN>
+// TMA bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+// Shared memory of one block slice: exchange planes (x, y) and the FIR
+// buffers, aliased.  Single region: every exchange is "barrier; write;
+// barrier; read".  Double-buffered (DB): two regions used alternately and
+// the choice is compile time -- an FFT's forward exchange P writes region
+// (P + 1) & 1, its inverse exchange P region P & 1, the half-warp tile
+// exchanges stay in region (NP - 2) & 1 (the one their half-warp just read),
+// and the rotation writes intensities to region 1 and (cos, sin) factors to
+// region 0 -- so every op starts and ends on the same parity and each write
+// phase goes to the region NOT read in the phase before: "write; barrier;
+// read" (the barrier of the previous phase already ordered the last reads of
+// this region).  ESSFM block at N = 2048: 6 CTA barriers instead of 11.
+template <int LOGN, bool DB = false>
 struct Shm {
-  float* base;   // slice base
+  float* base;    // region 0
+  float* base1;   // region 1 (== base without double buffering)
   int pol;
-  __device__ __forceinline__ static int plane_len() {
-    constexpr int N = Geo<LOGN>::N;
-    return N + N / 16;
+  __device__ __forceinline__ void init(float* slice_base, int slice_floats, int polarisation) {
+    base = slice_base;
+    base1 = DB ? slice_base + slice_floats / 2 : slice_base;
+    pol = polarisation;
   }
+  __device__ __forceinline__ static int plane_len() { return plane_elems(Geo<LOGN>::N); }
+  template <int R>
+  __device__ __forceinline__ float* region() const {
+    return (R & 1) ? base1 : base;
+  }
+  template <int R>
   __device__ __forceinline__ float2* plane() const {
-    constexpr int N = Geo<LOGN>::N;
-    return reinterpret_cast<float2*>(base) + pol * (N + N / 16);
-  }
-  __device__ __forceinline__ float* fir() const {
-    constexpr int N = Geo<LOGN>::N;
-    return base + (Geo<LOGN>::SEP_FIR ? 4 * (N + N / 16) : 0);
+    return reinterpret_cast<float2*>(region<R>()) + pol * plane_len();
   }
 #if DBP_EXPERIMENT_NOBAR   // timing experiment only: exchange barriers removed (WRONG results)
-  __device__ __forceinline__ void before_first_write() const { __syncwarp(); }
   __device__ __forceinline__ void before_write() const { __syncwarp(); }
   __device__ __forceinline__ void after_write() const { __syncwarp(); }
 #else
-  __device__ __forceinline__ void before_first_write() const {
-    if constexpr (!Geo<LOGN>::SEP_FIR) __syncthreads();
+  __device__ __forceinline__ void before_write() const {
+    if constexpr (!DB) __syncthreads();
   }
-  __device__ __forceinline__ void before_write() const { __syncthreads(); }
   __device__ __forceinline__ void after_write() const { __syncthreads(); }
 #endif
 };
@@ -371,8 +438,8 @@ __device__ __forceinline__ void apply_table_df(float2 (&v)[16], const float2* __
 // ---------------------------------------------------------------------------
 // TWP: which passes build twiddles by powers (DBP_TW_POWERS bits); the link
 // simulator passes 0 (table loads only: powers compound the magnitude error)
-template <int LOGN, int P, int TWP = DBP_TW_POWERS>
-__device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tw,
+template <int LOGN, int P, int TWP = DBP_TW_POWERS, bool DB = false>
+__device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, DB>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T, NP = G::NP;
@@ -393,36 +460,36 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
     }
     // exchange into the pass-1 layout
     constexpr int LS1 = G::log_s(1);
-    sh.before_first_write();
+    sh.before_write();
     if constexpr (G::X01_PAIRED) {
       // R0 = 8, N = 2048: positions i and i + T pair up on both sides of this
       // exchange (registers (m, m+1) when writing, gathers (e, e+8) when
       // reading), so the plane stores them adjacently -- layout
       // pad256(256 (i >> 8) + 2 (i & 127) + ((i >> 7) & 1)) -- and every
       // access is a conflict-free 16-byte vector: half the LDS/STS.
-      float2* plane = sh.plane() + 2 * t;
-      DBP_CHECK(2 * t + 272 * 7 + 1 < Shm<LOGN>::plane_len());
+      float2* plane = sh.template plane<1>() + 2 * t;
+      DBP_CHECK(2 * t + kTileLen * 7 + 1 < sh.plane_len());
 #pragma unroll
-      for (int m = 0; m < 16; m += 2) st_pair(plane + 272 * (m >> 1), v[m], v[m + 1]);
+      for (int m = 0; m < 16; m += 2) st_pair(plane + kTileLen * (m >> 1), v[m], v[m + 1]);
     } else {
-      float2* plane = sh.plane();
+      float2* plane = sh.template plane<1>();
 #pragma unroll
       for (int m = 0; m < 16; ++m) {
-        DBP_CHECK(side_index<LOGN, 0>(t, m) < Shm<LOGN>::plane_len());
+        DBP_CHECK(side_index<LOGN, 0>(t, m) < sh.plane_len());
         plane[side_index<LOGN, 0>(t, m)] = v[m];
       }
     }
     sh.after_write();
     if constexpr (G::X01_PAIRED) {
-      const float2* plane = sh.plane() + 272 * (t >> 4) + 2 * (t & 15);
+      const float2* plane = sh.template plane<1>() + kTileLen * (t >> 4) + 2 * (t & 15);
 #pragma unroll
       for (int e = 0; e < 8; ++e) ld_pair(plane + 32 * e, v[e], v[e + 8]);
     } else {
-      const float2* plane = sh.plane();
+      const float2* plane = sh.template plane<1>();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        DBP_CHECK(xchg_index<LOGN, 0>(base + (e << LS1)) < Shm<LOGN>::plane_len());
+        DBP_CHECK(xchg_index<LOGN, 0>(base + (e << LS1)) < sh.plane_len());
         v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
       }
     }
@@ -431,19 +498,26 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
     // second-to-last pass (S = 16) + last pass, joined by a half-warp-local
     // 16 x 16 transpose: half-warp h = t >> 4 owns sub-problem h, lane
     // ns = t & 15 holds its register k; the last pass's group (h, k) goes to
-    // lane k of the same half-warp.  The tile [272 h, 272 h + 272) is the
-    // region this half-warp alone read in the previous (pad256) exchange.
+    // lane k of the same half-warp.  The tile [288 h, 288 h + 288) is the
+    // region this half-warp alone read in the previous (pad256) exchange;
+    // rows of pitch 18 keep the row side 16-byte aligned (8 LDS.128) and
+    // both sides conflict free.
     dft<16, false>(v);
     twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
-    float2* tile = sh.plane() + 272 * (t >> 4);
+    float2* tile = sh.template plane<(NP - 2) & 1>() + kTileLen * (t >> 4);
     const int l = t & 15;
-    DBP_CHECK(272 * (t >> 4) + 272 <= Shm<LOGN>::plane_len());
+    DBP_CHECK(kTileLen * (t >> 4) + kTileLen <= sh.plane_len());
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) tile[l + 17 * k] = v[k];
+    for (int k = 0; k < 16; ++k) tile[l + kTilePitch * k] = v[k];
     __syncwarp();
+    if constexpr (kTilePitch % 2 == 0) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = tile[17 * l + e];
+      for (int e = 0; e < 16; e += 2) ld_pair(tile + kTilePitch * l + e, v[e], v[e + 1]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = tile[kTilePitch * l + e];
+    }
     dft<16, false>(v);  // last pass: group (h, l)
   } else if constexpr (P < NP - 1) {
     // middle radix-16 pass: group g = t, ns = t mod S_P
@@ -452,20 +526,20 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
     twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
     sh.before_write();
     {
-      float2* plane = sh.plane();
+      float2* plane = sh.template plane<(P + 1) & 1>();
 #pragma unroll
       for (int m = 0; m < 16; ++m) {
-        DBP_CHECK(side_index<LOGN, P>(t, m) < Shm<LOGN>::plane_len());
+        DBP_CHECK(side_index<LOGN, P>(t, m) < sh.plane_len());
         plane[side_index<LOGN, P>(t, m)] = v[m];
       }
     }
     sh.after_write();
     {
-      const float2* plane = sh.plane();
+      const float2* plane = sh.template plane<(P + 1) & 1>();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) {
-        DBP_CHECK(xchg_index<LOGN, P>(base + (e << LS1)) < Shm<LOGN>::plane_len());
+        DBP_CHECK(xchg_index<LOGN, P>(base + (e << LS1)) < sh.plane_len());
         v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
       }
     }
@@ -475,8 +549,8 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN>& sh, const fl
   }
 }
 
-template <int LOGN, int P, int TWP = DBP_TW_POWERS>
-__device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tw,
+template <int LOGN, int P, int TWP = DBP_TW_POWERS, bool DB = false>
+__device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, DB>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T, NP = G::NP;
@@ -488,22 +562,22 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
     fft_inv<LOGN, 1, TWP>(v, sh, tw, t);
     sh.before_write();
     if constexpr (G::X01_PAIRED) {
-      float2* plane = sh.plane() + 272 * (t >> 4) + 2 * (t & 15);
+      float2* plane = sh.template plane<0>() + kTileLen * (t >> 4) + 2 * (t & 15);
 #pragma unroll
       for (int e = 0; e < 8; ++e) st_pair(plane + 32 * e, v[e], v[e + 8]);
     } else {
-      float2* plane = sh.plane();
+      float2* plane = sh.template plane<0>();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) plane[xchg_index<LOGN, 0>(base + (e << LS1))] = v[e];
     }
     sh.after_write();
     if constexpr (G::X01_PAIRED) {
-      const float2* plane = sh.plane() + 2 * t;
+      const float2* plane = sh.template plane<0>() + 2 * t;
 #pragma unroll
-      for (int m = 0; m < 16; m += 2) ld_pair(plane + 272 * (m >> 1), v[m], v[m + 1]);
+      for (int m = 0; m < 16; m += 2) ld_pair(plane + kTileLen * (m >> 1), v[m], v[m + 1]);
     } else {
-      const float2* plane = sh.plane();
+      const float2* plane = sh.template plane<0>();
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, 0>(t, m)];
     }
@@ -519,14 +593,19 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
     }
   } else if constexpr (NP >= 3 && P == NP - 2) {
     dft<16, true>(v);  // last pass
-    float2* tile = sh.plane() + 272 * (t >> 4);
+    float2* tile = sh.template plane<(NP - 2) & 1>() + kTileLen * (t >> 4);
     const int l = t & 15;
     __syncwarp();
+    if constexpr (kTilePitch % 2 == 0) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) tile[17 * l + e] = v[e];
+      for (int e = 0; e < 16; e += 2) st_pair(tile + kTilePitch * l + e, v[e], v[e + 1]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) tile[kTilePitch * l + e] = v[e];
+    }
     __syncwarp();
 #pragma unroll
-    for (int k = 0; k < 16; ++k) v[k] = tile[l + 17 * k];
+    for (int k = 0; k < 16; ++k) v[k] = tile[l + kTilePitch * k];
     twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
     dft<16, true>(v);
   } else if constexpr (P < NP - 1) {
@@ -534,14 +613,14 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
     fft_inv<LOGN, P + 1, TWP>(v, sh, tw, t);
     sh.before_write();
     {
-      float2* plane = sh.plane();
+      float2* plane = sh.template plane<P & 1>();
       const int base = ((t >> LS1) << (LS1 + 4)) + (t & ((1 << LS1) - 1));
 #pragma unroll
       for (int e = 0; e < 16; ++e) plane[xchg_index<LOGN, P>(base + (e << LS1))] = v[e];
     }
     sh.after_write();
     {
-      const float2* plane = sh.plane();
+      const float2* plane = sh.template plane<P & 1>();
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
@@ -553,8 +632,8 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN>& sh, const fl
 }
 
 // FFT -> x table (bins in register order, 1/N folded in) -> IFFT
-template <int LOGN>
-__device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN>& sh, const float2* __restrict__ tab,
+template <int LOGN, bool DB>
+__device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN, DB>& sh, const float2* __restrict__ tab,
                                            const float2* __restrict__ tw, int t) {
   fft_fwd<LOGN, 0>(v, sh, tw, t);
   apply_table<LOGN>(v, tab, Geo<LOGN>::NP == 1 ? 0 : t);
@@ -680,31 +759,34 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
   store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
 }
 
-template <int LOGN>
-__device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const KernelParams& kp,
+template <int LOGN, bool DB>
+__device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, DB>& sh, const KernelParams& kp,
                                        int step_idx, int t, int pol, const float* __restrict__ cptr) {
   // per-item coefficient sets (training batches) read from global memory
   const float c0 = kp.coeff_stride ? __ldg(cptr) : kp.c[0];
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
   const float2 sg = __ldg(kp.steps + step_idx);  // (a_j, g_j)
-  // total dual-pol intensity: own |v|^2 plus the partner lane's (lane ^ 16)
-  float inten[16];
+  // total dual-pol intensity of positions t + T m, m = 8 pol .. 8 pol + 7:
+  // each lane of a pair forms half of the 16 (own |v|^2 plus the partner
+  // lane's, one shuffle per two positions)
+  float inten[8];
 #pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    const float own = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
-    const float other = __shfl_xor_sync(0xffffffffu, own, 16);
-    inten[m] = pol ? other + own : own + other;
+  for (int m = 0; m < 8; ++m) {
+    const float lo = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
+    const float hi = fmaf(v[m + 8].x, v[m + 8].x, v[m + 8].y * v[m + 8].y);
+    const float other = __shfl_xor_sync(0xffffffffu, pol ? lo : hi, 16);
+    inten[m] = (pol ? hi : lo) + other;
   }
   if (kp.nc == 0) {
     // F = c0 I: each lane of the pair evaluates half the factors, then swaps
     float2 fac[8];
     if (kp.precise_sincos) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<true>(sg.x, sg.y, c0 * (pol ? inten[8 + i] : inten[i]));
+      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<true>(sg.x, sg.y, c0 * inten[i]);
     } else {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<false>(sg.x, sg.y, c0 * (pol ? inten[8 + i] : inten[i]));
+      for (int i = 0; i < 8; ++i) fac[i] = rot_factor<false>(sg.x, sg.y, c0 * inten[i]);
     }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -716,31 +798,34 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
     }
   } else {
     const int pw = kp.fir_pad;
-    // intensity buffer (logical [-pw, N + pw)), (cos, sin) buffer behind it
-    float* ibuf = sh.fir();
-    float2* csbuf = reinterpret_cast<float2*>(sh.fir() + fir_phys(N + 2 * pw) + 4);
-    if constexpr (!Geo<LOGN>::SEP_FIR) __syncthreads();
-    // both lanes of a pair write the same 16 values (same addresses, no
-    // divergence): fir_phys(m T + t + pw) = m (5T/4) + fir_phys(t + pw) for T >= 16
+    // intensity buffer (logical [-pw, N + pw)) and (cos, sin) buffer: regions
+    // 1 and 0 when double-buffered, else the second behind the first
+    float* ibuf = sh.template region<1>();
+    float2* csbuf = DB ? reinterpret_cast<float2*>(sh.template region<0>())
+                       : reinterpret_cast<float2*>(ibuf + fir_phys(N + 2 * pw) + 4);
+    // each lane stores its half of the intensities
+    sh.before_write();
+    const int m0 = 8 * pol;
     if constexpr (T >= 16) {
-      float* ib = ibuf + fir_phys(t + pw);
+      // fir_phys(m T + t + pw) = m (5T/4) + fir_phys(t + pw) for T >= 16
+      float* ib = ibuf + fir_phys(t + pw) + m0 * (5 * T / 4);
 #pragma unroll
-      for (int m = 0; m < 16; ++m) ib[m * (5 * T / 4)] = inten[m];
+      for (int m = 0; m < 8; ++m) ib[m * (5 * T / 4)] = inten[m];
       if (pw <= T) {
-        if (t < pw) ibuf[fir_phys(t + N + pw)] = inten[0];                    // j = t < pw
-        if (t >= T - pw) ibuf[fir_phys(15 * T + t - N + pw)] = inten[15];     // j >= N - pw
+        if (!pol && t < pw) ibuf[fir_phys(t + N + pw)] = inten[0];                // j = t < pw
+        if (pol && t >= T - pw) ibuf[fir_phys(15 * T + t - N + pw)] = inten[7];   // j >= N - pw
       } else {
 #pragma unroll
-        for (int m = 0; m < 16; ++m) {
-          const int j = m * T + t;
+        for (int m = 0; m < 8; ++m) {
+          const int j = (m0 + m) * T + t;
           if (j < pw) ibuf[fir_phys(j + N + pw)] = inten[m];
           if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[m];
         }
       }
     } else {
 #pragma unroll
-      for (int m = 0; m < 16; ++m) {
-        const int j = m * T + t;
+      for (int m = 0; m < 8; ++m) {
+        const int j = (m0 + m) * T + t;
         ibuf[fir_phys(j + pw)] = inten[m];
         if (j < pw) ibuf[fir_phys(j + N + pw)] = inten[m];
         if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[m];
@@ -756,7 +841,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
       case 33: fir8_fixed<33>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
       default: fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp, cptr, c0); break;
     }
-    __syncthreads();
+    sh.after_write();
     if constexpr (T >= 16) {
       const float2* cb = csbuf + cs_phys(t);  // cs_phys(m T + t) = m (9T/8) + cs_phys(t)
 #pragma unroll
@@ -772,8 +857,8 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN>& sh, const Ker
 // the kernel
 // ---------------------------------------------------------------------------
 // One CTA-sized group of blocks (block slices) through the whole program.
-template <int LOGN>
-__device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN>& sh, long long grp,
+template <int LOGN, bool DB>
+__device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, DB>& sh, long long grp,
                                               long long n_groups, int t, int slice, int pol) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
@@ -788,7 +873,38 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN>&
   const float* cptr = kp.coeff + (kp.coeff_stride ? item * kp.coeff_stride : 0);
   float2 v[16];
   const long long s0 = b * kp.step - kp.lead;  // global index of block sample 0
-  if (active) {
+  bool loaded = false;
+  if constexpr (G::TMA_LOAD) {
+    // Interior block, 16-byte aligned rows (uniform per CTA): one elected
+    // thread copies both polarisation rows (2 x 8N bytes) into the planes
+    // with the TMA bulk engine and every thread then reads its 16 samples
+    // from shared memory (conflict free; the first exchange's leading
+    // barrier orders these reads before the planes are overwritten).  The
+    // LDG path would stage 32 KB per CTA in flight through L1, whose
+    // capacity (the unified L1 / shared array) measurably limits the kernel.
+    __shared__ alignas(8) uint64_t in_bar;
+    const long long off = kp.cyclic ? s0 : s0 - kp.in_origin;
+    const float2* src = kp.in + item * kp.in_item_stride + off;
+    const bool bulk = active && (!kp.cyclic || (s0 >= 0 && s0 + N <= kp.n_total)) &&
+                      ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(kp.in_pol_stride * 8)) & 15) == 0;
+    if (bulk) {
+      if (threadIdx.x == 0) mbar_init(&in_bar, 1);
+      __syncthreads();
+      float2* dst0 = reinterpret_cast<float2*>(sh.base);
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&in_bar, 2 * N * sizeof(float2));
+        bulk_load(dst0, src, N * sizeof(float2), &in_bar);
+        bulk_load(dst0 + sh.plane_len(), src + kp.in_pol_stride, N * sizeof(float2), &in_bar);
+      }
+      mbar_wait(&in_bar, 0);
+      const float2* pl = dst0 + pol * sh.plane_len() + t;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) v[m] = pl[m * T];
+      loaded = true;
+    }
+  }
+  if (loaded) {
+  } else if (active) {
     const float2* pin = kp.in + item * kp.in_item_stride + pol * kp.in_pol_stride;
     if (!kp.cyclic || (s0 >= 0 && s0 + N <= kp.n_total)) {
       // interior block (or pre-extended chunk): one contiguous window, immediate offsets
@@ -891,9 +1007,8 @@ dbp_block_kernel(const KernelParams kp) {
   const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);  // position-thread index within the CTA
   const int t = q % T;
   const int slice = q / T;
-  Shm<LOGN> sh;
-  sh.base = reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats;
-  sh.pol = pol;
+  Shm<LOGN, G::DB> sh;
+  sh.init(reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats, kp.slice_floats, pol);
 
   // N <= 4096: one group per CTA (full-size grid).  N = 8192: a persistent
   // grid strides over the groups, prefetching the next group's input into L2

@@ -142,7 +142,7 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   kp.n_steps = p->n_steps;
   kp.nc = p->nc;
   kp.fir_pad = (p->nc + 3) & ~3;
-  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().separate_fir);
+  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().double_buffer);
   kp.precise_sincos = p->n_steps >= 3 ? 1 : 0;
   kp.tab_full = p->d_full;
   kp.tab_half = p->d_half ? p->d_half : p->d_full;
@@ -625,7 +625,7 @@ int dbp_run_coeff_batch(dbp_plan* p, const void* d_in, void* d_out, int64_t n_to
   base_params(p, kp);
   kp.nc = p->batch_nc;
   kp.fir_pad = (p->batch_nc + 3) & ~3;
-  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().separate_fir);
+  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().double_buffer);
   kp.coeff = p->d_coeff_batch;
   kp.coeff_stride = p->batch_stride;
   kp.in = static_cast<const float2*>(d_in);

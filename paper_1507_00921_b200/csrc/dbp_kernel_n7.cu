@@ -8,12 +8,8 @@ template <>
 cudaError_t launch_block_kernel<7>(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                     cudaStream_t stream) {
   using G = Geo<7>;
-  if (smem_bytes > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(dbp_block_kernel<7>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem_bytes);
-    if (e != cudaSuccess) return e;
-  }
+  cudaError_t e = set_smem_attrs(dbp_block_kernel<7>, smem_bytes);
+  if (e != cudaSuccess) return e;
   dbp_block_kernel<7><<<dim3((unsigned)n_ctas), dim3(launch_shape<7>().threads_x, launch_shape<7>().threads_y), smem_bytes, stream>>>(kp);
   return cudaGetLastError();
 }

@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "dbp_block_kernel.cuh"
 
 namespace dbp {
@@ -14,7 +16,7 @@ struct LaunchShape {
   int threads_x;  // threads per CTA along x
   int threads_y;  // along y
   int slices;     // block slices per CTA
-  bool separate_fir;  // FIR buffers behind the exchange planes (Geo::SEP_FIR)
+  bool double_buffer;  // two exchange regions per slice (Geo::DB)
   int min_ctas;       // resident CTAs per SM the kernel is built for (Geo::MIN_CTAS)
 };
 
@@ -28,9 +30,25 @@ template <int LOGN>
 cudaError_t launch_ssfm_row(const SimParams& sp, long long n_ctas, size_t smem_bytes, cudaStream_t stream,
                             bool column);
 
+// Dynamic shared memory opt-in and, for tuning experiments, the preferred
+// shared-memory carve-out in percent (env DBP_CARVEOUT; default: the driver's choice).
+template <class K>
+cudaError_t set_smem_attrs(K* kernel, size_t smem_bytes) {
+  static const int carveout = [] {
+    const char* v = std::getenv("DBP_CARVEOUT");
+    return v && *v ? std::atoi(v) : -1;
+  }();
+  if (smem_bytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+  }
+  if (carveout >= 0) return cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);
+  return cudaSuccess;
+}
+
 template <int LOGN>
 LaunchShape launch_shape() {
-  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::SEP_FIR, Geo<LOGN>::MIN_CTAS};
+  return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::DB, Geo<LOGN>::MIN_CTAS};
 }
 
 }  // namespace dbp

@@ -110,9 +110,8 @@ ssfm_row_kernel(const SimParams sp) {
   const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);
   const int t = q % T;
   const int slice = q / T;
-  Shm<LOGN> sh;
-  sh.base = reinterpret_cast<float*>(smem_raw) + slice * sp.slice_floats;
-  sh.pol = pol;
+  Shm<LOGN> sh;   // single region (the column tile aliases it)
+  sh.init(reinterpret_cast<float*>(smem_raw) + slice * sp.slice_floats, sp.slice_floats, pol);
 
   float2 v[16];
   bool active;
@@ -160,7 +159,6 @@ ssfm_row_kernel(const SimParams sp) {
     // the span on-chip -- FFT, dispersion (double-float table, bins in
     // register order), inverse FFT, Manakov rotation and loss
     for (int k = 0; k < sp.steps; ++k) {
-      if constexpr (G::SEP_FIR) __syncthreads();   // see kSimCA below
       const int tf = opaque(t);
       fft_fwd<LOGN, 0, 0>(v, sh, sp.tw, tf);
       apply_table_df<LOGN>(v, sp.lin, sp.lin_lo, G::NP == 1 ? 0 : tf);
@@ -180,11 +178,6 @@ ssfm_row_kernel(const SimParams sp) {
       sim_nonlinear(v, sp, pol, sp.mode == kSimC);
     }
     if (sp.mode != kSimC) {
-      // fft_fwd's first exchange skips its leading barrier when the FIR region
-      // is separate (Geo::SEP_FIR); here it follows fft_inv's plane reads
-      if constexpr (G::SEP_FIR) {
-        if (sp.mode == kSimCA) __syncthreads();
-      }
       const int tf = opaque(t);
       fft_fwd<LOGN, 0, 0>(v, sh, sp.tw, tf);
       sim_twiddle_rows<LOGN>(v, sp.wtab + (long long)row * N, tf);

@@ -56,10 +56,14 @@ def twiddles2(g: Geo2) -> np.ndarray:
     return np.asarray(out if out else [1.0 + 0j])
 
 
+TILE_PITCH = 18                 # kernel kTilePitch
+TILE_LEN = 16 * TILE_PITCH      # kernel kTileLen
+
+
 def pair_layout(i: int) -> int:
     """X01_PAIRED layout (N = 2048): i and i + 128 adjacent, then pad256."""
     j = 256 * (i >> 8) + 2 * (i & 127) + ((i >> 7) & 1)
-    return j + ((j >> 8) << 4)
+    return j + ((j >> 8) << 5)
 
 
 def xchg2(g: Geo2, p: int, i: int) -> int:
@@ -69,7 +73,7 @@ def xchg2(g: Geo2, p: int, i: int) -> int:
     if g.NP == 2 and p == 0:
         return i + (i >> 4)                      # pad16
     if g.NP >= 3 and p + 1 == g.NP - 2:
-        return i + ((i >> 8) << 4)               # pad256
+        return i + ((i >> 8) << 5)               # pad256 (32 per 256)
     return i
 
 
@@ -94,7 +98,7 @@ def conv_model2(block: np.ndarray, table: np.ndarray, logn: int, trace=None) -> 
     for t in range(T):
         for m in range(16):
             regs[t, m] = block[t + T * m]
-    plane = np.full(N + N // 16, np.nan + 0j)
+    plane = np.full(N + N // 8, np.nan + 0j)
 
     def dft(v, inv):
         return np.fft.ifft(v) * v.size if inv else np.fft.fft(v)
@@ -163,28 +167,28 @@ def conv_model2(block: np.ndarray, table: np.ndarray, logn: int, trace=None) -> 
             for k in range(1, 16):
                 regs[t, k] *= tw[g.tw_offset(p) + (t & (s - 1)) + (k - 1) * s]
         if p == g.NP - 2:
-            # half-warp-local transpose through the 272-element tile
+            # half-warp-local transpose through the 288-element tile (pitch 18)
             for h in range(T // 16):
-                tile = np.full(272, np.nan + 0j)
-                base = 272 * h
+                tile = np.full(TILE_LEN, np.nan + 0j)
+                base = TILE_LEN * h
                 for l in range(16):
                     for k in range(16):
-                        tile[l + 17 * k] = regs[16 * h + l, k]
+                        tile[l + TILE_PITCH * k] = regs[16 * h + l, k]
                         if trace is not None:
-                            trace.append(("tile", h, base + l + 17 * k))
+                            trace.append(("tile", h, base + l + TILE_PITCH * k))
                 for l in range(16):
                     for e in range(16):
-                        regs[16 * h + l, e] = tile[17 * l + e]
+                        regs[16 * h + l, e] = tile[TILE_PITCH * l + e]
             for t in range(T):
                 last(t)
             for h in range(T // 16):
-                tile = np.full(272, np.nan + 0j)
+                tile = np.full(TILE_LEN, np.nan + 0j)
                 for l in range(16):
                     for e in range(16):
-                        tile[17 * l + e] = regs[16 * h + l, e]
+                        tile[TILE_PITCH * l + e] = regs[16 * h + l, e]
                 for l in range(16):
                     for k in range(16):
-                        regs[16 * h + l, k] = tile[l + 17 * k]
+                        regs[16 * h + l, k] = tile[l + TILE_PITCH * k]
         else:
             cta_exchange_fwd(p)
             rec(p + 1)

@@ -3,7 +3,7 @@
 import numpy as np
 import pytest
 
-from .layout_model import fir_phys
+from .layout_model import TILE_LEN, TILE_PITCH, fir_phys
 
 
 def test_fir_padding_conflict_free():
@@ -40,7 +40,7 @@ def test_v2_exchanges_bijective_and_conflict_free(logn):
                       and not (g.NP == 3 and g.R0 == 8 and p == 0)]   # paired: own test
     for p in cta_boundaries:
         idx = [xchg2(g, p, i) for i in range(n)]
-        assert len(set(idx)) == n and max(idx) < n + n // 16
+        assert len(set(idx)) == n and max(idx) < n + n // 8
         if T < 16:
             continue
         ls1 = g.log_s(p + 1)
@@ -59,11 +59,17 @@ def test_v2_exchanges_bijective_and_conflict_free(logn):
         for h in range(T // 16):
             reads = {xchg2(g, p, ((t >> ls1) << (ls1 + 4)) + (t & 15) + (e << ls1))
                      for t in range(16 * h, 16 * h + 16) for e in range(16)}
-            assert min(reads) >= 272 * h and max(reads) < 272 * h + 256
-        # tile accesses: writes l + 17 k (fixed k), gathers 17 l + e (fixed e): 16 distinct banks
+            assert min(reads) >= TILE_LEN * h and max(reads) < TILE_LEN * h + 256
+        # tile accesses: 8-byte column side l + 18 k (fixed k): 16 consecutive elements;
+        # 16-byte row side 18 l + e (e even, 16-byte aligned): 8 lanes per phase hit
+        # 8 distinct 16-byte bank groups
         for k in range(16):
-            assert len({(l + 17 * k) % 16 for l in range(16)}) == 16
-            assert len({(17 * l + k) % 16 for l in range(16)}) == 16
+            assert len({(l + TILE_PITCH * k) % 16 for l in range(16)}) == 16
+        for e in range(0, 16, 2):
+            assert all((TILE_PITCH * l + e) % 2 == 0 for l in range(16))
+            for l0 in (0, 8):
+                assert len({((TILE_PITCH * l + e) // 2) % 8 for l in range(l0, l0 + 8)}) == 8
+        assert TILE_PITCH * 15 + 15 < TILE_LEN
 
 
 def test_v2_side_index_linear_forms():
@@ -75,9 +81,9 @@ def test_v2_side_index_linear_forms():
                 for m in range(16):
                     i = t + g.T * m
                     if g.NP >= 3 and p + 1 == g.NP - 2:
-                        closed = (t + g.T * m + (((g.T * m) >> 8) << 4)) if g.T <= 256 else \
-                                 (t + ((t >> 8) << 4)) + m * (g.T + g.T // 16)
-                        assert closed == i + ((i >> 8) << 4)
+                        closed = (t + g.T * m + (((g.T * m) >> 8) << 5)) if g.T <= 256 else \
+                                 (t + ((t >> 8) << 5)) + m * (g.T + g.T // 8)
+                        assert closed == i + ((i >> 8) << 5)
 
 
 def test_v2_twiddle_table_size():
@@ -88,22 +94,22 @@ def test_v2_twiddle_table_size():
 
 
 def test_x01_paired_closed_forms_and_banks():
-    # N = 2048: the kernel's 16-byte accesses st/ld_pair(2t + 272 (m/2)) and
-    # ld/st_pair(272 (t >> 4) + 2 (t & 15) + 32 e) address pair_layout exactly
+    # N = 2048: the kernel's 16-byte accesses st/ld_pair(2t + TILE_LEN (m/2)) and
+    # ld/st_pair(TILE_LEN (t >> 4) + 2 (t & 15) + 32 e) address pair_layout exactly
     g = Geo2(11)
     T = g.T
     for t in range(T):
         for m in range(0, 16, 2):
-            assert pair_layout(t + T * m) == 2 * t + 272 * (m // 2)
-            assert pair_layout(t + T * (m + 1)) == 2 * t + 272 * (m // 2) + 1
+            assert pair_layout(t + T * m) == 2 * t + TILE_LEN * (m // 2)
+            assert pair_layout(t + T * (m + 1)) == 2 * t + TILE_LEN * (m // 2) + 1
         k0, ns = t >> 4, t & 15
         for e in range(8):
             i = 256 * k0 + 16 * e + ns
-            assert pair_layout(i) == 272 * k0 + 32 * e + 2 * ns
+            assert pair_layout(i) == TILE_LEN * k0 + 32 * e + 2 * ns
             assert pair_layout(i + 128) == pair_layout(i) + 1
     # 16-byte accesses: 8 lanes per shared-memory phase hit 8 distinct 16-byte groups
     for t0 in range(0, T, 8):
         for m in range(0, 16, 2):
-            assert len({((2 * t + 272 * (m // 2)) // 2) % 8 for t in range(t0, t0 + 8)}) == 8
+            assert len({((2 * t + TILE_LEN * (m // 2)) // 2) % 8 for t in range(t0, t0 + 8)}) == 8
         for e in range(8):
-            assert len({((272 * (t >> 4) + 2 * (t & 15) + 32 * e) // 2) % 8 for t in range(t0, t0 + 8)}) == 8
+            assert len({((TILE_LEN * (t >> 4) + 2 * (t & 15) + 32 * e) // 2) % 8 for t in range(t0, t0 + 8)}) == 8

@@ -12,7 +12,12 @@ VARIANTS = {
     "v2_1024": ["-DDBP_THREADS_PER_SM=1024"],
     "v2_cta64": ["-DDBP_CTA_POSITIONS=64", "-DDBP_THREADS_PER_SM=768"],
     "single": ["-DDBP_DOUBLE_BUFFER=0"],
-    "aliasfir": ["-DDBP_SEPARATE_FIR=0"],
+    "double": ["-DDBP_DOUBLE_BUFFER=1"],
+    "t17": ["-DDBP_TILE_PITCH=17"],
+    "t18": ["-DDBP_TILE_PITCH=18"],
+    "tma": ["-DDBP_TMA_LOAD=1"],
+    "notma": ["-DDBP_TMA_LOAD=0"],
+    "tma_db": ["-DDBP_TMA_LOAD=1", "-DDBP_DOUBLE_BUFFER=1"],
     "bounds": ["-DDBP_DEBUG_BOUNDS=1"],
     "pw0": ["-DDBP_TW_POWERS=0"],
     "scalar": ["-DDBP_F32X2=0"],
@@ -25,7 +30,6 @@ VARIANTS = {
     "cta32_768": ["-DDBP_CTA_POSITIONS=32", "-DDBP_THREADS_PER_SM=768"],
     "cta32_1024": ["-DDBP_CTA_POSITIONS=32", "-DDBP_THREADS_PER_SM=1024"],
     "xopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
-    "sepfir": ["-DDBP_SEPARATE_FIR=1"],
     "nobar": ["-DDBP_EXPERIMENT_NOBAR=1"],   # timing ceiling only: wrong results
     "tps768": ["-DDBP_THREADS_PER_SM=768"],
     "tps1024": ["-DDBP_THREADS_PER_SM=1024"],
