@@ -159,6 +159,10 @@ int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms);
 /* The same with sm_100a's packed FFMA2 (fma.rn.f32x2: two float32 FMAs per
  * lane per instruction); the FP32 roofline uses the larger of the two.      */
 int dbp_probe_fp32x2_peak(int device, int iters, double* tflops, double* ms);
+/* Packed and scalar FMAs interleaved (8 FFMA2 + scalar_chains FFMA chains per
+ * step, scalar_chains in {2, 4, 8, 16}): whether the scalar FMA pipe adds
+ * throughput beside FFMA2 (roofline denominator check).                     */
+int dbp_probe_fp32_mixed_peak(int device, int iters, int scalar_chains, double* tflops, double* ms);
 
 /* ------------------------------------------------------------------------
  * Whole-waveform split-step link simulator: the reference's

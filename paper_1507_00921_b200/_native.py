@@ -46,6 +46,8 @@ SIGNATURES = {
                                      ctypes.POINTER(ctypes.c_double)]),
     "dbp_probe_fp32x2_peak": (_c_int, [_c_int, _c_int, ctypes.POINTER(ctypes.c_double),
                                        ctypes.POINTER(ctypes.c_double)]),
+    "dbp_probe_fp32_mixed_peak": (_c_int, [_c_int, _c_int, _c_int, ctypes.POINTER(ctypes.c_double),
+                                           ctypes.POINTER(ctypes.c_double)]),
     "dbp_plan_set_coeff_batch": (_c_int, [_c_void_p, _c_double_p, _c_int, _c_int]),
     "dbp_run_coeff_batch": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int64, _c_int64,
                                      _c_void_p]),
@@ -94,6 +96,8 @@ def load_library(path: str | os.PathLike | None = None):
                 "(python -m paper_1507_00921_b200.build); there is no CPU fallback")
         lib = ctypes.CDLL(str(p))
         for name, (res, args) in SIGNATURES.items():
+            if name in OPTIONAL and not hasattr(lib, name):
+                continue   # measurement probes absent from older A/B variant builds
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
@@ -135,6 +139,17 @@ def probe_fp32x2_peak(device: int = 0, iters: int = 4096) -> tuple[float, float]
     _check(load_library().dbp_probe_fp32x2_peak(int(device), int(iters), ctypes.byref(tf), ctypes.byref(ms)),
            "dbp_probe_fp32x2_peak")
     return tf.value, ms.value
+
+
+def probe_fp32_mixed_peak(device: int = 0, iters: int = 4096, scalar_chains: int = 8) -> tuple[float, float]:
+    """(TFLOP/s, ms) of 8 FFMA2 + ``scalar_chains`` FFMA chains interleaved on ``device``."""
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    _check(load_library().dbp_probe_fp32_mixed_peak(int(device), int(iters), int(scalar_chains), ctypes.byref(tf),
+                                                     ctypes.byref(ms)), "dbp_probe_fp32_mixed_peak")
+    return tf.value, ms.value
+
+
+OPTIONAL = {"dbp_probe_fp32_mixed_peak"}
 
 
 def _dptr(a: np.ndarray):

@@ -699,8 +699,24 @@ __device__ __forceinline__ void store_factors8(float2* __restrict__ csbuf, int p
   else store_factors8<false>(csbuf, p0, f, a, g);
 }
 
+#ifndef DBP_FIR_PACKED
+#define DBP_FIR_PACKED 0
+#endif
+// Packed FP32 pairs for the FIR (FADD2 / FMUL2 / FFMA2 on float2)
+__device__ __forceinline__ float2 p_mul(float2 a, float2 b) {
+  return f2_unpack(f2_mul(f2_pack(a.x, a.y), f2_pack(b.x, b.y)));
+}
+__device__ __forceinline__ float2 p_fma(float2 a, float2 b, float2 c) {
+  return f2_unpack(f2_fma(f2_pack(a.x, a.y), f2_pack(b.x, b.y), f2_pack(c.x, c.y)));
+}
+
 // 8 consecutive FIR outputs p0 .. p0+7 from a register window of the padded
 // intensity buffer, turned into rotation factors and stored to csbuf.
+// Packed: the window's aligned register pairs (w[2k], w[2k+1]) feed FADD2 /
+// FFMA2 directly when the pair of outputs and the tap share parity, so the
+// centre and even taps accumulate into output pairs (f[2j], f[2j+1]) and the
+// odd taps into (f[2j-1], f[2j]) (j = 0..4; f[-1], f[8] are discarded), the
+// two halves added at the end: 166 instead of 280 FP instructions at N_c = 17.
 template <int NC>
 __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
                                            int p0, float a, float g, const KernelParams& kp, int n_blk) {
@@ -713,6 +729,34 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
     const float4 q = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
     w[4 * m] = q.x; w[4 * m + 1] = q.y; w[4 * m + 2] = q.z; w[4 * m + 3] = q.w;
   }
+#if DBP_FIR_PACKED
+  auto wp = [&](int k) { return make_float2(w[k], w[k + 1]); };   // k even: one register pair
+  float2 e[4], o[5];
+  const float2 cc0 = make_float2(kp.c[0], kp.c[0]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) e[j] = p_mul(cc0, wp(2 * j + PW));
+#pragma unroll
+  for (int i = 2; i <= NC; i += 2) {
+    const float2 ci = make_float2(kp.c[i], kp.c[i]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) e[j] = p_fma(ci, c_add(wp(2 * j + PW - i), wp(2 * j + PW + i)), e[j]);
+  }
+#pragma unroll
+  for (int i = 1; i <= NC; i += 2) {
+    const float2 ci = make_float2(kp.c[i], kp.c[i]);
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const float2 s = c_add(wp(2 * j - 1 + PW - i), wp(2 * j - 1 + PW + i));
+      o[j] = i == 1 ? p_mul(ci, s) : p_fma(ci, s, o[j]);
+    }
+  }
+  float f[8];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    f[2 * j] = e[j].x + o[j].y;
+    f[2 * j + 1] = e[j].y + o[j + 1].x;
+  }
+#else
   float f[8];
 #pragma unroll
   for (int o = 0; o < 8; ++o) {
@@ -721,11 +765,12 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
     for (int i = 1; i <= NC; ++i) acc = fmaf(kp.c[i], w[o + PW - i] + w[o + PW + i], acc);
     f[o] = acc;
   }
+#endif
   store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
 }
 
-// any nc: taps in chunks of four (same summation order as fir8_fixed, so
-// every path gives identical bits for a given coefficient set)
+// any nc (and per-item coefficient sets): taps in chunks of four, scalar
+// (summation order differs from the packed fir8_fixed at the last ulp)
 __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
                                              int p0, int pw, float a, float g, const KernelParams& kp,
                                              const float* __restrict__ cptr, float c0) {

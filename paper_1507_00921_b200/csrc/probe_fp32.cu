@@ -56,7 +56,42 @@ __global__ void __launch_bounds__(256) fma2_probe_kernel(float* sink, int iters,
   if (s == 1234.5f) sink[threadIdx.x] = s;
 }
 
-int probe(int device, int iters, bool packed, double* tflops, double* ms) {
+// packed and scalar FMAs interleaved: 8 FFMA2 chains + S scalar FFMA chains
+// per step -- does the scalar FMA (fma-lite) pipe run beside FFMA2?
+template <int S>
+__global__ void __launch_bounds__(256) fma_mixed_probe_kernel(float* sink, int iters, float a, float b) {
+  unsigned long long r[8];
+  float q[S > 0 ? S : 1];
+  const unsigned long long av = dbp_pack(a, a), bv = dbp_pack(b, b);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) r[k] = dbp_pack(threadIdx.x * 1e-7f + k * 1e-7f, threadIdx.x * 1e-7f + k * 2e-7f);
+#pragma unroll
+  for (int k = 0; k < S; ++k) q[k] = threadIdx.x * 1e-7f + k * 3e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(r[k]) : "l"(av), "l"(bv));
+        if (k < S) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(q[k]) : "f"(a), "f"(b));
+      }
+#pragma unroll
+      for (int k = 8; k < S; ++k) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+f"(q[k]) : "f"(a), "f"(b));
+    }
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    float lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(r[k]));
+    s += lo + hi;
+  }
+#pragma unroll
+  for (int k = 0; k < S; ++k) s += q[k];
+  if (s == 1234.5f) sink[threadIdx.x] = s;
+}
+
+int probe(int device, int iters, bool packed, double* tflops, double* ms, int mixed = -1) {
   if (!tflops || iters < 1) return DBP_EINVAL;
   if (cudaSetDevice(device) != cudaSuccess) return DBP_ECUDA;
   int sms = 0;
@@ -68,7 +103,11 @@ int probe(int device, int iters, bool packed, double* tflops, double* ms) {
   cudaEventCreate(&e1);
   const int blocks = sms * 8;
   auto launch = [&](int it) {
-    if (packed) fma2_probe_kernel<<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
+    if (mixed == 2) fma_mixed_probe_kernel<2><<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
+    else if (mixed == 4) fma_mixed_probe_kernel<4><<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
+    else if (mixed == 8) fma_mixed_probe_kernel<8><<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
+    else if (mixed == 16) fma_mixed_probe_kernel<16><<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
+    else if (packed) fma2_probe_kernel<<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
     else fma_probe_kernel<<<blocks, 256>>>(sink, it, 0.9999f, 1e-7f);
   };
   launch(iters / 8 + 1);  // warm-up
@@ -82,7 +121,8 @@ int probe(int device, int iters, bool packed, double* tflops, double* ms) {
   cudaEventDestroy(e1);
   cudaFree(sink);
   if (err != cudaSuccess) return DBP_ECUDA;
-  const double flops = 2.0 * (packed ? 2.0 : 1.0) * 8.0 * 16.0 * (double)iters * 256.0 * (double)blocks;
+  const double per_step = mixed > 0 ? 16.0 + mixed : (packed ? 2.0 : 1.0) * 8.0;
+  const double flops = 2.0 * per_step * 16.0 * (double)iters * 256.0 * (double)blocks;
   *tflops = flops / (t * 1e-3) / 1e12;
   if (ms) *ms = t;
   return DBP_OK;
@@ -96,4 +136,10 @@ extern "C" int dbp_probe_fp32x2_peak(int device, int iters, double* tflops, doub
 
 extern "C" int dbp_probe_fp32_peak(int device, int iters, double* tflops, double* ms) {
   return probe(device, iters, false, tflops, ms);
+}
+
+// 8 packed + S scalar FMA chains interleaved (S = 2, 4, 8, 16)
+extern "C" int dbp_probe_fp32_mixed_peak(int device, int iters, int scalar_chains, double* tflops, double* ms) {
+  if (scalar_chains != 2 && scalar_chains != 4 && scalar_chains != 8 && scalar_chains != 16) return DBP_EINVAL;
+  return probe(device, iters, true, tflops, ms, scalar_chains);
 }

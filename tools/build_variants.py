@@ -15,6 +15,11 @@ VARIANTS = {
     "double": ["-DDBP_DOUBLE_BUFFER=1"],
     "t17": ["-DDBP_TILE_PITCH=17"],
     "t18": ["-DDBP_TILE_PITCH=18"],
+    "t1024_pw0": ["-DDBP_THREADS_PER_SM=1024", "-DDBP_TW_POWERS=0"],
+    "t1024_pw1": ["-DDBP_THREADS_PER_SM=1024", "-DDBP_TW_POWERS=1"],
+    "t1024_pw3": ["-DDBP_THREADS_PER_SM=1024", "-DDBP_TW_POWERS=3"],
+    "fir1": ["-DDBP_FIR_PACKED=0"],
+    "fir2": ["-DDBP_FIR_PACKED=1"],
     "tma": ["-DDBP_TMA_LOAD=1"],
     "notma": ["-DDBP_TMA_LOAD=0"],
     "tma_db": ["-DDBP_TMA_LOAD=1", "-DDBP_DOUBLE_BUFFER=1"],

@@ -72,6 +72,9 @@ for r in srows[2:]:
         tot += e
 out["instruction_mix_pct"] = {o: round(c / tot * 100, 2) for o, c in ops.most_common(16)}
 json.dump(out, open(prefix + "_ncu.json", "w"), indent=1)
+if launches == "-":   # no launch list
+    print(json.dumps(out, indent=1))
+    sys.exit(0)
 with open(launches) as fh:
     lines = [ln for ln in fh if not ln.startswith("==")]
 lr = list(csv.reader(lines))
