@@ -68,6 +68,9 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
 #ifndef DBP_EXPERIMENT_NOBAR
 #define DBP_EXPERIMENT_NOBAR 0
 #endif
+#ifndef DBP_EXPERIMENT_NOWAR
+#define DBP_EXPERIMENT_NOWAR 0
+#endif
 #ifndef DBP_CTA_POSITIONS
 #define DBP_CTA_POSITIONS 32
 #endif
@@ -337,6 +340,9 @@ struct Shm {
 #if DBP_EXPERIMENT_NOBAR   // timing experiment only: exchange barriers removed (WRONG results)
   __device__ __forceinline__ void before_write() const { __syncwarp(); }
   __device__ __forceinline__ void after_write() const { __syncwarp(); }
+#elif DBP_EXPERIMENT_NOWAR   // timing experiment only: write-after-read barriers removed (racy)
+  __device__ __forceinline__ void before_write() const {}
+  __device__ __forceinline__ void after_write() const { __syncthreads(); }
 #else
   __device__ __forceinline__ void before_write() const {
     if constexpr (!DB) __syncthreads();

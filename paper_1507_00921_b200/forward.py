@@ -16,6 +16,7 @@ seeded run reproduces the reference realisation.
 from __future__ import annotations
 
 import math
+import os
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -214,23 +215,30 @@ def propagate_link_batch(samples: np.ndarray, sample_rate: float, link: LinkConf
     dz, dz_eff, loss = _span_args(link.span, cfg)
     g_amp = 10.0 ** (link.gain_db / 20.0)
 
-    def draws(s):
-        # host draws of span s (ASE, Haar), made while the GPU propagates span s
+    def draw_noise(s, i, out):
+        out[i] = _ase_noise(n, sample_rate, link.gain_db, link.amp_noise_figure_db, link.center_wavelength_nm,
+                            children[i][2 * s])
+
+    def draws(s, rng_pool):
+        # host draws of span s (ASE, Haar), made while the GPU propagates span s;
+        # the waveforms' independent streams are drawn in parallel (numpy's
+        # generators release the GIL), each item's values unchanged
         noise = None
         if link.amp_noise_figure_db is not None:
-            noise = np.stack([_ase_noise(n, sample_rate, link.gain_db, link.amp_noise_figure_db,
-                                         link.center_wavelength_nm, ch[2 * s]) for ch in children])
+            noise = np.empty((b, 2, n), dtype=np.complex64)
+            list(rng_pool.map(lambda i: draw_noise(s, i, noise), range(b)))
         jones = np.stack([haar_random_unitary(ch[2 * s + 1]) for ch in children]) if link.pol_rotation else None
         return noise, jones
 
-    with ThreadPoolExecutor(max_workers=1) as pool:
-        pending = pool.submit(draws, 0)
+    workers = max(1, min(b, os.cpu_count() or 1))
+    with ThreadPoolExecutor(max_workers=1) as pool, ThreadPoolExecutor(max_workers=workers) as rng_pool:
+        pending = pool.submit(draws, 0, rng_pool)
         for s in range(link.num_spans):
             sim.span(b, sample_rate, link.span.beta2, link.span.gamma, dz, dz_eff, loss, cfg.steps_per_span,
                      cfg.nonlinear_enabled)
             noise, jones = pending.result()
             if s + 1 < link.num_spans:
-                pending = pool.submit(draws, s + 1)
+                pending = pool.submit(draws, s + 1, rng_pool)
             sim.amplify(b, g_amp, noise, jones)
     return sim.download(b)
 

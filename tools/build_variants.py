@@ -36,6 +36,7 @@ VARIANTS = {
     "cta32_1024": ["-DDBP_CTA_POSITIONS=32", "-DDBP_THREADS_PER_SM=1024"],
     "xopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "nobar": ["-DDBP_EXPERIMENT_NOBAR=1"],   # timing ceiling only: wrong results
+    "nowar": ["-DDBP_EXPERIMENT_NOWAR=1"],   # timing ceiling only: racy
     "tps768": ["-DDBP_THREADS_PER_SM=768"],
     "tps1024": ["-DDBP_THREADS_PER_SM=1024"],
     "pw3_1024": ["-DDBP_TW_POWERS=3", "-DDBP_THREADS_PER_SM=1024"],
