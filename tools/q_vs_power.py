@@ -10,7 +10,10 @@ rotations, 1 km steps; all launch powers as one batch) -> DBP variants
 (CD-only FFE, SSFM with 1 and 40 steps, ESSFM with 1 step and N_c = 17
 coefficients fitted per power by ``optimize_coefficients``) -> the
 receiver chain ``receive_batch`` (CMA, carrier recovery, decisions, BER).
-Reports Q (dB) per power and variant plus the time of every stage.
+Reports Q (dB) per power and variant plus the time of every stage: the whole
+experiment runs twice (the second pass must reproduce the first exactly) and
+the stage times are the second pass's, the first pass's total -- one-time
+set-up included -- is ``first_pass_total_s``; ``--no-warmup`` runs once.
 """
 
 from __future__ import annotations
@@ -58,6 +61,8 @@ def main():
     ap.add_argument("--powers", default="-4,-3,-2,-1,0,1,2,3,4")
     ap.add_argument("--steps-per-span", type=int, default=80)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--no-warmup", action="store_true",
+                    help="one pass only, timings include the cold starts")
     a = ap.parse_args()
     import paper_1507_00921_b200 as pb
 
@@ -69,53 +74,66 @@ def main():
     tx, sym = rrc_tx(m, seed=0)
     batch = np.stack([tx * math.sqrt(10 ** ((p - 30) / 10)) for p in powers]).astype(np.complex64)
 
-    timings = {}
-    t0 = time.perf_counter()
-    rx = pb.propagate_link_batch(batch, fs, link, pb.SsfmStepConfig(a.steps_per_span),
-                                 [np.random.SeedSequence([7, i]) for i in range(len(powers))])
-    timings["link_s"] = time.perf_counter() - t0
     quiet = pb.LinkConfig(span=span, num_spans=40, amp_gain_db=None, amp_noise_figure_db=None, pol_rotation=False)
     plan = pb.OverlapPlan(2048, 700)
-    variants = {
-        "cdc": pb.DbpConfig("ffe", plan, quiet),
-        "ssfm_1": pb.DbpConfig("ssfm", plan, quiet, num_steps=1),
-        "ssfm_40": pb.DbpConfig("ssfm", plan, quiet, num_steps=40),
-    }
-    q = {name: [] for name in list(variants) + ["essfm_1_nc17"]}
-    ber = {name: [] for name in q}
-    timings["dbp_s"] = 0.0
-    timings["train_s"] = 0.0
-    timings["rx_s"] = 0.0
-    for name, cfg in variants.items():
-        t0 = time.perf_counter()
-        out = pb.backpropagate_batch(rx, fs, cfg)
-        timings["dbp_s"] += time.perf_counter() - t0
-        t0 = time.perf_counter()
-        mets = pb.receive_batch(out, 28e9, sym)
-        timings["rx_s"] += time.perf_counter() - t0
-        q[name] = [None if isinstance(r, Exception) else r.q_factor_db for r in mets]
-        ber[name] = [None if isinstance(r, Exception) else r.ber for r in mets]
-    # ESSFM: one step, N_c = 17 coefficients fitted per launch power (train.py:86-188)
     tcfg = pb.TrainConfig(n_coeffs=17, target_steps_per_span=4, train_samples=16384, max_iterations=10)
-    outs = []
-    coeffs = []
-    for i in range(len(powers)):
-        sig = pb.DualPolSignal(rx[i, 0], rx[i, 1], fs)
-        geometry = pb.DbpConfig("essfm", plan, quiet, num_steps=1, coeffs=pb.EssfmCoefficients.identity(17))
-        t0 = time.perf_counter()
-        res = pb.optimize_coefficients(sig, geometry, tcfg)
-        timings["train_s"] += time.perf_counter() - t0
-        coeffs.append(res.coefficients.c.tolist())
-        cfg = pb.DbpConfig("essfm", plan, quiet, num_steps=1, coeffs=res.coefficients)
-        t0 = time.perf_counter()
-        outs.append(pb.backpropagate_batch(rx[i:i + 1], fs, cfg)[0])
-        timings["dbp_s"] += time.perf_counter() - t0
-    t0 = time.perf_counter()
-    mets = pb.receive_batch(np.stack(outs), 28e9, sym)
-    timings["rx_s"] += time.perf_counter() - t0
-    q["essfm_1_nc17"] = [None if isinstance(r, Exception) else r.q_factor_db for r in mets]
-    ber["essfm_1_nc17"] = [None if isinstance(r, Exception) else r.ber for r in mets]
 
+    def one_pass():
+        timings = {}
+        t0 = time.perf_counter()
+        rx = pb.propagate_link_batch(batch, fs, link, pb.SsfmStepConfig(a.steps_per_span),
+                                     [np.random.SeedSequence([7, i]) for i in range(len(powers))])
+        timings["link_s"] = time.perf_counter() - t0
+        variants = {
+            "cdc": pb.DbpConfig("ffe", plan, quiet),
+            "ssfm_1": pb.DbpConfig("ssfm", plan, quiet, num_steps=1),
+            "ssfm_40": pb.DbpConfig("ssfm", plan, quiet, num_steps=40),
+        }
+        q = {name: [] for name in list(variants) + ["essfm_1_nc17"]}
+        ber = {name: [] for name in q}
+        timings["dbp_s"] = 0.0
+        timings["train_s"] = 0.0
+        timings["rx_s"] = 0.0
+        for name, cfg in variants.items():
+            t0 = time.perf_counter()
+            out = pb.backpropagate_batch(rx, fs, cfg)
+            timings["dbp_s"] += time.perf_counter() - t0
+            t0 = time.perf_counter()
+            mets = pb.receive_batch(out, 28e9, sym)
+            timings["rx_s"] += time.perf_counter() - t0
+            q[name] = [None if isinstance(r, Exception) else r.q_factor_db for r in mets]
+            ber[name] = [None if isinstance(r, Exception) else r.ber for r in mets]
+        # ESSFM: one step, N_c = 17 coefficients fitted per launch power (train.py:86-188)
+        outs = []
+        coeffs = []
+        for i in range(len(powers)):
+            sig = pb.DualPolSignal(rx[i, 0], rx[i, 1], fs)
+            geometry = pb.DbpConfig("essfm", plan, quiet, num_steps=1, coeffs=pb.EssfmCoefficients.identity(17))
+            t0 = time.perf_counter()
+            res = pb.optimize_coefficients(sig, geometry, tcfg)
+            timings["train_s"] += time.perf_counter() - t0
+            coeffs.append(res.coefficients.c.tolist())
+            cfg = pb.DbpConfig("essfm", plan, quiet, num_steps=1, coeffs=res.coefficients)
+            t0 = time.perf_counter()
+            outs.append(pb.backpropagate_batch(rx[i:i + 1], fs, cfg)[0])
+            timings["dbp_s"] += time.perf_counter() - t0
+        t0 = time.perf_counter()
+        mets = pb.receive_batch(np.stack(outs), 28e9, sym)
+        timings["rx_s"] += time.perf_counter() - t0
+        q["essfm_1_nc17"] = [None if isinstance(r, Exception) else r.q_factor_db for r in mets]
+        ber["essfm_1_nc17"] = [None if isinstance(r, Exception) else r.ber for r in mets]
+        return q, ber, coeffs, timings
+
+    # pass 1 pays the one-time costs (simulator tables for this length, DBP
+    # engines, lazily loaded CUDA modules, cuFFT plans, receiver buffers);
+    # pass 2 repeats the identical experiment and gives the steady-state stage times
+    t0 = time.perf_counter()
+    q, ber, coeffs, timings = one_pass()
+    first = time.perf_counter() - t0
+    if not a.no_warmup:
+        q2, ber2, coeffs2, timings = one_pass()
+        assert q2 == q and coeffs2 == coeffs, "the repeated pass must reproduce the first"
+        timings["first_pass_total_s"] = first
     print("launch dBm " + " ".join(f"{p:>6.1f}" for p in powers))
     for name in q:
         print(f"{name:12s} " + " ".join("   n/a" if v is None else f"{min(v, 99.0):6.2f}" for v in q[name]))
