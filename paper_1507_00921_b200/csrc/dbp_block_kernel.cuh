@@ -46,13 +46,14 @@ namespace dbp {
 // CTAs hold max(1, 32 / T) blocks, so every block of N >= 512 has its own
 // CTA and its own barrier domain).  Tuned on B200 with the packed-FP32
 // kernel (tools/ab_small_n.sh, profiles/r1/ab_small_n.txt): N <= 256: 512
-// threads/SM; N = 512, 1024, 2048: 768 (85 / 80 regs); N >= 4096: 1024
-// (64 regs).  -DDBP_THREADS_PER_SM overrides.
+// threads/SM; N = 512, 1024: 896 (7 / 14 CTAs, 72 regs; +0.7% over 768,
+// profiles/r1/ab_896.txt); N = 2048: 768 (80 regs); N >= 4096: 1024 (64
+// regs).  -DDBP_THREADS_PER_SM overrides.
 __host__ __device__ constexpr int threads_per_sm(int logn) {
 #ifdef DBP_THREADS_PER_SM
   return DBP_THREADS_PER_SM + 0 * logn;
 #else
-  return logn <= 8 ? 512 : (logn <= 11 ? 768 : 1024);
+  return logn <= 8 ? 512 : (logn <= 10 ? 896 : (logn == 11 ? 768 : 1024));
 #endif
 }
 // Block input through the TMA bulk-copy engine into the exchange planes

@@ -18,6 +18,7 @@ VARIANTS = {
     "t1024_pw0": ["-DDBP_THREADS_PER_SM=1024", "-DDBP_TW_POWERS=0"],
     "t1024_pw1": ["-DDBP_THREADS_PER_SM=1024", "-DDBP_TW_POWERS=1"],
     "t1024_pw3": ["-DDBP_THREADS_PER_SM=1024", "-DDBP_TW_POWERS=3"],
+    "tps896": ["-DDBP_THREADS_PER_SM=896"],
     "fir1": ["-DDBP_FIR_PACKED=0"],
     "fir2": ["-DDBP_FIR_PACKED=1"],
     "tma": ["-DDBP_TMA_LOAD=1"],
