@@ -997,32 +997,12 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     }
   }
 
-  // operator program (dbp.py:212-233)
-  int n_ops;
-  if (kp.program == kFFE) n_ops = 1;
-  else if (kp.program == kRotateOnly) n_ops = kp.n_steps;
-  else n_ops = 2 * kp.n_steps + (kp.arrangement == kSymmetric ? 1 : 0);
-
+  // operator program (dbp.py:212-233), decoded on the host (KernelParams)
+  const int n_ops = kp.n_ops;
   for (int op = 0; op < n_ops; ++op) {
-    bool is_conv;
-    int sidx = 0;
-    const float2* tab = kp.tab_full;
-    if (kp.program == kFFE) {
-      is_conv = true;
-    } else if (kp.program == kRotateOnly) {
-      is_conv = false;
-      sidx = op;
-    } else if (kp.arrangement == kSymmetric) {
-      is_conv = (op & 1) == 0;
-      sidx = op >> 1;
-      if (op == 0 || op == n_ops - 1) tab = kp.tab_half;
-    } else if (kp.arrangement == kLinearFirst) {
-      is_conv = (op & 1) == 0;
-      sidx = op >> 1;
-    } else {
-      is_conv = (op & 1) == 1;
-      sidx = op >> 1;
-    }
+    const bool is_conv = kp.conv_all || (op & 1) == kp.conv_parity;
+    const float2* tab = kp.half_ends && (op == 0 || op == n_ops - 1) ? kp.tab_half : kp.tab_full;
+    const int sidx = op >> kp.sidx_shift;
     if (is_conv) {
       conv_block<LOGN>(v, sh, tab, kp.twiddle, t);
     } else {

@@ -140,6 +140,19 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   kp.program = p->program;
   kp.arrangement = p->arrangement;
   kp.n_steps = p->n_steps;
+  if (p->program == dbp::kFFE) {
+    kp.n_ops = 1;
+    kp.conv_all = 1;
+    kp.conv_parity = -1;
+  } else if (p->program == dbp::kRotateOnly) {
+    kp.n_ops = p->n_steps;
+    kp.conv_parity = -1;
+  } else {
+    kp.n_ops = 2 * p->n_steps + (p->arrangement == dbp::kSymmetric ? 1 : 0);
+    kp.conv_parity = p->arrangement == dbp::kNonlinearFirst ? 1 : 0;
+    kp.half_ends = p->arrangement == dbp::kSymmetric ? 1 : 0;
+    kp.sidx_shift = 1;
+  }
   kp.nc = p->nc;
   kp.fir_pad = (p->nc + 3) & ~3;
   kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().double_buffer);

@@ -31,6 +31,15 @@ struct KernelParams {
   int program;                // Program
   int arrangement;            // Arrangement
   int n_steps;                // nonlinear steps
+  // operator program decoded on the host (dbp.py:212-233): n_ops operators;
+  // op is a convolution iff conv_all, or (op & 1) == conv_parity when
+  // conv_parity >= 0; the first and last op use tab_half iff half_ends;
+  // a rotation's step index is op >> sidx_shift
+  int n_ops;
+  int conv_all;
+  int conv_parity;
+  int half_ends;
+  int sidx_shift;
   int nc;                     // side coefficients of the intensity FIR
   int fir_pad;                // nc rounded up to a multiple of 4
   int slice_floats;           // shared floats per block slice
