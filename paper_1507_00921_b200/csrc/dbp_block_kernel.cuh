@@ -918,7 +918,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   const bool active = blk < kp.total_blocks;
   long long item = 0, b = 0;
   if (active) {
-    item = blk / kp.blocks_per_item;
+    item = kp.bpi_magic ? (long long)__umul64hi(kp.bpi_magic, (unsigned long long)blk) : blk / kp.blocks_per_item;
     b = kp.block_begin + (blk - item * kp.blocks_per_item);
   }
 

@@ -191,7 +191,12 @@ int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
     const long long resident = (long long)sms * sh.min_ctas * persistent;
     if (resident > 0 && resident < grid) grid = resident;
   }
-  cudaError_t e = d.launch[p->logn](kp, grid, smem, s);
+  dbp::KernelParams k = kp;
+  // item = blk / blocks_per_item by multiply-high (exact for 32-bit operands)
+  k.bpi_magic = 0;
+  if (kp.blocks_per_item > 1 && kp.blocks_per_item <= 0xffffffffLL && kp.total_blocks <= 0xffffffffLL)
+    k.bpi_magic = ~0ULL / (unsigned long long)kp.blocks_per_item + 1;
+  cudaError_t e = d.launch[p->logn](k, grid, smem, s);
   if (e != cudaSuccess) return cuda_fail(e, "dbp_block_kernel launch");
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return DBP_OK;

@@ -25,6 +25,8 @@ struct KernelParams {
   long long block_begin;      // first overlap-save block processed per item
   long long blocks_per_item;  // blocks processed per item in this launch
   long long total_blocks;     // blocks_per_item * items
+  unsigned long long bpi_magic;  // ceil(2^64 / blocks_per_item) when both fit 32 bits (else 0):
+                                 // blk / blocks_per_item = umulhi(bpi_magic, blk) (Lemire fastdiv)
   int cyclic;                 // 1: global index taken modulo n_total
   int step;                   // N - M
   int lead;                   // M / 2
