@@ -28,7 +28,11 @@
 // __syncwarp), and at N = 2048 the first exchange pairs positions i, i + T
 // into 16-byte accesses (Geo::X01_PAIRED).  Twiddles are built by powers of
 // one table load per group (DBP_TW_POWERS), and all complex arithmetic runs
-// on the packed FP32 pipe (FADD2 / FMUL2 / FFMA2, dft_small.cuh).
+// on the packed FP32 pipe (FADD2 / FMUL2 / FFMA2, dft_small.cuh).  The
+// operator program arrives decoded (KernelParams::n_ops, conv_parity, ...).
+// Measured-and-off compile-time options: double-buffered exchange regions
+// (DBP_DOUBLE_BUFFER), TMA bulk input (DBP_TMA_LOAD), packed FIR
+// (DBP_FIR_PACKED) -- DESIGN.md section 4.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
