@@ -990,7 +990,8 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     // L2 prefetch of the next group's block: one 128-byte line per thread and polarisation
     const long long nblk = (grp + gridDim.x) * G::BPC + slice;
     if (nblk < kp.total_blocks) {
-      const long long nitem = nblk / kp.blocks_per_item;
+      const long long nitem = kp.bpi_magic ? (long long)__umul64hi(kp.bpi_magic, (unsigned long long)nblk)
+                                           : nblk / kp.blocks_per_item;
       const long long nb = kp.block_begin + (nblk - nitem * kp.blocks_per_item);
       const long long ns0 = nb * kp.step - kp.lead;
       if (!kp.cyclic || (ns0 >= 0 && ns0 + N <= kp.n_total)) {
