@@ -147,6 +147,18 @@ def test_batch_items_bit_equal_single(rng):
         np.testing.assert_array_equal(batch[i], _run(x[i], cfg)[0])
 
 
+@pytest.mark.parametrize("n", [700, 1348, 1349, 2696, 4100])
+def test_batch_item_index_every_blocks_per_item(rng, n):
+    # blocks -> (item, block) (the kernel's multiply-high division): 1, 1, 2, 2
+    # and 4 blocks per item (step 1348), batch of 7, each item == its single run
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(4, STD),
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    x = (0.03 * (rng.normal(size=(7, 2, n)) + 1j * rng.normal(size=(7, 2, n)))).astype(np.complex64)
+    batch = _run(x, cfg)
+    for i in range(7):
+        np.testing.assert_array_equal(batch[i], _run(x[i], cfg)[0])
+
+
 @pytest.mark.parametrize("parts", [2, 3, 8])
 def test_block_range_shards_bit_equal_whole(rng, parts):
     # multi-GPU contract: chunks on multiples of N - M are bitwise equal
