@@ -80,8 +80,9 @@ def test_amplifier_and_rotation_match_reference(golden_fwd):
         pb.apply_jones_matrix(sig, np.eye(3))
 
 
-@pytest.mark.parametrize("log_n", [8, 9, 12, 15, 17, 20])
+@pytest.mark.parametrize("log_n", [8, 9, 10, 11, 12, 13, 14, 15, 17, 20])
 def test_span_matches_oracle_across_lengths(log_n):
+    # every layout boundary: block mode (<= 2^12), column tiles with N1 = 2^7 (2^13, 2^14) and 2^8
     n = 1 << log_n
     rng = np.random.default_rng(log_n)
     amp = math.sqrt(10 ** ((3.0 - 30) / 10) / 4.0)
