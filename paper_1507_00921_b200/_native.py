@@ -171,12 +171,13 @@ class NativePlan:
         self.device = int(device)
         self.block_len = int(block_len)
         self.overlap = int(overlap)
-        self.lock = threading.Lock()
+        self.lock = threading.RLock()
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
-            self._lib.dbp_plan_destroy(self._h)
-            self._h = ctypes.c_void_p()
+            with self.lock:   # never under a running call
+                self._lib.dbp_plan_destroy(self._h)
+                self._h = ctypes.c_void_p()
 
     def __del__(self):
         try:
@@ -308,11 +309,15 @@ class NativeSim:
         _check(lib.dbp_sim_create(ctypes.byref(h), int(device), int(log2_n), int(max_batch)), "dbp_sim_create")
         self._h, self._lib = h, lib
         self.device, self.n, self.max_batch = int(device), 1 << int(log2_n), int(max_batch)
+        # the simulator's device state (the resident waveform) belongs to one
+        # upload .. download sequence at a time: callers hold this lock
+        self.lock = threading.RLock()
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
-            self._lib.dbp_sim_destroy(self._h)
-            self._h = ctypes.c_void_p()
+            with self.lock:
+                self._lib.dbp_sim_destroy(self._h)
+                self._h = ctypes.c_void_p()
 
     def __del__(self):
         try:
@@ -361,11 +366,13 @@ class NativeRx:
         _check(lib.dbp_rx_create(ctypes.byref(h), int(device), int(n_symbols), int(max_batch)), "dbp_rx_create")
         self._h, self._lib = h, lib
         self.device, self.n_symbols, self.max_batch = int(device), int(n_symbols), int(max_batch)
+        self.lock = threading.RLock()   # one call at a time on the device buffers
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:
-            self._lib.dbp_rx_destroy(self._h)
-            self._h = ctypes.c_void_p()
+            with self.lock:
+                self._lib.dbp_rx_destroy(self._h)
+                self._h = ctypes.c_void_p()
 
     def __del__(self):
         try:
@@ -379,9 +386,10 @@ class NativeRx:
         out = np.empty((b, 2, self.n_symbols), dtype=np.complex128)
         reinits = np.zeros(b, dtype=np.int32)
         tp = np.empty((b, 4, taps), dtype=np.complex128) if want_taps else None
-        _check(self._lib.dbp_rx_equalize(self._h, x.ctypes.data, b, int(taps), float(step_size), int(passes),
-                                          out.ctypes.data, _iptr(reinits), None if tp is None else tp.ctypes.data),
-               "dbp_rx_equalize")
+        with self.lock:
+            _check(self._lib.dbp_rx_equalize(self._h, x.ctypes.data, b, int(taps), float(step_size), int(passes),
+                                              out.ctypes.data, _iptr(reinits), None if tp is None else tp.ctypes.data),
+                   "dbp_rx_equalize")
         return out, reinits, tp
 
     def carrier_recover(self, s: np.ndarray, symbol_rate: float, reference, window: int):
@@ -391,16 +399,18 @@ class NativeRx:
         out = np.empty_like(s)
         f_off = np.zeros(b)
         status = np.zeros(b, dtype=np.int32)
-        _check(self._lib.dbp_rx_carrier_recover(self._h, s.ctypes.data, b, float(symbol_rate),
-                                                None if ref is None else ref.ctypes.data, int(window),
-                                                out.ctypes.data, _dptr(f_off), _iptr(status)),
-               "dbp_rx_carrier_recover")
+        with self.lock:
+            _check(self._lib.dbp_rx_carrier_recover(self._h, s.ctypes.data, b, float(symbol_rate),
+                                                    None if ref is None else ref.ctypes.data, int(window),
+                                                    out.ctypes.data, _dptr(f_off), _iptr(status)),
+                   "dbp_rx_carrier_recover")
         return out, f_off, status
 
     def decide(self, s: np.ndarray) -> np.ndarray:
         s = np.ascontiguousarray(s, dtype=np.complex128)
         bits = np.empty(s.shape[:-1] + (2 * s.shape[-1],), dtype=np.uint8)
-        _check(self._lib.dbp_rx_decide(self._h, s.ctypes.data, s.shape[0], bits.ctypes.data), "dbp_rx_decide")
+        with self.lock:
+            _check(self._lib.dbp_rx_decide(self._h, s.ctypes.data, s.shape[0], bits.ctypes.data), "dbp_rx_decide")
         return bits
 
     def count_errors(self, dec: np.ndarray, ref: np.ndarray, skip_bits: int):
@@ -409,9 +419,10 @@ class NativeRx:
         b = dec.shape[0]
         errors = np.zeros(b, dtype=np.int64)
         counted = ctypes.c_int64()
-        _check(self._lib.dbp_rx_count_errors(self._h, dec.ctypes.data, b, ref.ctypes.data, int(skip_bits),
-                                              errors.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
-                                              ctypes.byref(counted)), "dbp_rx_count_errors")
+        with self.lock:
+            _check(self._lib.dbp_rx_count_errors(self._h, dec.ctypes.data, b, ref.ctypes.data, int(skip_bits),
+                                                  errors.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                                  ctypes.byref(counted)), "dbp_rx_count_errors")
         return errors, counted.value
 
     def chain(self, x: np.ndarray, taps, step_size, passes, symbol_rate, ref_symbols, window, skip_bits):
@@ -421,9 +432,10 @@ class NativeRx:
         ref = np.ascontiguousarray(ref_symbols, dtype=np.complex128)
         metrics = np.zeros((b, 6))
         status = np.zeros(b, dtype=np.int32)
-        _check(self._lib.dbp_rx_chain(self._h, x.ctypes.data, int(c64), b, int(taps), float(step_size), int(passes),
-                                      float(symbol_rate), ref.ctypes.data, int(window), int(skip_bits),
-                                      _dptr(metrics), _iptr(status)), "dbp_rx_chain")
+        with self.lock:
+            _check(self._lib.dbp_rx_chain(self._h, x.ctypes.data, int(c64), b, int(taps), float(step_size), int(passes),
+                                          float(symbol_rate), ref.ctypes.data, int(window), int(skip_bits),
+                                          _dptr(metrics), _iptr(status)), "dbp_rx_chain")
         return metrics, status
 
 

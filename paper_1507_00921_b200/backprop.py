@@ -194,8 +194,9 @@ def get_engine(cfg: DbpConfig, sample_rate: float, device: int = 0) -> DbpEngine
     with _ENGINES_LOCK:
         _ENGINES[key] = eng
         while len(_ENGINES) > _MAX_ENGINES:
-            _, old = _ENGINES.popitem(last=False)
-            old.close()
+            # dropped, not closed: a thread may still hold the evicted engine;
+            # its plan is freed with the last reference (NativePlan.__del__)
+            _ENGINES.popitem(last=False)
     return eng
 
 

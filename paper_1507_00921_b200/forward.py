@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import math
 import os
+import threading
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
@@ -69,18 +70,22 @@ def _log2_length(n: int) -> int:
 
 
 class _SimCache:
+    """One simulator per (device, length), grown to the largest batch seen.  A
+    replaced simulator is dropped, not closed: a thread still holding it
+    finishes its sequence and the handle is freed with the last reference."""
+
     sims: dict = {}
+    lock = threading.Lock()
 
     @classmethod
     def get(cls, device: int, log2_n: int, batch: int) -> _native.NativeSim:
         key = (device, log2_n)
-        sim = cls.sims.get(key)
-        if sim is None or sim.max_batch < batch:
-            if sim is not None:
-                sim.close()
-            sim = _native.NativeSim(device, log2_n, max(batch, 1))
-            cls.sims[key] = sim
-        return sim
+        with cls.lock:
+            sim = cls.sims.get(key)
+            if sim is None or sim.max_batch < batch:
+                sim = _native.NativeSim(device, log2_n, max(batch, 1))
+                cls.sims[key] = sim
+            return sim
 
 
 def _span_args(fiber: FiberParams, cfg: SsfmStepConfig):
@@ -99,10 +104,11 @@ def propagate_span(sig: DualPolSignal, fiber: FiberParams, cfg: SsfmStepConfig, 
     x = np.empty((1, 2, n), dtype=np.complex64)
     x[0, 0], x[0, 1] = sig.x, sig.y
     dz, dz_eff, loss = _span_args(fiber, cfg)
-    sim.upload(x)
-    sim.span(1, sig.sample_rate, fiber.beta2, fiber.gamma, dz, dz_eff, loss, cfg.steps_per_span,
-             cfg.nonlinear_enabled)
-    out = sim.download(1)[0]
+    with sim.lock:
+        sim.upload(x)
+        sim.span(1, sig.sample_rate, fiber.beta2, fiber.gamma, dz, dz_eff, loss, cfg.steps_per_span,
+                 cfg.nonlinear_enabled)
+        out = sim.download(1)[0]
     return DualPolSignal(out[0], out[1], sig.sample_rate)
 
 
@@ -133,9 +139,10 @@ def _apply(sig: DualPolSignal, g_amp: float, noise, jones, device: int) -> DualP
     sim = _SimCache.get(device, lg, 1)
     x = np.empty((1, 2, n), dtype=np.complex64)
     x[0, 0], x[0, 1] = sig.x, sig.y
-    sim.upload(x)
-    sim.amplify(1, g_amp, None if noise is None else noise[None], None if jones is None else jones[None])
-    out = sim.download(1)[0]
+    with sim.lock:
+        sim.upload(x)
+        sim.amplify(1, g_amp, None if noise is None else noise[None], None if jones is None else jones[None])
+        out = sim.download(1)[0]
     return DualPolSignal(out[0], out[1], sig.sample_rate)
 
 
@@ -211,7 +218,6 @@ def propagate_link_batch(samples: np.ndarray, sample_rate: float, link: LinkConf
         ss = r if isinstance(r, np.random.SeedSequence) else np.random.SeedSequence(r)
         children.append(ss.spawn(2 * link.num_spans))
     sim = _SimCache.get(device, lg, b)
-    sim.upload(x)
     dz, dz_eff, loss = _span_args(link.span, cfg)
     g_amp = 10.0 ** (link.gain_db / 20.0)
 
@@ -231,7 +237,8 @@ def propagate_link_batch(samples: np.ndarray, sample_rate: float, link: LinkConf
         return noise, jones
 
     workers = max(1, min(b, os.cpu_count() or 1))
-    with ThreadPoolExecutor(max_workers=1) as pool, ThreadPoolExecutor(max_workers=workers) as rng_pool:
+    with sim.lock, ThreadPoolExecutor(max_workers=1) as pool, ThreadPoolExecutor(max_workers=workers) as rng_pool:
+        sim.upload(x)
         pending = pool.submit(draws, 0, rng_pool)
         for s in range(link.num_spans):
             sim.span(b, sample_rate, link.span.beta2, link.span.gamma, dz, dz_eff, loss, cfg.steps_per_span,
@@ -240,7 +247,7 @@ def propagate_link_batch(samples: np.ndarray, sample_rate: float, link: LinkConf
             if s + 1 < link.num_spans:
                 pending = pool.submit(draws, s + 1, rng_pool)
             sim.amplify(b, g_amp, noise, jones)
-    return sim.download(b)
+        return sim.download(b)
 
 
 def propagate_link(sig: DualPolSignal, link: LinkConfig, cfg: SsfmStepConfig, rng=None, *,

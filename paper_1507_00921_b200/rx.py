@@ -13,6 +13,7 @@ Equalisation, carrier recovery, decisions and error counting run in the
 from __future__ import annotations
 
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -48,18 +49,23 @@ class RxMetrics:
 
 
 class _RxCache:
+    """One receiver per (device, length), grown to the largest batch seen; a
+    replaced one is dropped (freed with its last reference), not closed under
+    a caller that may still be using it.  Calls on one receiver serialise on
+    its lock (``_native.NativeRx``)."""
+
     rx: dict = {}
+    lock = threading.Lock()
 
     @classmethod
     def get(cls, device: int, n_symbols: int, batch: int) -> _native.NativeRx:
         key = (device, n_symbols)
-        r = cls.rx.get(key)
-        if r is None or r.max_batch < batch:
-            if r is not None:
-                r.close()
-            r = _native.NativeRx(device, n_symbols, max(batch, 1))
-            cls.rx[key] = r
-        return r
+        with cls.lock:
+            r = cls.rx.get(key)
+            if r is None or r.max_batch < batch:
+                r = _native.NativeRx(device, n_symbols, max(batch, 1))
+                cls.rx[key] = r
+            return r
 
 
 def qpsk_map(bits_i, bits_q) -> np.ndarray:
