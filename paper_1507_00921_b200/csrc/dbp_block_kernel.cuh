@@ -67,6 +67,10 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
 // extra barrier and shared reads cost 1.9% (ESSFM) / +0.1% (FFE); with
 // double-buffered exchanges on top it is +2.9% (FFE) / -0.8% (ESSFM)
 // (tools/ab.sh, variants tma / tma_db / notma).
+// Split write-after-read exchange barriers (Shm kShmSplitWar, see Geo).
+#ifndef DBP_SPLIT_WAR
+#define DBP_SPLIT_WAR 1
+#endif
 #ifndef DBP_TMA_LOAD
 #define DBP_TMA_LOAD 0
 #endif
@@ -126,6 +130,14 @@ struct Geo {
   // 228 KB (N = 128, 512 .. 2048): one CTA barrier per exchange instead of two
   static constexpr bool DB =
       DBP_DOUBLE_BUFFER && MIN_CTAS * (2 * 16 * plane_elems(N) * BPC + 1024) <= 228 * 1024;
+  // split write-after-read barriers (Shm kShmSplitWar, needs every warp in one
+  // slice): measured per block length against __syncthreads
+  // (profiles/r1/ab_split_war.txt): N = 256 +1.7%, 4096 +3 to +5%; N = 512
+  // -1.5%, 1024 -0.8%, 2048 -0.3% (ESSFM; FFE +2%), 8192 -17% (32 warps
+  // polling one mbarrier, one CTA per SM) -- on for N = 256 and 4096 only
+  // (DBP_SPLIT_WAR=2: every N >= 256, 0: none)
+  static constexpr bool SPLIT_WAR =
+      !DB && T >= 16 && (DBP_SPLIT_WAR == 2 || (DBP_SPLIT_WAR == 1 && (LOGN == 8 || LOGN == 12)));
   // one block per CTA and one group per CTA (no persistent loop): input by TMA
   static constexpr bool TMA_LOAD = DBP_TMA_LOAD && BPC == 1 && LOGN >= 9 && LOGN <= 12;
   // first exchange with 16-byte paired accesses (see fft_fwd)
@@ -296,6 +308,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -323,15 +338,33 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 // phase goes to the region NOT read in the phase before: "write; barrier;
 // read" (the barrier of the previous phase already ordered the last reads of
 // this region).  ESSFM block at N = 2048: 6 CTA barriers instead of 11.
-template <int LOGN, bool DB = false>
+//
+// Split write-after-read barriers (MODE kShmSplitWar, single region): the
+// barrier before an exchange's writes only has to know that every warp of
+// the slice finished its reads of the previous exchange.  Each warp arrives
+// on the slice's mbarrier right after its last read of a phase
+// (``reads_done``) and the next write phase waits on it (``before_write``),
+// so the wait overlaps the pass computed in between instead of a
+// __syncthreads.  Arrive / wait alternate strictly: one initial arrive at
+// kernel start, then per CTA-wide write phase one wait and, after the last
+// read before the next such phase, one arrive.
+enum ShmMode : int { kShmSync = 0, kShmDouble = 1, kShmSplitWar = 2 };
+
+template <int LOGN, int MODE = kShmSync>
 struct Shm {
+  static constexpr bool DB = MODE == kShmDouble;
+  static constexpr bool SPLIT = MODE == kShmSplitWar;
   float* base;    // region 0
   float* base1;   // region 1 (== base without double buffering)
   int pol;
+  uint64_t* war;  // SPLIT: the slice's write-after-read mbarrier
+  uint32_t war_phase;
   __device__ __forceinline__ void init(float* slice_base, int slice_floats, int polarisation) {
     base = slice_base;
     base1 = DB ? slice_base + slice_floats / 2 : slice_base;
     pol = polarisation;
+    war = nullptr;
+    war_phase = 0;
   }
   __device__ __forceinline__ static int plane_len() { return plane_elems(Geo<LOGN>::N); }
   template <int R>
@@ -345,14 +378,27 @@ struct Shm {
 #if DBP_EXPERIMENT_NOBAR   // timing experiment only: exchange barriers removed (WRONG results)
   __device__ __forceinline__ void before_write() const { __syncwarp(); }
   __device__ __forceinline__ void after_write() const { __syncwarp(); }
+  __device__ __forceinline__ void reads_done() const {}
 #elif DBP_EXPERIMENT_NOWAR   // timing experiment only: write-after-read barriers removed (racy)
   __device__ __forceinline__ void before_write() const {}
   __device__ __forceinline__ void after_write() const { __syncthreads(); }
+  __device__ __forceinline__ void reads_done() const {}
 #else
-  __device__ __forceinline__ void before_write() const {
-    if constexpr (!DB) __syncthreads();
+  __device__ __forceinline__ void before_write() {
+    if constexpr (SPLIT) {
+      mbar_wait(war, war_phase);
+      war_phase ^= 1u;
+    } else if constexpr (!DB) {
+      __syncthreads();
+    }
   }
   __device__ __forceinline__ void after_write() const { __syncthreads(); }
+  __device__ __forceinline__ void reads_done() const {
+    if constexpr (SPLIT) {
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(war);
+    }
+  }
 #endif
 };
 
@@ -449,8 +495,8 @@ __device__ __forceinline__ void apply_table_df(float2 (&v)[16], const float2* __
 // ---------------------------------------------------------------------------
 // TWP: which passes build twiddles by powers (DBP_TW_POWERS bits); the link
 // simulator passes 0 (table loads only: powers compound the magnitude error)
-template <int LOGN, int P, int TWP = DBP_TW_POWERS, bool DB = false>
-__device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, DB>& sh, const float2* __restrict__ tw,
+template <int LOGN, int P, int TWP = DBP_TW_POWERS, int MODE = kShmSync>
+__device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T, NP = G::NP;
@@ -504,6 +550,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, DB>& sh, cons
         v[e] = plane[xchg_index<LOGN, 0>(base + (e << LS1))];
       }
     }
+    if constexpr (NP != 3) sh.reads_done();   // NP == 3: the half-warp tile follows
     fft_fwd<LOGN, 1, TWP>(v, sh, tw, t);
   } else if constexpr (NP >= 3 && P == NP - 2) {
     // second-to-last pass (S = 16) + last pass, joined by a half-warp-local
@@ -554,14 +601,15 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, DB>& sh, cons
         v[e] = plane[xchg_index<LOGN, P>(base + (e << LS1))];
       }
     }
+    if constexpr (P + 1 != NP - 2) sh.reads_done();
     fft_fwd<LOGN, P + 1, TWP>(v, sh, tw, t);
   } else {
     dft<16, false>(v);  // last pass: S = 1, group g = t, bins t + T e
   }
 }
 
-template <int LOGN, int P, int TWP = DBP_TW_POWERS, bool DB = false>
-__device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, DB>& sh, const float2* __restrict__ tw,
+template <int LOGN, int P, int TWP = DBP_TW_POWERS, int MODE = kShmSync>
+__device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T, NP = G::NP;
@@ -592,6 +640,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, DB>& sh, cons
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, 0>(t, m)];
     }
+    sh.reads_done();
 #pragma unroll
     for (int q = 0; q < G0; ++q) {
       float2 u[R0];
@@ -617,6 +666,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, DB>& sh, cons
     __syncwarp();
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[l + kTilePitch * k];
+    sh.reads_done();
     twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
     dft<16, true>(v);
   } else if constexpr (P < NP - 1) {
@@ -635,6 +685,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, DB>& sh, cons
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
+    sh.reads_done();
     twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
     dft<16, true>(v);
   } else {
@@ -643,8 +694,8 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, DB>& sh, cons
 }
 
 // FFT -> x table (bins in register order, 1/N folded in) -> IFFT
-template <int LOGN, bool DB>
-__device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN, DB>& sh, const float2* __restrict__ tab,
+template <int LOGN, int MODE>
+__device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tab,
                                            const float2* __restrict__ tw, int t) {
   fft_fwd<LOGN, 0>(v, sh, tw, t);
   apply_table<LOGN>(v, tab, Geo<LOGN>::NP == 1 ? 0 : t);
@@ -815,8 +866,8 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
   store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
 }
 
-template <int LOGN, bool DB>
-__device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, DB>& sh, const KernelParams& kp,
+template <int LOGN, int MODE>
+__device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, const KernelParams& kp,
                                        int step_idx, int t, int pol, const float* __restrict__ cptr) {
   // per-item coefficient sets (training batches) read from global memory
   const float c0 = kp.coeff_stride ? __ldg(cptr) : kp.c[0];
@@ -857,7 +908,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, DB>& sh, const
     // intensity buffer (logical [-pw, N + pw)) and (cos, sin) buffer: regions
     // 1 and 0 when double-buffered, else the second behind the first
     float* ibuf = sh.template region<1>();
-    float2* csbuf = DB ? reinterpret_cast<float2*>(sh.template region<0>())
+    float2* csbuf = Shm<LOGN, MODE>::DB ? reinterpret_cast<float2*>(sh.template region<0>())
                        : reinterpret_cast<float2*>(ibuf + fir_phys(N + 2 * pw) + 4);
     // each lane stores its half of the intensities
     sh.before_write();
@@ -900,11 +951,16 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, DB>& sh, const
     sh.after_write();
     if constexpr (T >= 16) {
       const float2* cb = csbuf + cs_phys(t);  // cs_phys(m T + t) = m (9T/8) + cs_phys(t)
+      float2 cs[16];
 #pragma unroll
-      for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], cb[m * (9 * T / 8)]);
+      for (int m = 0; m < 16; ++m) cs[m] = cb[m * (9 * T / 8)];
+      sh.reads_done();
+#pragma unroll
+      for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], cs[m]);
     } else {
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], csbuf[cs_phys(m * T + t)]);
+      sh.reads_done();
     }
   }
 }
@@ -913,8 +969,8 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, DB>& sh, const
 // the kernel
 // ---------------------------------------------------------------------------
 // One CTA-sized group of blocks (block slices) through the whole program.
-template <int LOGN, bool DB>
-__device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, DB>& sh, long long grp,
+template <int LOGN, int MODE>
+__device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, MODE>& sh, long long grp,
                                               long long n_groups, int t, int slice, int pol) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
@@ -1044,8 +1100,17 @@ dbp_block_kernel(const KernelParams kp) {
   const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);  // position-thread index within the CTA
   const int t = q % T;
   const int slice = q / T;
-  Shm<LOGN, G::DB> sh;
+  constexpr int MODE = G::DB ? kShmDouble : (G::SPLIT_WAR ? kShmSplitWar : kShmSync);
+  Shm<LOGN, MODE> sh;
   sh.init(reinterpret_cast<float*>(smem_raw) + slice * kp.slice_floats, kp.slice_floats, pol);
+  if constexpr (MODE == kShmSplitWar) {
+    // one write-after-read mbarrier per slice, arrived on by each of its T/16 warps
+    __shared__ alignas(8) uint64_t war_bars[G::BPC];
+    if (threadIdx.x < G::BPC) mbar_init(&war_bars[threadIdx.x], T / 16);
+    __syncthreads();
+    sh.war = &war_bars[slice];
+    sh.reads_done();   // nothing to protect before the first write phase
+  }
 
   // N <= 4096: one group per CTA (full-size grid).  N = 8192: a persistent
   // grid strides over the groups, prefetching the next group's input into L2

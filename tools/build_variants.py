@@ -38,6 +38,9 @@ VARIANTS = {
     "xopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "nobar": ["-DDBP_EXPERIMENT_NOBAR=1"],   # timing ceiling only: wrong results
     "nowar": ["-DDBP_EXPERIMENT_NOWAR=1"],   # timing ceiling only: racy
+    "split": ["-DDBP_SPLIT_WAR=2"],
+    "splitsel": ["-DDBP_SPLIT_WAR=1"],
+    "nosplit": ["-DDBP_SPLIT_WAR=0"],
     "tps768": ["-DDBP_THREADS_PER_SM=768"],
     "tps1024": ["-DDBP_THREADS_PER_SM=1024"],
     "pw3_1024": ["-DDBP_TW_POWERS=3", "-DDBP_THREADS_PER_SM=1024"],
