@@ -67,6 +67,11 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
 // extra barrier and shared reads cost 1.9% (ESSFM) / +0.1% (FFE); with
 // double-buffered exchanges on top it is +2.9% (FFE) / -0.8% (ESSFM)
 // (tools/ab.sh, variants tma / tma_db / notma).
+// Block lengths compiled with the persistent group loop (the launcher uses it
+// for N = 8192; smaller N only as the DBP_PERSISTENT experiment).
+#ifndef DBP_PERSIST_MIN_LOGN
+#define DBP_PERSIST_MIN_LOGN 13
+#endif
 // Split write-after-read exchange barriers (Shm kShmSplitWar, see Geo).
 #ifndef DBP_SPLIT_WAR
 #define DBP_SPLIT_WAR 1
@@ -1117,7 +1122,7 @@ dbp_block_kernel(const KernelParams kp) {
   // meanwhile (the launcher sizes it; DBP_PERSISTENT).
   // (compile-time split: the strided loop costs ~0.5% where it is not used)
   const long long n_groups = (kp.total_blocks + G::BPC - 1) / G::BPC;
-  if constexpr (LOGN >= 13) {
+  if constexpr (LOGN >= DBP_PERSIST_MIN_LOGN) {
     for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x)
       process_group<LOGN>(kp, sh, grp, n_groups, t, slice, pol);
   } else {

@@ -182,7 +182,8 @@ int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
     return v ? std::atoi(v) : -1;
   }();
   // only the N = 8192 kernel loops; smaller N always get the full grid
-  const int persistent = p->logn < 13 ? 0 : env_persistent >= 0 ? env_persistent : 1;
+  const int persistent = p->logn < DBP_PERSIST_MIN_LOGN ? 0 : env_persistent >= 0 ? env_persistent
+                                                            : (p->logn >= 13 ? 1 : 0);
   long long grid = ctas;
   if (persistent > 0) {
     int dev = 0, sms = 0;

@@ -38,6 +38,7 @@ VARIANTS = {
     "xopt": ["-Xptxas", "--allow-expensive-optimizations=true"],
     "nobar": ["-DDBP_EXPERIMENT_NOBAR=1"],   # timing ceiling only: wrong results
     "nowar": ["-DDBP_EXPERIMENT_NOWAR=1"],   # timing ceiling only: racy
+    "persist11": ["-DDBP_PERSIST_MIN_LOGN=10"],
     "split": ["-DDBP_SPLIT_WAR=2"],
     "splitsel": ["-DDBP_SPLIT_WAR=1"],
     "nosplit": ["-DDBP_SPLIT_WAR=0"],
