@@ -317,7 +317,13 @@ def run_ours(a) -> int:
         from oracle.cpu_bench import CpuBaseline
         cores = os.cpu_count() or 1
         cb = CpuBaseline(port_kwargs(a), SAMPLE_RATE, n, POWER_DBM, cores)
+        # calibrate on two waveforms per core, then time a sample of ~10-30 s of
+        # CPU work: the whole per-GPU workload when it fits, else a slice of it
         waves = max(16, 2 * cores)
+        secs, _ = cb.step(waves, seed0=100_000)
+        per_wave = secs / waves
+        waves = a.waveforms if per_wave * a.waveforms <= 30.0 else \
+            max(waves, int(15.0 / per_wave) // cores * cores)
         secs, samples = cb.step(waves)
         one_core = cb.one_core_rate()
         cb.close()
