@@ -123,7 +123,9 @@ def workload_config(a, world: int) -> dict:
         "n_coeffs": a.nc if a.algorithm == "essfm" else 0, "block_len": a.block_len, "overlap": a.overlap,
         "waveforms_per_gpu": a.waveforms, "samples_per_waveform": 1 << a.log2_samples,
         "global_waveforms": a.waveforms * world, "sharding": f"waveforms split over {world} GPU(s), no collective",
-        "l2": "inputs (2 GiB/GPU) larger than L2; no flush",
+        "l2": (f"inputs ({a.waveforms * (16 << a.log2_samples) / 2**30:.3g} GiB/GPU) "
+               + ("larger than the 126 MB L2; no flush" if a.waveforms * (16 << a.log2_samples) > 126e6
+                  else "NOT larger than L2 (tuning run, not a bench line)")),
     }
 
 
