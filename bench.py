@@ -281,7 +281,7 @@ def run_ours(a) -> int:
         ("essfm", "symmetric", 1, 17, 2048, 700)
     if prof.exists() and default:
         pj = json.loads(prof.read_text())
-        if f"dbp_block_kernel<{int(math.log2(a.block_len))}>" in str(pj.get("kernel", "")):
+        if f"dbp_block_kernel<{int(math.log2(a.block_len))}" in str(pj.get("kernel", "")):
             traffic = pj["dram_bytes_per_sample"] * per_launch_samples
             traffic_src = ("profiles/latest_ncu.json: dram__bytes_read.sum + dram__bytes_write.sum of one "
                            "ncu --set full launch of this command, scaled per launch")
@@ -349,7 +349,8 @@ def run_ours(a) -> int:
                          "flops_per_sample": f_s, "traffic": traffic, "traffic_unit": "bytes per launch",
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": b_s * per_launch_samples,
-                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}>"},
+                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}, "
+                                   f"{'true' if a.algorithm == 'ffe' and a.block_len >= 4096 else 'false'}>"},
             "roofline_hbm": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved_gbs / hbm_peak, "bytes_per_sample": b_s,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},

@@ -500,7 +500,7 @@ __device__ __forceinline__ void apply_table_df(float2 (&v)[16], const float2* __
 // ---------------------------------------------------------------------------
 // TWP: which passes build twiddles by powers (DBP_TW_POWERS bits); the link
 // simulator passes 0 (table loads only: powers compound the magnitude error)
-template <int LOGN, int P, int TWP = DBP_TW_POWERS, int MODE = kShmSync>
+template <int LOGN, int P, int TWP = DBP_TW_POWERS, int MODE = kShmSync, bool CALLER_WAR = false>
 __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
@@ -522,7 +522,10 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     }
     // exchange into the pass-1 layout
     constexpr int LS1 = G::log_s(1);
-    sh.before_write();
+    // CALLER_WAR: the caller omits this exchange's write-after-read barrier
+    // (the FFE kernel's single convolution in a CTA that has not read shared
+    // memory yet)
+    if constexpr (!CALLER_WAR) sh.before_write();
     if constexpr (G::X01_PAIRED) {
       // R0 = 8, N = 2048: positions i and i + T pair up on both sides of this
       // exchange (registers (m, m+1) when writing, gathers (e, e+8) when
@@ -699,10 +702,10 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
 }
 
 // FFT -> x table (bins in register order, 1/N folded in) -> IFFT
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, bool CALLER_WAR = false>
 __device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tab,
                                            const float2* __restrict__ tw, int t) {
-  fft_fwd<LOGN, 0>(v, sh, tw, t);
+  fft_fwd<LOGN, 0, DBP_TW_POWERS, MODE, CALLER_WAR>(v, sh, tw, t);
   apply_table<LOGN>(v, tab, Geo<LOGN>::NP == 1 ? 0 : t);
   // value barrier: the inverse recomputes its indices instead of holding the
   // forward ones (and reloading twiddles) across the last pass
@@ -974,7 +977,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
 // the kernel
 // ---------------------------------------------------------------------------
 // One CTA-sized group of blocks (block slices) through the whole program.
-template <int LOGN, int MODE>
+template <int LOGN, int MODE, bool FFE_ONLY>
 __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, MODE>& sh, long long grp,
                                               long long n_groups, int t, int slice, int pol) {
   using G = Geo<LOGN>;
@@ -1064,6 +1067,19 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   }
 
   // operator program (dbp.py:212-233), decoded on the host (KernelParams)
+  if constexpr (FFE_ONLY) {
+    // linear-only program (dbp.py:185-191): one convolution with H.  Its
+    // exchange needs no write-after-read barrier when the CTA has not read
+    // shared memory before (one group per CTA, input by LDG, plain
+    // __syncthreads barriers): 3 CTA barriers instead of 4.  Used for N >= 4096
+    // (launch.h); at N = 8192 it also drops the generic kernel's stack spill.
+    // In the generic kernel the same skip costs more than it saves (the
+    // ESSFM / SSFM programs lose 0.1-1.8% to a moved barrier, a runtime op == 0
+    // predicate that spills, or a peeled first operator:
+    // profiles/r1/ab_fresh_start.txt).
+    constexpr bool kFresh = MODE == kShmSync && !G::TMA_LOAD && LOGN < DBP_PERSIST_MIN_LOGN;
+    conv_block<LOGN, MODE, kFresh>(v, sh, kp.tab_full, kp.twiddle, t);
+  } else {
   const int n_ops = kp.n_ops;
   for (int op = 0; op < n_ops; ++op) {
     const bool is_conv = kp.conv_all || (op & 1) == kp.conv_parity;
@@ -1074,6 +1090,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     } else {
       rotate<LOGN>(v, sh, kp, sidx, t, pol, cptr);
     }
+  }
   }
 
   if (active) {
@@ -1094,7 +1111,8 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   }
 }
 
-template <int LOGN>
+// FFE_ONLY: the single-convolution (FFE) program, launched for kFFE
+template <int LOGN, bool FFE_ONLY = false>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
 dbp_block_kernel(const KernelParams kp) {
   using G = Geo<LOGN>;
@@ -1124,9 +1142,9 @@ dbp_block_kernel(const KernelParams kp) {
   const long long n_groups = (kp.total_blocks + G::BPC - 1) / G::BPC;
   if constexpr (LOGN >= DBP_PERSIST_MIN_LOGN) {
     for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x)
-      process_group<LOGN>(kp, sh, grp, n_groups, t, slice, pol);
+      process_group<LOGN, MODE, FFE_ONLY>(kp, sh, grp, n_groups, t, slice, pol);
   } else {
-    process_group<LOGN>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
+    process_group<LOGN, MODE, FFE_ONLY>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
   }
 }
 

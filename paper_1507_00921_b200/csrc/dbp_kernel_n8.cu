@@ -7,11 +7,7 @@ namespace dbp {
 template <>
 cudaError_t launch_block_kernel<8>(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                     cudaStream_t stream) {
-  using G = Geo<8>;
-  cudaError_t e = set_smem_attrs(dbp_block_kernel<8>, smem_bytes);
-  if (e != cudaSuccess) return e;
-  dbp_block_kernel<8><<<dim3((unsigned)n_ctas), dim3(launch_shape<8>().threads_x, launch_shape<8>().threads_y), smem_bytes, stream>>>(kp);
-  return cudaGetLastError();
+  return launch_block_kernel_impl<8>(kp, n_ctas, smem_bytes, stream);
 }
 
 template <>

@@ -47,6 +47,34 @@ cudaError_t set_smem_attrs(K* kernel, size_t smem_bytes) {
 }
 
 template <int LOGN>
+LaunchShape launch_shape();
+
+// Block lengths whose linear (FFE) program runs the FFE-only instantiation
+// (measured, tools/ab_ffe_kernel.sh -> profiles/r1/ab_ffe_kernel.txt: N = 8192
+// +6.5%, 4096 +0.2%; N = 1024 / 2048 -0.8% / -0.15%, so they keep the generic
+// kernel)
+#ifndef DBP_FFE_KERNEL_MIN_LOGN
+#define DBP_FFE_KERNEL_MIN_LOGN 12
+#endif
+
+// The fused block kernel for one block length: the FFE-only instantiation for
+// the linear program (N >= 2^DBP_FFE_KERNEL_MIN_LOGN), the generic
+// operator-program kernel otherwise.
+template <int LOGN>
+cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
+                                     cudaStream_t stream) {
+  auto* kernel = dbp_block_kernel<LOGN, false>;
+  if constexpr (LOGN >= DBP_FFE_KERNEL_MIN_LOGN) {
+    if (kp.program == kFFE) kernel = dbp_block_kernel<LOGN, true>;
+  }
+  cudaError_t e = set_smem_attrs(kernel, smem_bytes);
+  if (e != cudaSuccess) return e;
+  const LaunchShape sh = launch_shape<LOGN>();
+  kernel<<<dim3((unsigned)n_ctas), dim3(sh.threads_x, sh.threads_y), smem_bytes, stream>>>(kp);
+  return cudaGetLastError();
+}
+
+template <int LOGN>
 LaunchShape launch_shape() {
   return LaunchShape{Geo<LOGN>::THREADS, 1, Geo<LOGN>::BPC, Geo<LOGN>::DB, Geo<LOGN>::MIN_CTAS};
 }

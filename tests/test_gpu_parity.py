@@ -395,3 +395,21 @@ def test_integration_stub_runs_and_matches(golden, manifest, tmp_path):
     errs = dbp_port.per_block_rel_l2(got, want, case["block_len"], case["overlap"])
     assert errs.max() <= TOL_BLOCK
     np.testing.assert_array_equal(got.astype(np.complex64), _run(x, cfg)[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_blk,m", [(4096, 700), (4096, 1400), (8192, 1024)])
+def test_ffe_kernel_large_blocks_match_oracle(n_blk, m):
+    # the FFE-only kernel instantiation (launch.h, N >= 4096): whole-signal cyclic
+    # framing with edge blocks, a ragged length and a 2-item batch, per-block
+    # rel-L2 <= 1e-5 against the oracle (dbp.py:185-191) and batch == single runs
+    gen = np.random.default_rng(n_blk + m)
+    span = pb.FiberParams(-21.68, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("ffe", pb.OverlapPlan(n_blk, m), quiet_link(40, span))
+    n = 5 * (n_blk - m) + 123
+    x = (0.02 * (gen.normal(size=(2, 2, n)) + 1j * gen.normal(size=(2, 2, n)))).astype(np.complex64)
+    got = _run(x, cfg)
+    for i in range(2):
+        want = dbp_port.backpropagate_arrays(x[i].astype(np.complex128), 56e9, port_config(cfg))
+        assert dbp_port.per_block_rel_l2(got[i], want, n_blk, m).max() <= TOL_BLOCK
+        np.testing.assert_array_equal(got[i], _run(x[i:i + 1], cfg)[0])
