@@ -350,7 +350,7 @@ def run_ours(a) -> int:
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": b_s * per_launch_samples,
                          "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}, "
-                                   f"{'true' if a.algorithm == 'ffe' and a.block_len >= 4096 else 'false'}>"},
+                                   f"{'true' if a.algorithm == 'ffe' and a.block_len >= 2048 else 'false'}>"},
             "roofline_hbm": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved_gbs / hbm_peak, "bytes_per_sample": b_s,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},

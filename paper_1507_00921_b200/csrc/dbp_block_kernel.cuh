@@ -60,6 +60,18 @@ __host__ __device__ constexpr int threads_per_sm(int logn) {
   return logn <= 8 ? 512 : (logn <= 10 ? 896 : (logn == 11 ? 768 : 1024));
 #endif
 }
+// Resident threads per SM of the FFE-only kernel (launch.h selects it for
+// N >= 2^DBP_FFE_KERNEL_MIN_LOGN).  Without the rotation it fits 64 registers,
+// so N = 2048 runs four 256-thread CTAs per SM instead of the ESSFM kernel's
+// three: FFE 87.0 -> 91.9 GS/s; 768 / 512 threads -0.1% / -9%
+// (profiles/r1/ab_ffe_tps.txt).  -DDBP_FFE_THREADS_PER_SM overrides.
+__host__ __device__ constexpr int ffe_threads_per_sm(int logn) {
+#ifdef DBP_FFE_THREADS_PER_SM
+  return DBP_FFE_THREADS_PER_SM + 0 * logn;
+#else
+  return logn == 11 ? 1024 : threads_per_sm(logn);
+#endif
+}
 // Block input through the TMA bulk-copy engine into the exchange planes
 // (Geo::TMA_LOAD): the loads bypass the L1 data path, so the kernel no
 // longer depends on the L1 share of the unified array (carve-out 86%: LDG
@@ -131,6 +143,9 @@ struct Geo {
   static constexpr int BPC = T >= DBP_CTA_POSITIONS ? 1 : DBP_CTA_POSITIONS / T;
   static constexpr int THREADS = 2 * T * BPC;
   static constexpr int MIN_CTAS = threads_per_sm(LOGN) / THREADS > 0 ? threads_per_sm(LOGN) / THREADS : 1;
+  // the FFE-only instantiation (no rotation, fewer live registers)
+  static constexpr int FFE_MIN_CTAS =
+      ffe_threads_per_sm(LOGN) / THREADS > 0 ? ffe_threads_per_sm(LOGN) / THREADS : 1;
   // two exchange regions per slice while MIN_CTAS CTAs still fit the SM's
   // 228 KB (N = 128, 512 .. 2048): one CTA barrier per exchange instead of two
   static constexpr bool DB =
@@ -1071,8 +1086,9 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     // linear-only program (dbp.py:185-191): one convolution with H.  Its
     // exchange needs no write-after-read barrier when the CTA has not read
     // shared memory before (one group per CTA, input by LDG, plain
-    // __syncthreads barriers): 3 CTA barriers instead of 4.  Used for N >= 4096
-    // (launch.h); at N = 8192 it also drops the generic kernel's stack spill.
+    // __syncthreads barriers): 3 CTA barriers instead of 4.  Used for N >= 2048
+    // (launch.h): at N = 2048 with 1024 threads per SM (ffe_threads_per_sm),
+    // at N = 8192 it also drops the generic kernel's stack spill.
     // In the generic kernel the same skip costs more than it saves (the
     // ESSFM / SSFM programs lose 0.1-1.8% to a moved barrier, a runtime op == 0
     // predicate that spills, or a peeled first operator:
@@ -1113,7 +1129,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
 
 // FFE_ONLY: the single-convolution (FFE) program, launched for kFFE
 template <int LOGN, bool FFE_ONLY = false>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS, Geo<LOGN>::MIN_CTAS)
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, FFE_ONLY ? Geo<LOGN>::FFE_MIN_CTAS : Geo<LOGN>::MIN_CTAS)
 dbp_block_kernel(const KernelParams kp) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;

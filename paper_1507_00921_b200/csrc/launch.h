@@ -50,11 +50,11 @@ template <int LOGN>
 LaunchShape launch_shape();
 
 // Block lengths whose linear (FFE) program runs the FFE-only instantiation
-// (measured, tools/ab_ffe_kernel.sh -> profiles/r1/ab_ffe_kernel.txt: N = 8192
-// +6.5%, 4096 +0.2%; N = 1024 / 2048 -0.8% / -0.15%, so they keep the generic
-// kernel)
+// (measured, profiles/r1/ab_ffe_kernel.txt, ab_ffe_tps.txt: N = 8192 +6.5%,
+// 4096 +0.2%, 2048 +5.6% at 1024 threads per SM; N = 1024 -0.2 to -2.7% at
+// any occupancy, so it keeps the generic kernel)
 #ifndef DBP_FFE_KERNEL_MIN_LOGN
-#define DBP_FFE_KERNEL_MIN_LOGN 12
+#define DBP_FFE_KERNEL_MIN_LOGN 11
 #endif
 
 // The fused block kernel for one block length: the FFE-only instantiation for

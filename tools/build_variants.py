@@ -7,6 +7,10 @@ from paper_1507_00921_b200 import build as B
 ROOT = Path(__file__).resolve().parent.parent / "build" / "variants"
 VARIANTS = {
     "base": [],
+    "ffe10": ["-DDBP_FFE_KERNEL_MIN_LOGN=10"],
+    "ffe10_768": ["-DDBP_FFE_KERNEL_MIN_LOGN=10", "-DDBP_FFE_THREADS_PER_SM=768"],
+    "ffe10_1024": ["-DDBP_FFE_KERNEL_MIN_LOGN=10", "-DDBP_FFE_THREADS_PER_SM=1024"],
+    "ffe10_512": ["-DDBP_FFE_KERNEL_MIN_LOGN=10", "-DDBP_FFE_THREADS_PER_SM=512"],
     "v2_512": ["-DDBP_THREADS_PER_SM=512"],
     "tps640": ["-DDBP_THREADS_PER_SM=640"],
     "v2_1024": ["-DDBP_THREADS_PER_SM=1024"],
