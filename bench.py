@@ -103,6 +103,18 @@ def work_per_sample(a, gains_not_one: bool = False) -> tuple[float, float]:
     return flops / (n - m), 16.0 * (2 * n - m) / (n - m)
 
 
+def kernel_prog(a) -> int:
+    """Which instantiation of the block kernel the launcher picks (csrc/launch.h):
+    0 generic, 1 FFE-only, 2 no-FIR split-step."""
+    if a.block_len < 2048:
+        return 0
+    if a.algorithm == "ffe":
+        return 1
+    if a.algorithm == "ssfm" or a.nc == 0:
+        return 2
+    return 0
+
+
 def cpu_model() -> str:
     """The host CPU model (state the cores and the model beside the CPU figure)."""
     try:
@@ -349,8 +361,7 @@ def run_ours(a) -> int:
                          "flops_per_sample": f_s, "traffic": traffic, "traffic_unit": "bytes per launch",
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": b_s * per_launch_samples,
-                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}, "
-                                   f"{'true' if a.algorithm == 'ffe' and a.block_len >= 2048 else 'false'}>"},
+                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}, {kernel_prog(a)}>"},
             "roofline_hbm": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved_gbs / hbm_peak, "bytes_per_sample": b_s,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},

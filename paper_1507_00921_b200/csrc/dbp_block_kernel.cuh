@@ -72,6 +72,20 @@ __host__ __device__ constexpr int ffe_threads_per_sm(int logn) {
   return logn == 11 ? 1024 : threads_per_sm(logn);
 #endif
 }
+// Resident threads per SM of the no-FIR split-step kernel (SSFM, ESSFM N_c = 0;
+// launch.h selects it for N >= 2^DBP_NOFIR_KERNEL_MIN_LOGN).  Without the FIR
+// window (48 floats beside the 16 samples) it fits 64 registers without
+// spills: N = 2048 runs 1024 threads per SM (SSFM-20 +2.0 / +2.6%, ESSFM
+// N_c = 0 +4.3%), N = 4096 / 8192 lose the generic kernel's stack spill (+1% /
+// +4.2%) (profiles/r1/ab_nofir.txt).  -DDBP_NOFIR_THREADS_PER_SM overrides.
+__host__ __device__ constexpr int nofir_threads_per_sm(int logn) {
+#ifdef DBP_NOFIR_THREADS_PER_SM
+  return DBP_NOFIR_THREADS_PER_SM + 0 * logn;
+#else
+  return logn == 11 ? 1024 : threads_per_sm(logn);
+#endif
+}
+enum KernelProg : int { kProgGeneric = 0, kProgFFE = 1, kProgNoFir = 2 };
 // Block input through the TMA bulk-copy engine into the exchange planes
 // (Geo::TMA_LOAD): the loads bypass the L1 data path, so the kernel no
 // longer depends on the L1 share of the unified array (carve-out 86%: LDG
@@ -146,6 +160,8 @@ struct Geo {
   // the FFE-only instantiation (no rotation, fewer live registers)
   static constexpr int FFE_MIN_CTAS =
       ffe_threads_per_sm(LOGN) / THREADS > 0 ? ffe_threads_per_sm(LOGN) / THREADS : 1;
+  static constexpr int NOFIR_MIN_CTAS =
+      nofir_threads_per_sm(LOGN) / THREADS > 0 ? nofir_threads_per_sm(LOGN) / THREADS : 1;
   // two exchange regions per slice while MIN_CTAS CTAs still fit the SM's
   // 228 KB (N = 128, 512 .. 2048): one CTA barrier per exchange instead of two
   static constexpr bool DB =
@@ -889,7 +905,8 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
   store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
 }
 
-template <int LOGN, int MODE>
+// NOFIR: compiled for programs without an intensity FIR (SSFM, ESSFM N_c = 0)
+template <int LOGN, int MODE, bool NOFIR = false>
 __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, const KernelParams& kp,
                                        int step_idx, int t, int pol, const float* __restrict__ cptr) {
   // per-item coefficient sets (training batches) read from global memory
@@ -908,7 +925,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
     const float other = __shfl_xor_sync(0xffffffffu, pol ? lo : hi, 16);
     inten[m] = (pol ? hi : lo) + other;
   }
-  if (kp.nc == 0) {
+  if (NOFIR || kp.nc == 0) {
     // F = c0 I: each lane of the pair evaluates half the factors, then swaps
     float2 fac[8];
     if (kp.precise_sincos) {
@@ -992,7 +1009,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
 // the kernel
 // ---------------------------------------------------------------------------
 // One CTA-sized group of blocks (block slices) through the whole program.
-template <int LOGN, int MODE, bool FFE_ONLY>
+template <int LOGN, int MODE, int PROG>
 __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, MODE>& sh, long long grp,
                                               long long n_groups, int t, int slice, int pol) {
   using G = Geo<LOGN>;
@@ -1082,7 +1099,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   }
 
   // operator program (dbp.py:212-233), decoded on the host (KernelParams)
-  if constexpr (FFE_ONLY) {
+  if constexpr (PROG == kProgFFE) {
     // linear-only program (dbp.py:185-191): one convolution with H.  Its
     // exchange needs no write-after-read barrier when the CTA has not read
     // shared memory before (one group per CTA, input by LDG, plain
@@ -1104,7 +1121,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     if (is_conv) {
       conv_block<LOGN>(v, sh, tab, kp.twiddle, t);
     } else {
-      rotate<LOGN>(v, sh, kp, sidx, t, pol, cptr);
+      rotate<LOGN, MODE, PROG == kProgNoFir>(v, sh, kp, sidx, t, pol, cptr);
     }
   }
   }
@@ -1127,9 +1144,12 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   }
 }
 
-// FFE_ONLY: the single-convolution (FFE) program, launched for kFFE
-template <int LOGN, bool FFE_ONLY = false>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS, FFE_ONLY ? Geo<LOGN>::FFE_MIN_CTAS : Geo<LOGN>::MIN_CTAS)
+// PROG: kProgGeneric (any operator program), kProgFFE (the single-convolution
+// FFE program), kProgNoFir (split-step programs without an intensity FIR)
+template <int LOGN, int PROG = kProgGeneric>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, PROG == kProgFFE     ? Geo<LOGN>::FFE_MIN_CTAS
+                                                      : PROG == kProgNoFir ? Geo<LOGN>::NOFIR_MIN_CTAS
+                                                                           : Geo<LOGN>::MIN_CTAS)
 dbp_block_kernel(const KernelParams kp) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
@@ -1158,9 +1178,9 @@ dbp_block_kernel(const KernelParams kp) {
   const long long n_groups = (kp.total_blocks + G::BPC - 1) / G::BPC;
   if constexpr (LOGN >= DBP_PERSIST_MIN_LOGN) {
     for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x)
-      process_group<LOGN, MODE, FFE_ONLY>(kp, sh, grp, n_groups, t, slice, pol);
+      process_group<LOGN, MODE, PROG>(kp, sh, grp, n_groups, t, slice, pol);
   } else {
-    process_group<LOGN, MODE, FFE_ONLY>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
+    process_group<LOGN, MODE, PROG>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
   }
 }
 

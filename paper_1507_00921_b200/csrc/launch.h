@@ -60,12 +60,22 @@ LaunchShape launch_shape();
 // The fused block kernel for one block length: the FFE-only instantiation for
 // the linear program (N >= 2^DBP_FFE_KERNEL_MIN_LOGN), the generic
 // operator-program kernel otherwise.
+// Block lengths whose split-step programs without an intensity FIR (SSFM,
+// ESSFM N_c = 0) run the no-FIR instantiation (profiles/r1/ab_nofir.txt:
+// N = 2048 +2 to +4%, 4096 +1%, 8192 +4.2%; N = 1024 +0.1%, kept generic)
+#ifndef DBP_NOFIR_KERNEL_MIN_LOGN
+#define DBP_NOFIR_KERNEL_MIN_LOGN 11
+#endif
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
-  auto* kernel = dbp_block_kernel<LOGN, false>;
+  auto* kernel = dbp_block_kernel<LOGN, kProgGeneric>;
   if constexpr (LOGN >= DBP_FFE_KERNEL_MIN_LOGN) {
-    if (kp.program == kFFE) kernel = dbp_block_kernel<LOGN, true>;
+    if (kp.program == kFFE) kernel = dbp_block_kernel<LOGN, kProgFFE>;
+  }
+  if constexpr (LOGN >= DBP_NOFIR_KERNEL_MIN_LOGN) {
+    if ((kp.program == kSSFM || kp.program == kESSFM) && kp.nc == 0) kernel = dbp_block_kernel<LOGN, kProgNoFir>;
   }
   cudaError_t e = set_smem_attrs(kernel, smem_bytes);
   if (e != cudaSuccess) return e;

@@ -7,6 +7,9 @@ from paper_1507_00921_b200 import build as B
 ROOT = Path(__file__).resolve().parent.parent / "build" / "variants"
 VARIANTS = {
     "base": [],
+    "nofir": ["-DDBP_NOFIR_KERNEL_MIN_LOGN=10"],
+    "nofir_1024": ["-DDBP_NOFIR_KERNEL_MIN_LOGN=10", "-DDBP_NOFIR_THREADS_PER_SM=1024"],
+    "nofir_896": ["-DDBP_NOFIR_KERNEL_MIN_LOGN=10", "-DDBP_NOFIR_THREADS_PER_SM=896"],
     "ffe10": ["-DDBP_FFE_KERNEL_MIN_LOGN=10"],
     "ffe10_768": ["-DDBP_FFE_KERNEL_MIN_LOGN=10", "-DDBP_FFE_THREADS_PER_SM=768"],
     "ffe10_1024": ["-DDBP_FFE_KERNEL_MIN_LOGN=10", "-DDBP_FFE_THREADS_PER_SM=1024"],
