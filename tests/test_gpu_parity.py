@@ -413,3 +413,27 @@ def test_ffe_kernel_large_blocks_match_oracle(n_blk, m):
         want = dbp_port.backpropagate_arrays(x[i].astype(np.complex128), 56e9, port_config(cfg))
         assert dbp_port.per_block_rel_l2(got[i], want, n_blk, m).max() <= TOL_BLOCK
         np.testing.assert_array_equal(got[i], _run(x[i:i + 1], cfg)[0])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("alg,n_blk,m,steps,arr", [
+    ("ssfm", 2048, 700, 20, "linear-first"), ("ssfm", 2048, 700, 3, "symmetric"),
+    ("essfm0", 2048, 700, 1, "symmetric"), ("ssfm", 4096, 1400, 4, "nonlinear-first"),
+    ("ssfm", 8192, 1024, 20, "linear-first")])
+def test_nofir_kernel_matches_oracle(alg, n_blk, m, steps, arr):
+    # the no-FIR split-step instantiation (launch.h, N >= 2048: SSFM and ESSFM
+    # with N_c = 0): whole-signal framing with edge blocks, ragged length, 2-item
+    # batch; per-block rel-L2 <= 1e-5 against the oracle (dbp.py:193-235) and
+    # batch == single runs
+    gen = np.random.default_rng(n_blk + steps)
+    span = pb.FiberParams(-21.68, 1.3, 0.2, 80.0)
+    coeffs = pb.EssfmCoefficients(np.array([0.9])) if alg == "essfm0" else None
+    cfg = pb.DbpConfig("essfm" if alg == "essfm0" else "ssfm", pb.OverlapPlan(n_blk, m), quiet_link(40, span),
+                       num_steps=steps, coeffs=coeffs, arrangement=arr)
+    n = 4 * (n_blk - m) + 77
+    x = (0.03 * (gen.normal(size=(2, 2, n)) + 1j * gen.normal(size=(2, 2, n)))).astype(np.complex64)
+    got = _run(x, cfg)
+    for i in range(2):
+        want = dbp_port.backpropagate_arrays(x[i].astype(np.complex128), 56e9, port_config(cfg))
+        assert dbp_port.per_block_rel_l2(got[i], want, n_blk, m).max() <= TOL_BLOCK
+        np.testing.assert_array_equal(got[i], _run(x[i:i + 1], cfg)[0])
