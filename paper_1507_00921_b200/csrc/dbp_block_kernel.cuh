@@ -50,15 +50,23 @@ namespace dbp {
 // CTAs hold max(1, 32 / T) blocks, so every block of N >= 512 has its own
 // CTA and its own barrier domain).  Tuned on B200 with the packed-FP32
 // kernel (tools/ab_small_n.sh, profiles/r1/ab_small_n.txt): N <= 256: 512
-// threads/SM; N = 512, 1024: 896 (7 / 14 CTAs, 72 regs; +0.7% over 768,
-// profiles/r1/ab_896.txt); N = 2048: 768 (80 regs); N >= 4096: 1024 (64
-// regs).  -DDBP_THREADS_PER_SM overrides.
+// threads/SM; N = 512: 896 (7 CTAs, 72 regs; profiles/r1/ab_896.txt);
+// N >= 1024: 1024 (64 regs) since the direct-form FIR (DBP_FIR_DIRECT) and
+// the separate generic-FIR instantiation (kProgGenericFir) left the fixed-tap
+// kernel without spills at 64 registers: ESSFM 2048 +3.9%, 1024 +0.4%
+// (profiles/r1/ab_fir_direct.txt; before: 896 / 768 / 1024 at N = 1024 /
+// 2048 / 4096, still used by kProgGenericFir).  -DDBP_THREADS_PER_SM overrides.
 __host__ __device__ constexpr int threads_per_sm(int logn) {
 #ifdef DBP_THREADS_PER_SM
   return DBP_THREADS_PER_SM + 0 * logn;
 #else
-  return logn <= 8 ? 512 : (logn <= 10 ? 896 : (logn == 11 ? 768 : 1024));
+  return logn <= 8 ? 512 : (logn == 9 ? 896 : 1024);
 #endif
+}
+// ... of the generic-FIR instantiation (runtime N_c / per-item coefficient
+// sets: fir8_generic's 24-float tap windows need the pre-v8 register budgets)
+__host__ __device__ constexpr int genfir_threads_per_sm(int logn) {
+  return logn <= 8 ? 512 : (logn <= 10 ? 896 : (logn == 11 ? 768 : 1024));
 }
 // Resident threads per SM of the FFE-only kernel (launch.h selects it for
 // N >= 2^DBP_FFE_KERNEL_MIN_LOGN).  Without the rotation it fits 64 registers,
@@ -85,7 +93,12 @@ __host__ __device__ constexpr int nofir_threads_per_sm(int logn) {
   return logn == 11 ? 1024 : threads_per_sm(logn);
 #endif
 }
-enum KernelProg : int { kProgGeneric = 0, kProgFFE = 1, kProgNoFir = 2 };
+enum KernelProg : int { kProgGeneric = 0, kProgFFE = 1, kProgNoFir = 2, kProgGenericFir = 3 };
+// N_c with a compiled fixed-tap FIR (fir8_fixed); anything else, and per-item
+// coefficient sets, run fir8_generic in the kProgGenericFir instantiation
+__host__ __device__ constexpr bool fixed_fir_nc(int nc) {
+  return nc == 1 || nc == 9 || nc == 17 || nc == 32 || nc == 33;
+}
 // Block input through the TMA bulk-copy engine into the exchange planes
 // (Geo::TMA_LOAD): the loads bypass the L1 data path, so the kernel no
 // longer depends on the L1 share of the unified array (carve-out 86%: LDG
@@ -162,6 +175,8 @@ struct Geo {
       ffe_threads_per_sm(LOGN) / THREADS > 0 ? ffe_threads_per_sm(LOGN) / THREADS : 1;
   static constexpr int NOFIR_MIN_CTAS =
       nofir_threads_per_sm(LOGN) / THREADS > 0 ? nofir_threads_per_sm(LOGN) / THREADS : 1;
+  static constexpr int GENFIR_MIN_CTAS =
+      genfir_threads_per_sm(LOGN) / THREADS > 0 ? genfir_threads_per_sm(LOGN) / THREADS : 1;
   // two exchange regions per slice while MIN_CTAS CTAs still fit the SM's
   // 228 KB (N = 128, 512 .. 2048): one CTA barrier per exchange instead of two
   static constexpr bool DB =
@@ -818,11 +833,43 @@ __device__ __forceinline__ float2 p_fma(float2 a, float2 b, float2 c) {
 // centre and even taps accumulate into output pairs (f[2j], f[2j+1]) and the
 // odd taps into (f[2j-1], f[2j]) (j = 0..4; f[-1], f[8] are discarded), the
 // two halves added at the end: 166 instead of 280 FP instructions at N_c = 17.
-template <int NC>
+#ifndef DBP_FIR_DIRECT
+#define DBP_FIR_DIRECT 1
+#endif
+// DIRECT: the streamed direct form (N >= 1024, where it lets the fixed-tap
+// kernel fit 64 registers); below, the folded symmetric form measured 0.2-1%
+// faster (profiles/r1/ab_v8.txt)
+template <int NC, bool DIRECT>
 __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
                                            int p0, float a, float g, const KernelParams& kp, int n_blk) {
   constexpr int PW = (NC + 3) & ~3;
   constexpr int W = 8 + 2 * PW;
+  if constexpr (DIRECT) {
+  // Direct form streamed over the window: each 4-float piece of the padded
+  // intensity window is folded into the 8 accumulators with the coefficient of
+  // its tap offset (a constant-bank FFMA operand), so only f[8] and one piece
+  // are live -- the same 2 N_c + 1 FP instructions per output as the folded
+  // symmetric form, ~40 fewer registers at N_c = 17.
+  float fd[8];
+#pragma unroll
+  for (int o = 0; o < 8; ++o) fd[o] = 0.f;
+#pragma unroll
+  for (int m = 0; m < W / 4; ++m) {
+    DBP_CHECK(fir_phys(p0 + 4 * m) + 3 < fir_phys(n_blk + 2 * PW) + 4);
+    const float4 q = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
+    const float wq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+#pragma unroll
+      for (int o = 0; o < 8; ++o) {
+        const int d = 4 * m + e - PW - o;   // tap offset of this window sample for output o
+        if (d >= -NC && d <= NC) fd[o] = fmaf(kp.c[d < 0 ? -d : d], wq[e], fd[o]);
+      }
+    }
+  }
+  store_factors8(csbuf, p0, fd, a, g, kp.precise_sincos);
+  return;
+  }
   float w[W];
 #pragma unroll
   for (int m = 0; m < W / 4; ++m) {
@@ -905,8 +952,9 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
   store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
 }
 
-// NOFIR: compiled for programs without an intensity FIR (SSFM, ESSFM N_c = 0)
-template <int LOGN, int MODE, bool NOFIR = false>
+// PROG (KernelProg): kProgNoFir compiles the F = c0 I path only; kProgGeneric
+// the fixed-tap FIRs; kProgGenericFir adds the runtime-N_c fir8_generic
+template <int LOGN, int MODE, int PROG = kProgGenericFir>
 __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, const KernelParams& kp,
                                        int step_idx, int t, int pol, const float* __restrict__ cptr) {
   // per-item coefficient sets (training batches) read from global memory
@@ -925,7 +973,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
     const float other = __shfl_xor_sync(0xffffffffu, pol ? lo : hi, 16);
     inten[m] = (pol ? hi : lo) + other;
   }
-  if (NOFIR || kp.nc == 0) {
+  if (PROG == kProgNoFir || kp.nc == 0) {
     // F = c0 I: each lane of the pair evaluates half the factors, then swaps
     float2 fac[8];
     if (kp.precise_sincos) {
@@ -980,13 +1028,17 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
     }
     sh.after_write();
     const int p0 = 16 * t + 8 * pol;
+    constexpr bool kDirectFir = DBP_FIR_DIRECT && LOGN >= 10;
     switch (kp.coeff_stride ? -1 : kp.nc) {
-      case 1: fir8_fixed<1>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 9: fir8_fixed<9>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 17: fir8_fixed<17>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 32: fir8_fixed<32>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 33: fir8_fixed<33>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      default: fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp, cptr, c0); break;
+      case 1: fir8_fixed<1, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 9: fir8_fixed<9, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 17: fir8_fixed<17, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 32: fir8_fixed<32, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 33: fir8_fixed<33, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      default:
+        if constexpr (PROG == kProgGenericFir) fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp, cptr, c0);
+        else __trap();   // the launcher routes these programs to kProgGenericFir
+        break;
     }
     sh.after_write();
     if constexpr (T >= 16) {
@@ -1121,7 +1173,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     if (is_conv) {
       conv_block<LOGN>(v, sh, tab, kp.twiddle, t);
     } else {
-      rotate<LOGN, MODE, PROG == kProgNoFir>(v, sh, kp, sidx, t, pol, cptr);
+      rotate<LOGN, MODE, PROG>(v, sh, kp, sidx, t, pol, cptr);
     }
   }
   }
@@ -1147,9 +1199,10 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
 // PROG: kProgGeneric (any operator program), kProgFFE (the single-convolution
 // FFE program), kProgNoFir (split-step programs without an intensity FIR)
 template <int LOGN, int PROG = kProgGeneric>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS, PROG == kProgFFE     ? Geo<LOGN>::FFE_MIN_CTAS
-                                                      : PROG == kProgNoFir ? Geo<LOGN>::NOFIR_MIN_CTAS
-                                                                           : Geo<LOGN>::MIN_CTAS)
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, PROG == kProgFFE          ? Geo<LOGN>::FFE_MIN_CTAS
+                                                      : PROG == kProgNoFir      ? Geo<LOGN>::NOFIR_MIN_CTAS
+                                                      : PROG == kProgGenericFir ? Geo<LOGN>::GENFIR_MIN_CTAS
+                                                                                : Geo<LOGN>::MIN_CTAS)
 dbp_block_kernel(const KernelParams kp) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;

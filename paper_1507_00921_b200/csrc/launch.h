@@ -77,6 +77,8 @@ cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, s
   if constexpr (LOGN >= DBP_NOFIR_KERNEL_MIN_LOGN) {
     if ((kp.program == kSSFM || kp.program == kESSFM) && kp.nc == 0) kernel = dbp_block_kernel<LOGN, kProgNoFir>;
   }
+  if (kp.program != kFFE && kp.nc > 0 && (kp.coeff_stride != 0 || !fixed_fir_nc(kp.nc)))
+    kernel = dbp_block_kernel<LOGN, kProgGenericFir>;
   cudaError_t e = set_smem_attrs(kernel, smem_bytes);
   if (e != cudaSuccess) return e;
   const LaunchShape sh = launch_shape<LOGN>();
