@@ -184,11 +184,13 @@ struct Geo {
   // split write-after-read barriers (Shm kShmSplitWar, needs every warp in one
   // slice): measured per block length against __syncthreads
   // (profiles/r1/ab_split_war.txt): N = 256 +1.7%, 4096 +3 to +5%; N = 512
-  // -1.5%, 1024 -0.8%, 2048 -0.3% (ESSFM; FFE +2%), 8192 -17% (32 warps
-  // polling one mbarrier, one CTA per SM) -- on for N = 256 and 4096 only
-  // (DBP_SPLIT_WAR=2: every N >= 256, 0: none)
+  // -1.5%, 1024 -0.8%, 8192 -17% (32 warps polling one mbarrier, one CTA per
+  // SM); N = 2048 -0.3% with the v7 kernel's 3 CTAs per SM but +1.3% (ESSFM) /
+  // +1.7% (FFE) with v8's 4 (profiles/r1/ab_v8_opts.txt) -- on for N = 256,
+  // 2048 and 4096 (DBP_SPLIT_WAR=2: every N >= 256, 0: none)
   static constexpr bool SPLIT_WAR =
-      !DB && T >= 16 && (DBP_SPLIT_WAR == 2 || (DBP_SPLIT_WAR == 1 && (LOGN == 8 || LOGN == 12)));
+      !DB && T >= 16 &&
+      (DBP_SPLIT_WAR == 2 || (DBP_SPLIT_WAR == 1 && (LOGN == 8 || LOGN == 11 || LOGN == 12)));
   // one block per CTA and one group per CTA (no persistent loop): input by TMA
   static constexpr bool TMA_LOAD = DBP_TMA_LOAD && BPC == 1 && LOGN >= 9 && LOGN <= 12;
   // first exchange with 16-byte paired accesses (see fft_fwd)
