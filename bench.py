@@ -12,8 +12,10 @@ the fused block kernel over the whole per-GPU batch.  Multi-GPU: one process
 per GPU (torchrun), each its own 512 waveforms (weak scaling, no data-path
 collective), timed with CUDA events, max over ranks.
 
-Prints ONE JSON line (rank 0).  ``--impl reference`` times the CPU oracle
-port of the reference path on this host's cores instead (rank 0 only).
+Prints ONE JSON line (rank 0).  ``--impl reference`` times the reference's
+own CPU implementation, ``fiberdbp.dbp.backpropagate`` installed unmodified
+in oracle/_ref (oracle/install_ref.sh), on this host's cores instead (rank 0
+only; the oracle port only if oracle/_ref is absent).
 """
 
 from __future__ import annotations
@@ -104,15 +106,18 @@ def work_per_sample(a, gains_not_one: bool = False) -> tuple[float, float]:
 
 
 def kernel_prog(a) -> int:
-    """Which instantiation of the block kernel the launcher picks (csrc/launch.h):
-    0 generic, 1 FFE-only, 2 no-FIR split-step."""
-    if a.block_len < 2048:
-        return 0
-    if a.algorithm == "ffe":
-        return 1
-    if a.algorithm == "ssfm" or a.nc == 0:
-        return 2
-    return 0
+    """Which instantiation of the block kernel the launcher picks (csrc/launch.h
+    launch_block_kernel_impl): 0 generic (fixed-tap FIR), 1 FFE-only, 2 no-FIR
+    split-step, 3 generic FIR (runtime N_c outside {1, 9, 17, 32, 33})."""
+    nc = a.nc if a.algorithm == "essfm" else 0
+    prog = 0
+    if a.block_len >= 2048 and a.algorithm == "ffe":
+        prog = 1
+    if a.block_len >= 2048 and a.algorithm != "ffe" and nc == 0:
+        prog = 2
+    if a.algorithm != "ffe" and nc > 0 and nc not in (1, 9, 17, 32, 33):
+        prog = 3
+    return prog
 
 
 def cpu_model() -> str:
@@ -341,9 +346,9 @@ def run_ours(a) -> int:
         secs, samples = cb.step(waves)
         one_core = cb.one_core_rate()
         cb.close()
-        cpu = {"value": samples / secs / 1e9, "unit": UNIT, "cores": cores, "kind": "port",
-               "sample": f"{waves} waveforms x 2^{a.log2_samples} samples of the same workload, "
-                         f"oracle/dbp_port.py float64 numpy (pocketfft), {cores} single-threaded processes",
+        cpu = {"value": samples / secs / 1e9, "unit": UNIT, "cores": cores, "kind": cb.kind,
+               "sample": f"{waves} waveforms x 2^{a.log2_samples} samples of the same workload through "
+                         + cb.describe(),
                "seconds": secs, "cpu_model": cpu_model(), "one_core_value": one_core / 1e9}
 
     if rank == 0:
@@ -374,7 +379,7 @@ def run_ours(a) -> int:
 
 
 # ---------------------------------------------------------------------------
-# reference arm: the CPU oracle port of the reference path on host cores
+# reference arm: the reference's own CPU DBP (oracle/_ref) on the host cores
 # ---------------------------------------------------------------------------
 
 def run_reference(a) -> int:
@@ -393,6 +398,8 @@ def run_reference(a) -> int:
         s, m = cb.step(cores, seed0=k * cores)
         tot_s += s
         tot_n += m
+    one_core = cb.one_core_rate()
+    kind, desc = cb.kind, cb.describe()
     cb.close()
     value = tot_n / tot_s / 1e9
     line = {
@@ -401,9 +408,10 @@ def run_reference(a) -> int:
         "scaling": "weak", "vs_baseline": None, "dtype": "fp64 (complex128)",
         "data": "synthetic: seeded complex Gaussian dual-pol waveforms at 0 dBm",
         "config": workload_config(a, world), "impl": "reference",
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": f"each step: {cores} waveforms x 2^{a.log2_samples} samples "
-                                   "(one per core) through oracle/dbp_port.py", "cpu_model": cpu_model()},
+                                   f"(one per core) through {desc}", "cpu_model": cpu_model(),
+                         "one_core_value": one_core / 1e9},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -206,6 +206,31 @@ struct Geo {
     for (int q = 0; q < p; ++q) off += q == 0 ? (R0 / 2) * (N / R0) * 2 : 8 * (1 << log_s(q)) * 2;
     return off;
   }
+  // Decimation-in-time base tables (one float2 per entry) behind the k-paired
+  // tables (make_twiddles):
+  //  forward pass p >= 1: W_{R0 16^p}^{K}, R0 16^(p-1) entries, indexed by the
+  //    thread's sub-problem K = t >> log_s(p) -- except the last pass (NP >= 2),
+  //    indexed by t (K = (t >> 4) + (N / 256)(t & 15) after the tile transpose
+  //    for NP >= 3, K = t for NP == 2);
+  //  inverse pass 0: W_N^{-g}, g = t + T q < N / R0; inverse middle pass p:
+  //    W_{16 S_p}^{-ns}, ns = t mod S_p < S_p.
+  __host__ __device__ static constexpr int tw_legacy_size() { return NP > 1 ? tw_offset(NP - 1) : 1; }
+  __host__ __device__ static constexpr int dit_fwd_size(int p) {
+    int s = R0;
+    for (int q = 1; q < p; ++q) s *= 16;
+    return s;
+  }
+  __host__ __device__ static constexpr int dit_fwd_offset(int p) {
+    int off = tw_legacy_size();
+    for (int q = 1; q < p; ++q) off += dit_fwd_size(q);
+    return off;
+  }
+  __host__ __device__ static constexpr int dit_inv_size(int p) { return p == 0 ? N / R0 : (1 << log_s(p)); }
+  __host__ __device__ static constexpr int dit_inv_offset(int p) {
+    int off = dit_fwd_offset(NP);
+    for (int q = 0; q < p; ++q) off += dit_inv_size(q);
+    return off;
+  }
 };
 
 // Twiddle tables, float64 -> float32, k-paired (see Geo::tw_offset):
@@ -264,6 +289,25 @@ inline std::vector<float2> make_twiddles(int logn) {
     }
   }
   if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
+  // decimation-in-time bases (Geo::dit_fwd_offset / dit_inv_offset)
+  if (np > 1) {
+    const long long tt = n / 16;
+    for (int p = 1; p < np; ++p) {
+      const long long period = r0 << (4 * p), size = period / 16;
+      if (p == np - 1) {
+        for (long long t = 0; t < tt; ++t) {
+          const long long k = np >= 3 ? (t >> 4) + (n / 256) * (t & 15) : t;
+          tw.push_back(w(k, period));
+        }
+      } else {
+        for (long long k = 0; k < size; ++k) tw.push_back(w(k, period));
+      }
+    }
+    for (int p = 0; p < np - 1; ++p) {
+      const long long period = p == 0 ? n : n >> (logr0 + 4 * p - 4), size = p == 0 ? n / r0 : period / 16;
+      for (long long k = 0; k < size; ++k) tw.push_back(unit_float2(2.0 * M_PI * (double)k / (double)period));
+    }
+  }
   return tw;
 }
 
@@ -503,6 +547,17 @@ __device__ __forceinline__ void twiddle_powers(float2* u, const float2* col) {
 #ifndef DBP_TW_POWERS
 #define DBP_TW_POWERS 3
 #endif
+// TWP value of the decimation-in-time fused-twiddle FFT (see dit_base)
+constexpr int kTwDit = 4;
+// Programs with at most this many nonlinear steps run the fused-twiddle FFT;
+// longer programs keep the exact-adjoint FFT (DBP_TW_POWERS), whose forward
+// and inverse twiddles are conjugates of the same rounded values, so phase
+// errors cancel within each transform pair instead of accumulating coherently
+// over the steps (SSFM-20 at +5.6 dBm: 1.3e-5 per-block rel-L2 with the fused
+// FFT, tolerance 1e-5).  -DDBP_DIT_MAX_STEPS=0 disables the fused FFT.
+#ifndef DBP_DIT_MAX_STEPS
+#define DBP_DIT_MAX_STEPS 2
+#endif
 
 template <int R, bool CONJ, bool FIRST, int TWP>
 __device__ __forceinline__ void twiddle(float2* u, const float2* col, int row_stride) {
@@ -539,6 +594,18 @@ __device__ __forceinline__ void apply_table_df(float2 (&v)[16], const float2* __
   }
 }
 
+// Decimation-in-time twiddles (TWP != 0, the DBP kernel): the forward passes
+// p >= 1 take their twiddles at the input as powers of one base per thread
+// (W_{R0 16^p}^{K}, K the thread's accumulated sub-problem index) and the
+// inverse passes keep theirs at the input too, so every twiddle multiply
+// fuses into a DFT butterfly (dft_tw, dft_small.cuh): 74 + 30 + 28 -> 112
+// instructions per twiddled radix-16 pass, and the radix-R0 forward pass
+// carries none (v9).  TWP == 0 (the link simulator) keeps the table-twiddle
+// decimation-in-frequency forward, whose magnitude error does not compound.
+__device__ __forceinline__ float2 dit_base(const float2* __restrict__ tw, int off, int idx) {
+  return ldg_table(tw + off + idx);
+}
+
 // ---------------------------------------------------------------------------
 // Block FFT on one polarisation: fft_fwd walks the decimation-in-frequency
 // passes 0 .. NP-1 (register m of thread t holds block position t + T m on
@@ -548,7 +615,7 @@ __device__ __forceinline__ void apply_table_df(float2 (&v)[16], const float2* __
 // ---------------------------------------------------------------------------
 // TWP: which passes build twiddles by powers (DBP_TW_POWERS bits); the link
 // simulator passes 0 (table loads only: powers compound the magnitude error)
-template <int LOGN, int P, int TWP = DBP_TW_POWERS, int MODE = kShmSync, bool CALLER_WAR = false>
+template <int LOGN, int P, int TWP = kTwDit, int MODE = kShmSync, bool CALLER_WAR = false>
 __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
@@ -564,7 +631,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
       dft<R0, false>(u);
-      twiddle<R0, false, true, TWP>(u, tw + 2 * (t + T * q), 2 * S0);
+      if constexpr (TWP != kTwDit) twiddle<R0, false, true, TWP>(u, tw + 2 * (t + T * q), 2 * S0);
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
@@ -616,8 +683,12 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     // region this half-warp alone read in the previous (pad256) exchange;
     // rows of pitch 18 keep the row side 16-byte aligned (8 LDS.128) and
     // both sides conflict free.
-    dft<16, false>(v);
-    twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
+    if constexpr (TWP != kTwDit) {
+      dft<16, false>(v);
+      twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
+    } else {
+      dft_tw<16, false>(v, dit_base(tw, G::dit_fwd_offset(P), t >> G::log_s(P)));
+    }
     float2* tile = sh.template plane<(NP - 2) & 1>() + kTileLen * (t >> 4);
     const int l = t & 15;
     DBP_CHECK(kTileLen * (t >> 4) + kTileLen <= sh.plane_len());
@@ -632,12 +703,17 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
 #pragma unroll
       for (int e = 0; e < 16; ++e) v[e] = tile[kTilePitch * l + e];
     }
-    dft<16, false>(v);  // last pass: group (h, l)
+    if constexpr (TWP != kTwDit) dft<16, false>(v);  // last pass: group (h, l)
+    else dft_tw<16, false>(v, dit_base(tw, G::dit_fwd_offset(NP - 1), t));
   } else if constexpr (P < NP - 1) {
     // middle radix-16 pass: group g = t, ns = t mod S_P
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
-    dft<16, false>(v);
-    twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
+    if constexpr (TWP != kTwDit) {
+      dft<16, false>(v);
+      twiddle<16, false, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
+    } else {
+      dft_tw<16, false>(v, dit_base(tw, G::dit_fwd_offset(P), t >> LS));
+    }
     sh.before_write();
     {
       float2* plane = sh.template plane<(P + 1) & 1>();
@@ -660,11 +736,13 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     if constexpr (P + 1 != NP - 2) sh.reads_done();
     fft_fwd<LOGN, P + 1, TWP>(v, sh, tw, t);
   } else {
-    dft<16, false>(v);  // last pass: S = 1, group g = t, bins t + T e
+    // last pass (NP == 2): S = 1, group g = t, bins t + T e
+    if constexpr (TWP != kTwDit) dft<16, false>(v);
+    else dft_tw<16, false>(v, dit_base(tw, G::dit_fwd_offset(P), t));
   }
 }
 
-template <int LOGN, int P, int TWP = DBP_TW_POWERS, int MODE = kShmSync>
+template <int LOGN, int P, int TWP = kTwDit, int MODE = kShmSync>
 __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tw,
                                         int t) {
   using G = Geo<LOGN>;
@@ -702,8 +780,12 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
       float2 u[R0];
 #pragma unroll
       for (int e = 0; e < R0; ++e) u[e] = v[q + G0 * e];
-      twiddle<R0, true, true, TWP>(u, tw + 2 * (t + T * q), 2 * S0);
-      dft<R0, true>(u);
+      if constexpr (TWP != kTwDit) {
+        twiddle<R0, true, true, TWP>(u, tw + 2 * (t + T * q), 2 * S0);
+        dft<R0, true>(u);
+      } else {
+        dft_tw<R0, true>(u, dit_base(tw, G::dit_inv_offset(0), t + T * q));
+      }
 #pragma unroll
       for (int e = 0; e < R0; ++e) v[q + G0 * e] = u[e];
     }
@@ -723,8 +805,12 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = tile[l + kTilePitch * k];
     sh.reads_done();
-    twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
-    dft<16, true>(v);
+    if constexpr (TWP != kTwDit) {
+      twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & 15), 2 * 16);
+      dft<16, true>(v);
+    } else {
+      dft_tw<16, true>(v, dit_base(tw, G::dit_inv_offset(P), t & 15));
+    }
   } else if constexpr (P < NP - 1) {
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
     fft_inv<LOGN, P + 1, TWP>(v, sh, tw, t);
@@ -742,22 +828,26 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
       for (int m = 0; m < 16; ++m) v[m] = plane[side_index<LOGN, P>(t, m)];
     }
     sh.reads_done();
-    twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
-    dft<16, true>(v);
+    if constexpr (TWP != kTwDit) {
+      twiddle<16, true, false, TWP>(v, tw + G::tw_offset(P) + 2 * (t & (S - 1)), 2 * S);
+      dft<16, true>(v);
+    } else {
+      dft_tw<16, true>(v, dit_base(tw, G::dit_inv_offset(P), t & (S - 1)));
+    }
   } else {
     dft<16, true>(v);  // last pass
   }
 }
 
 // FFT -> x table (bins in register order, 1/N folded in) -> IFFT
-template <int LOGN, int MODE, bool CALLER_WAR = false>
+template <int LOGN, int MODE, bool CALLER_WAR = false, int TWP = kTwDit>
 __device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tab,
                                            const float2* __restrict__ tw, int t) {
-  fft_fwd<LOGN, 0, DBP_TW_POWERS, MODE, CALLER_WAR>(v, sh, tw, t);
+  fft_fwd<LOGN, 0, TWP, MODE, CALLER_WAR>(v, sh, tw, t);
   apply_table<LOGN>(v, tab, Geo<LOGN>::NP == 1 ? 0 : t);
   // value barrier: the inverse recomputes its indices instead of holding the
   // forward ones (and reloading twiddles) across the last pass
-  fft_inv<LOGN, 0>(v, sh, tw, opaque(t));
+  fft_inv<LOGN, 0, TWP>(v, sh, tw, opaque(t));
 }
 
 // ---------------------------------------------------------------------------
@@ -771,7 +861,7 @@ __device__ __forceinline__ void conv_block(float2 (&v)[16], Shm<LOGN, MODE>& sh,
 // SFU's __sincosf, whose smooth argument-correlated absolute error (up to
 // 2^-21.4) accumulates coherently over many SSFM steps -- the host picks the
 // precise form for programs with >= 3 nonlinear steps.
-template <bool PRECISE>
+template <bool PRECISE, bool GAIN = true>
 __device__ __forceinline__ float2 rot_factor(float a, float g, float f) {
   const float th = a * f;
   float s, c;
@@ -797,7 +887,8 @@ __device__ __forceinline__ float2 rot_factor(float a, float g, float f) {
     r = fmaf(k, 1.74845553e-7f, r);
     __sincosf(r, &s, &c);
   }
-  return make_float2(c * g, s * g);
+  if constexpr (GAIN) return make_float2(c * g, s * g);
+  else return make_float2(c, s);   // g == 1: c * 1 == c, bit-identical
 }
 
 // 8 filtered intensities -> rotation factors -> (cos, sin) buffer
@@ -815,6 +906,40 @@ __device__ __forceinline__ void store_factors8(float2* __restrict__ csbuf, int p
                                                float a, float g, bool precise) {
   if (precise) store_factors8<true>(csbuf, p0, f, a, g);
   else store_factors8<false>(csbuf, p0, f, a, g);
+}
+
+// What the FIR lanes publish for the rotation (DBP_NL_PUBLISH_F):
+//  1 (default): the filtered intensity F itself, 4 bytes per position at
+//    fir_phys(p) -- each lane then evaluates the (cos, sin) of its own 16
+//    positions (twice the SFU work, which has room) and the shared-memory
+//    traffic of the factor exchange halves: 2 STS.128 + 16 LDS.32 (24
+//    wavefronts per warp) instead of 4 STS.128 + 16 LDS.64 (48);
+//  0: the rotation factors (cos, sin) g, 8 bytes per position at cs_phys(p).
+#ifndef DBP_NL_PUBLISH_F
+#define DBP_NL_PUBLISH_F 1
+#endif
+__device__ __forceinline__ void publish8(float* __restrict__ nlbuf, int p0, const float (&f)[8], float a, float g,
+                                         bool precise) {
+#if DBP_NL_PUBLISH_F
+  // p0 = 16 t + 8 pol: both float4 stay inside one 16-float pad group
+  float* dst = nlbuf + fir_phys(p0);
+  *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
+  *reinterpret_cast<float4*>(dst + 4) = make_float4(f[4], f[5], f[6], f[7]);
+#else
+  store_factors8(reinterpret_cast<float2*>(nlbuf), p0, f, a, g, precise);
+#endif
+}
+
+// v[m] *= (cos, sin)(a F_m) g for the 16 published F of this lane's positions
+template <bool PRECISE>
+__device__ __forceinline__ void rotate_by_f(float2 (&v)[16], const float (&fv)[16], float a, float g) {
+  if (g == 1.0f) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], rot_factor<PRECISE, false>(a, g, fv[m]));
+  } else {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], rot_factor<PRECISE, true>(a, g, fv[m]));
+  }
 }
 
 #ifndef DBP_FIR_PACKED
@@ -842,7 +967,7 @@ __device__ __forceinline__ float2 p_fma(float2 a, float2 b, float2 c) {
 // kernel fit 64 registers); below, the folded symmetric form measured 0.2-1%
 // faster (profiles/r1/ab_v8.txt)
 template <int NC, bool DIRECT>
-__device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
+__device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float* __restrict__ nlbuf,
                                            int p0, float a, float g, const KernelParams& kp, int n_blk) {
   constexpr int PW = (NC + 3) & ~3;
   constexpr int W = 8 + 2 * PW;
@@ -869,7 +994,7 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
       }
     }
   }
-  store_factors8(csbuf, p0, fd, a, g, kp.precise_sincos);
+  publish8(nlbuf, p0, fd, a, g, kp.precise_sincos);
   return;
   }
   float w[W];
@@ -916,12 +1041,12 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
     f[o] = acc;
   }
 #endif
-  store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
+  publish8(nlbuf, p0, f, a, g, kp.precise_sincos);
 }
 
 // any nc (and per-item coefficient sets): taps in chunks of four, scalar
 // (summation order differs from the packed fir8_fixed at the last ulp)
-__device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float2* __restrict__ csbuf,
+__device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float* __restrict__ nlbuf,
                                              int p0, int pw, float a, float g, const KernelParams& kp,
                                              const float* __restrict__ cptr, float c0) {
   float f[8];
@@ -951,7 +1076,7 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
       for (int o = 0; o < 8; ++o) f[o] = fmaf(ci, l[o + 3 - d] + r[o + 1 + d], f[o]);
     }
   }
-  store_factors8(csbuf, p0, f, a, g, kp.precise_sincos);
+  publish8(nlbuf, p0, f, a, g, kp.precise_sincos);
 }
 
 // PROG (KernelProg): kProgNoFir compiles the F = c0 I path only; kProgGeneric
@@ -998,8 +1123,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
     // intensity buffer (logical [-pw, N + pw)) and (cos, sin) buffer: regions
     // 1 and 0 when double-buffered, else the second behind the first
     float* ibuf = sh.template region<1>();
-    float2* csbuf = Shm<LOGN, MODE>::DB ? reinterpret_cast<float2*>(sh.template region<0>())
-                       : reinterpret_cast<float2*>(ibuf + fir_phys(N + 2 * pw) + 4);
+    float* nlbuf = Shm<LOGN, MODE>::DB ? sh.template region<0>() : ibuf + fir_phys(N + 2 * pw) + 4;
     // each lane stores its half of the intensities
     sh.before_write();
     const int m0 = 8 * pol;
@@ -1032,17 +1156,32 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
     const int p0 = 16 * t + 8 * pol;
     constexpr bool kDirectFir = DBP_FIR_DIRECT && LOGN >= 10;
     switch (kp.coeff_stride ? -1 : kp.nc) {
-      case 1: fir8_fixed<1, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 9: fir8_fixed<9, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 17: fir8_fixed<17, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 32: fir8_fixed<32, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
-      case 33: fir8_fixed<33, kDirectFir>(ibuf, csbuf, p0, sg.x, sg.y, kp, N); break;
+      case 1: fir8_fixed<1, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
+      case 9: fir8_fixed<9, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
+      case 17: fir8_fixed<17, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
+      case 32: fir8_fixed<32, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
+      case 33: fir8_fixed<33, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
       default:
-        if constexpr (PROG == kProgGenericFir) fir8_generic(ibuf, csbuf, p0, pw, sg.x, sg.y, kp, cptr, c0);
+        if constexpr (PROG == kProgGenericFir) fir8_generic(ibuf, nlbuf, p0, pw, sg.x, sg.y, kp, cptr, c0);
         else __trap();   // the launcher routes these programs to kProgGenericFir
         break;
     }
     sh.after_write();
+#if DBP_NL_PUBLISH_F
+    float fv[16];
+    if constexpr (T >= 16) {
+      const float* fb = nlbuf + fir_phys(t);  // fir_phys(m T + t) = m (5T/4) + fir_phys(t)
+#pragma unroll
+      for (int m = 0; m < 16; ++m) fv[m] = fb[m * (5 * T / 4)];
+    } else {
+#pragma unroll
+      for (int m = 0; m < 16; ++m) fv[m] = nlbuf[fir_phys(m * T + t)];
+    }
+    sh.reads_done();
+    if (kp.precise_sincos) rotate_by_f<true>(v, fv, sg.x, sg.y);
+    else rotate_by_f<false>(v, fv, sg.x, sg.y);
+#else
+    const float2* csbuf = reinterpret_cast<const float2*>(nlbuf);
     if constexpr (T >= 16) {
       const float2* cb = csbuf + cs_phys(t);  // cs_phys(m T + t) = m (9T/8) + cs_phys(t)
       float2 cs[16];
@@ -1056,6 +1195,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
       for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], csbuf[cs_phys(m * T + t)]);
       sh.reads_done();
     }
+#endif
   }
 }
 
@@ -1063,7 +1203,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
 // the kernel
 // ---------------------------------------------------------------------------
 // One CTA-sized group of blocks (block slices) through the whole program.
-template <int LOGN, int MODE, int PROG>
+template <int LOGN, int MODE, int PROG, int TWP>
 __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, MODE>& sh, long long grp,
                                               long long n_groups, int t, int slice, int pol) {
   using G = Geo<LOGN>;
@@ -1165,7 +1305,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     // predicate that spills, or a peeled first operator:
     // profiles/r1/ab_fresh_start.txt).
     constexpr bool kFresh = MODE == kShmSync && !G::TMA_LOAD && LOGN < DBP_PERSIST_MIN_LOGN;
-    conv_block<LOGN, MODE, kFresh>(v, sh, kp.tab_full, kp.twiddle, t);
+    conv_block<LOGN, MODE, kFresh, TWP>(v, sh, kp.tab_full, kp.twiddle, t);
   } else {
   const int n_ops = kp.n_ops;
   for (int op = 0; op < n_ops; ++op) {
@@ -1173,7 +1313,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     const float2* tab = kp.half_ends && (op == 0 || op == n_ops - 1) ? kp.tab_half : kp.tab_full;
     const int sidx = op >> kp.sidx_shift;
     if (is_conv) {
-      conv_block<LOGN>(v, sh, tab, kp.twiddle, t);
+      conv_block<LOGN, MODE, false, TWP>(v, sh, tab, kp.twiddle, t);
     } else {
       rotate<LOGN, MODE, PROG>(v, sh, kp, sidx, t, pol, cptr);
     }
@@ -1198,9 +1338,10 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   }
 }
 
-// PROG: kProgGeneric (any operator program), kProgFFE (the single-convolution
-// FFE program), kProgNoFir (split-step programs without an intensity FIR)
-template <int LOGN, int PROG = kProgGeneric>
+// PROG: kProgGeneric (any operator program, fixed-tap FIRs), kProgFFE (the
+// single-convolution FFE program), kProgNoFir (split-step programs without an
+// intensity FIR), kProgGenericFir (runtime N_c and per-item coefficient sets)
+template <int LOGN, int PROG = kProgGeneric, int TWP = kTwDit>
 __global__ void __launch_bounds__(Geo<LOGN>::THREADS, PROG == kProgFFE          ? Geo<LOGN>::FFE_MIN_CTAS
                                                       : PROG == kProgNoFir      ? Geo<LOGN>::NOFIR_MIN_CTAS
                                                       : PROG == kProgGenericFir ? Geo<LOGN>::GENFIR_MIN_CTAS
@@ -1233,9 +1374,9 @@ dbp_block_kernel(const KernelParams kp) {
   const long long n_groups = (kp.total_blocks + G::BPC - 1) / G::BPC;
   if constexpr (LOGN >= DBP_PERSIST_MIN_LOGN) {
     for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x)
-      process_group<LOGN, MODE, PROG>(kp, sh, grp, n_groups, t, slice, pol);
+      process_group<LOGN, MODE, PROG, TWP>(kp, sh, grp, n_groups, t, slice, pol);
   } else {
-    process_group<LOGN, MODE, PROG>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
+    process_group<LOGN, MODE, PROG, TWP>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
   }
 }
 

@@ -325,29 +325,32 @@ int dbp_plan_set_linear(dbp_plan* p, const double* kernel, const double* half_ke
   std::vector<int> bin(p->N);
   for (int t = 0; t < T; ++t)
     for (int e = 0; e < 16; ++e) bin[dbp::tab_index(p->logn, t, e)] = dbp::last_pass_bin(p->logn, t, e);
-  std::vector<float2> h(p->N);
-  for (int j = 0; j < p->N; ++j) {
-    const int k = bin[j];
-    const double re = kernel[2 * k], im = kernel[2 * k + 1];
-    if (!std::isfinite(re) || !std::isfinite(im)) return fail(DBP_EINVAL, "kernel must be finite");
-    h[j] = make_float2((float)(re * inv_n), (float)(im * inv_n));
-  }
-  int rc = upload(&p->d_full, h);
-  if (rc != DBP_OK) return rc;
-  p->have_full = true;
-  if (half_kernel) {
+  // validate and convert both tables before touching the plan, so a failed
+  // call leaves the previous (full, half) pair in place
+  auto convert = [&](const double* src, std::vector<float2>& h) {
+    h.resize(p->N);
     for (int j = 0; j < p->N; ++j) {
       const int k = bin[j];
-      const double re = half_kernel[2 * k], im = half_kernel[2 * k + 1];
-      if (!std::isfinite(re) || !std::isfinite(im)) return fail(DBP_EINVAL, "half kernel must be finite");
+      const double re = src[2 * k], im = src[2 * k + 1];
+      if (!std::isfinite(re) || !std::isfinite(im)) return false;
       h[j] = make_float2((float)(re * inv_n), (float)(im * inv_n));
     }
-    rc = upload(&p->d_half, h);
+    return true;
+  };
+  std::vector<float2> h, hh;
+  if (!convert(kernel, h)) return fail(DBP_EINVAL, "kernel must be finite");
+  if (half_kernel && !convert(half_kernel, hh)) return fail(DBP_EINVAL, "half kernel must be finite");
+  // a failed upload leaves the tables undefined: drop both flags first
+  p->have_full = false;
+  p->have_half = false;
+  int rc = upload(&p->d_full, h);
+  if (rc != DBP_OK) return rc;
+  if (half_kernel) {
+    rc = upload(&p->d_half, hh);
     if (rc != DBP_OK) return rc;
-    p->have_half = true;
-  } else {
-    p->have_half = false;
   }
+  p->have_full = true;
+  p->have_half = half_kernel != nullptr;
   return DBP_OK;
 }
 
@@ -359,49 +362,55 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
     return fail(DBP_EINVAL, "unknown algorithm code " + std::to_string(algorithm));
   if (arrangement < DBP_ARR_SYMMETRIC || arrangement > DBP_ARR_NONLINEAR_FIRST)
     return fail(DBP_EINVAL, "unknown arrangement code " + std::to_string(arrangement));
+  // validate everything into locals; the plan changes only once every check passed
+  float c[dbp::kMaxSideCoeffs + 4] = {};
+  c[0] = 1.0f;
+  int nc = 0;
+  std::vector<float2> st;
+  if (algorithm != DBP_ALG_FFE) {
+    if (num_steps < 1) return fail(DBP_EINVAL, "num_steps must be >= 1");
+    if (!weights || !gains) return fail(DBP_EINVAL, "null weights or gains");
+    if (!std::isfinite(gamma)) return fail(DBP_EINVAL, "gamma must be finite");
+    if (algorithm == DBP_ALG_ESSFM || algorithm == DBP_ALG_ROTATE) {
+      if (!coeffs) return fail(DBP_EINVAL, "essfm requires a coefficient set");
+      if (n_coeffs < 0 || n_coeffs > DBP_MAX_SIDE_COEFFS)
+        return fail(DBP_EINVAL, "n_coeffs must be in [0, " + std::to_string(DBP_MAX_SIDE_COEFFS) + "]");
+      if (p->N <= 2 * n_coeffs) return fail(DBP_EINVAL, "block length too short for the coefficient memory");
+      for (int i = 0; i <= n_coeffs; ++i)
+        if (!std::isfinite(coeffs[i])) return fail(DBP_EINVAL, "coefficients must be finite");
+      nc = n_coeffs;
+      // trailing zero side taps contribute fma(0, s, acc) == acc: drop them (bit-identical)
+      while (nc > 0 && (float)coeffs[nc] == 0.0f) --nc;
+      for (int i = 0; i <= nc; ++i) c[i] = (float)coeffs[i];
+    }
+    st.resize(num_steps);
+    for (int j = 0; j < num_steps; ++j) {
+      if (!std::isfinite(weights[j]) || !std::isfinite(gains[j])) return fail(DBP_EINVAL, "schedule must be finite");
+      // reference rotation exp(-j * gamma * w * F)  ==  exp(+j * a * F), a = -gamma * w
+      st[j] = make_float2((float)(-gamma * weights[j]), (float)gains[j]);
+    }
+  }
   DeviceGuard g(p->device);
+  // from here on a failure leaves the plan without a step program (ESTATE on run)
+  p->have_steps = false;
+  if (algorithm != DBP_ALG_FFE) {
+    if (num_steps > p->steps_cap) {
+      cudaFree(p->d_steps);
+      p->d_steps = nullptr;
+      p->steps_cap = 0;
+      DBP_CUDA(cudaMalloc(&p->d_steps, num_steps * sizeof(float2)), "cudaMalloc(steps)");
+      p->steps_cap = num_steps;
+    }
+    DBP_CUDA(cudaMemcpy(p->d_steps, st.data(), num_steps * sizeof(float2), cudaMemcpyHostToDevice),
+             "cudaMemcpy(steps)");
+    if (!p->d_coeff) DBP_CUDA(cudaMalloc(&p->d_coeff, sizeof(p->c)), "cudaMalloc(coeff)");
+    DBP_CUDA(cudaMemcpy(p->d_coeff, c, sizeof(c), cudaMemcpyHostToDevice), "cudaMemcpy(coeff)");
+  }
   p->program = algorithm;
   p->arrangement = arrangement;
-  std::memset(p->c, 0, sizeof(p->c));
-  p->c[0] = 1.0f;
-  p->nc = 0;
-  if (algorithm == DBP_ALG_FFE) {
-    p->n_steps = 0;
-    p->have_steps = true;
-    return DBP_OK;
-  }
-  if (num_steps < 1) return fail(DBP_EINVAL, "num_steps must be >= 1");
-  if (!weights || !gains) return fail(DBP_EINVAL, "null weights or gains");
-  if (!std::isfinite(gamma)) return fail(DBP_EINVAL, "gamma must be finite");
-  if (algorithm == DBP_ALG_ESSFM || algorithm == DBP_ALG_ROTATE) {
-    if (!coeffs) return fail(DBP_EINVAL, "essfm requires a coefficient set");
-    if (n_coeffs < 0 || n_coeffs > DBP_MAX_SIDE_COEFFS)
-      return fail(DBP_EINVAL, "n_coeffs must be in [0, " + std::to_string(DBP_MAX_SIDE_COEFFS) + "]");
-    if (p->N <= 2 * n_coeffs) return fail(DBP_EINVAL, "block length too short for the coefficient memory");
-    int nc = n_coeffs;
-    for (int i = 0; i <= n_coeffs; ++i)
-      if (!std::isfinite(coeffs[i])) return fail(DBP_EINVAL, "coefficients must be finite");
-    // trailing zero side taps contribute fma(0, s, acc) == acc: drop them (bit-identical)
-    while (nc > 0 && (float)coeffs[nc] == 0.0f) --nc;
-    for (int i = 0; i <= nc; ++i) p->c[i] = (float)coeffs[i];
-    p->nc = nc;
-  }
-  std::vector<float2> st(num_steps);
-  for (int j = 0; j < num_steps; ++j) {
-    if (!std::isfinite(weights[j]) || !std::isfinite(gains[j])) return fail(DBP_EINVAL, "schedule must be finite");
-    // reference rotation exp(-j * gamma * w * F)  ==  exp(+j * a * F), a = -gamma * w
-    st[j] = make_float2((float)(-gamma * weights[j]), (float)gains[j]);
-  }
-  if (num_steps > p->steps_cap) {
-    cudaFree(p->d_steps);
-    p->d_steps = nullptr;
-    DBP_CUDA(cudaMalloc(&p->d_steps, num_steps * sizeof(float2)), "cudaMalloc(steps)");
-    p->steps_cap = num_steps;
-  }
-  DBP_CUDA(cudaMemcpy(p->d_steps, st.data(), num_steps * sizeof(float2), cudaMemcpyHostToDevice), "cudaMemcpy(steps)");
-  if (!p->d_coeff) DBP_CUDA(cudaMalloc(&p->d_coeff, sizeof(p->c)), "cudaMalloc(coeff)");
-  DBP_CUDA(cudaMemcpy(p->d_coeff, p->c, sizeof(p->c), cudaMemcpyHostToDevice), "cudaMemcpy(coeff)");
-  p->n_steps = num_steps;
+  std::memcpy(p->c, c, sizeof(c));
+  p->nc = nc;
+  p->n_steps = algorithm == DBP_ALG_FFE ? 0 : num_steps;
   p->have_steps = true;
   return DBP_OK;
 }
@@ -527,6 +536,16 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
   if (out_hi > n_total) out_hi = n_total;
   const char* src = static_cast<const char*>(h_in);
   char* dst = static_cast<char*>(h_out);
+  // copies that read / write the caller's host buffers may still be queued
+  // when a later call fails: drain both staging streams before returning,
+  // so the caller can free its buffers on any return code
+  struct StreamDrain {
+    dbp_plan* p;
+    ~StreamDrain() {
+      for (int s = 0; s < 2; ++s)
+        if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
+    }
+  } drain{p};
 
   if (item <= slot_budget) {
     // whole items per chunk, cyclic mode, two streams ping-pong

@@ -199,6 +199,116 @@ __device__ __forceinline__ void dft16(float2* v) {
   for (int i = 0; i < 16; ++i) v[i] = x[i];
 }
 
+// ---------------------------------------------------------------------------
+// DFTs with a runtime input twiddle: X_k = sum_e W_R^{e k} b^e v_e for a base b
+// (decimation in time).  Every twiddled radix-2 butterfly p +- w q is fused
+// (3 packed instructions for both outputs instead of a complex multiply plus
+// an add and a subtract), and the powers b^e are never formed: stage 1 uses
+// b^{R/4}, b^{R/2}, stage 2 the rotated bases W_R^{k1} b and their squares.
+// DFT16 with its 15 twiddles: 96 + 16 instructions (the multiply-then-DFT
+// form with twiddles by powers: 74 + 30 + 28).
+// ---------------------------------------------------------------------------
+
+// (p + w q, p - w q) for a runtime w (minus = 2 p - plus, as pm_w16)
+__device__ __forceinline__ void pm_rt(float2 p, float2 q, float2 w, float2& plus, float2& minus) {
+#if DBP_F32X2
+  const unsigned long long in = f2_fma(f2_pack(-q.y, q.x), f2_pack(w.y, w.y), f2_pack(p.x, p.y));
+  plus = f2_unpack(f2_fma(f2_pack(q.x, q.y), f2_pack(w.x, w.x), in));
+  minus = f2_unpack(f2_fma(f2_pack(p.x, p.y), f2_pack(2.0f, 2.0f), f2_pack(-plus.x, -plus.y)));
+#else
+  plus = make_float2(fmaf(w.x, q.x, fmaf(-w.y, q.y, p.x)), fmaf(w.x, q.y, fmaf(w.y, q.x, p.y)));
+  minus = make_float2(fmaf(2.0f, p.x, -plus.x), fmaf(2.0f, p.y, -plus.y));
+#endif
+}
+
+// a * a (FMUL2 + FFMA2, the c_mul form)
+__device__ __forceinline__ float2 c_sq(float2 a) { return c_mul(a, a); }
+
+// a * W_16^M (conjugate constant for INV), compile-time M
+template <bool INV, int M>
+__device__ __forceinline__ float2 c_mul_w16(float2 a) {
+  constexpr int m = M & 15;
+  if constexpr (m == 0) return a;
+  else if constexpr (m == 4) return c_rot90<INV>(a);
+  else if constexpr (m == 8) return make_float2(-a.x, -a.y);
+  else if constexpr (m == 12) return c_rot90<!INV>(a);
+  else return c_mul(a, w16<INV, M>());
+}
+
+// X_k = sum_n W_4^{n k} g^n a_n, k = 0..3 in place (g2 = g^2): 4 fused butterflies
+template <bool INV>
+__device__ __forceinline__ void tw_dft4(float2& a0, float2& a1, float2& a2, float2& a3, float2 g, float2 g2) {
+  float2 e0p, e0m, e1p, e1m;
+  pm_rt(a0, a2, g2, e0p, e0m);
+  pm_rt(a1, a3, g2, e1p, e1m);
+  pm_rt(e0p, e1p, g, a0, a2);
+  pm_rt(e0m, e1m, c_rot90<INV>(g), a1, a3);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft2_tw(float2* v, float2 b) {
+  pm_rt(v[0], v[1], b, v[0], v[1]);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4_tw(float2* v, float2 b) {
+  tw_dft4<INV>(v[0], v[1], v[2], v[3], b, c_sq(b));
+}
+
+// 8 = 2 x 4: n = 4 n1 + n2, k = k1 + 2 k2; stage 1 weights b^{4 n1}, stage 2
+// bases W_8^{k1} b
+template <bool INV>
+__device__ __forceinline__ void dft8_tw(float2* v, float2 b) {
+  const float2 b2 = c_sq(b), b4 = c_sq(b2);
+  float2 y[8];
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) pm_rt(v[n2], v[n2 + 4], b4, y[n2], y[n2 + 4]);   // k1 = 0 | 1
+  tw_dft4<INV>(y[0], y[1], y[2], y[3], b, b2);
+  tw_dft4<INV>(y[4], y[5], y[6], y[7], c_mul_w16<INV, 2>(b), c_rot90<INV>(b2));
+#pragma unroll
+  for (int k2 = 0; k2 < 4; ++k2) {
+    v[2 * k2] = y[k2];
+    v[2 * k2 + 1] = y[4 + k2];
+  }
+}
+
+// 16 = 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2; stage 1 (over n1) base b^4, stage 2
+// (over n2, row k1) base W_16^{k1} b
+template <bool INV>
+__device__ __forceinline__ void dft16_tw(float2* v, float2 b) {
+  const float2 b2 = c_sq(b), b4 = c_sq(b2), b8 = c_sq(b4);
+#pragma unroll
+  for (int n2 = 0; n2 < 4; ++n2) tw_dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2], b4, b8);
+  // v[4 k1 + n2] holds Y[n2][k1]
+  tw_dft4<INV>(v[0], v[1], v[2], v[3], b, b2);
+  tw_dft4<INV>(v[4], v[5], v[6], v[7], c_mul_w16<INV, 1>(b), c_mul_w16<INV, 2>(b2));
+  tw_dft4<INV>(v[8], v[9], v[10], v[11], c_mul_w16<INV, 2>(b), c_rot90<INV>(b2));
+  tw_dft4<INV>(v[12], v[13], v[14], v[15], c_mul_w16<INV, 3>(b), c_mul_w16<INV, 6>(b2));
+  // row k1 holds X[k1 + 4 k2] at v[4 k1 + k2]: transpose the 4 x 4 index map
+  float2 x[16];
+#pragma unroll
+  for (int k1 = 0; k1 < 4; ++k1)
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = v[4 * k1 + k2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = x[i];
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft_tw(float2* v, float2 b) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
+    dft2_tw<INV>(v, b);
+  } else if constexpr (R == 4) {
+    dft4_tw<INV>(v, b);
+  } else if constexpr (R == 8) {
+    dft8_tw<INV>(v, b);
+  } else {
+    static_assert(R == 16, "radix must be 1, 2, 4, 8 or 16");
+    dft16_tw<INV>(v, b);
+  }
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void dft(float2* v) {
   if constexpr (R == 1) {

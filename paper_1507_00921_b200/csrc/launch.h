@@ -67,18 +67,39 @@ LaunchShape launch_shape();
 #define DBP_NOFIR_KERNEL_MIN_LOGN 11
 #endif
 
+// FFT flavour per program (DBP_DIT_MAX_STEPS): the fused-twiddle FFT for the
+// linear program and split-step programs of <= DBP_DIT_MAX_STEPS steps, the
+// exact-adjoint FFT above.  DBP_FFT=dit|adjoint (env) forces one (A/B runs).
+inline bool use_dit_fft(const KernelParams& kp) {
+  static const int forced = [] {
+    const char* v = std::getenv("DBP_FFT");
+    if (!v || !*v) return -1;
+    return (v[0] == 'd') ? 1 : 0;
+  }();
+  if (forced >= 0) return forced == 1;
+  return kp.program == kFFE || kp.n_steps <= DBP_DIT_MAX_STEPS;
+}
+
+template <int LOGN, int TWP>
+auto select_block_kernel(const KernelParams& kp) {
+  auto* kernel = dbp_block_kernel<LOGN, kProgGeneric, TWP>;
+  if constexpr (LOGN >= DBP_FFE_KERNEL_MIN_LOGN) {
+    if (kp.program == kFFE) kernel = dbp_block_kernel<LOGN, kProgFFE, TWP>;
+  }
+  if constexpr (LOGN >= DBP_NOFIR_KERNEL_MIN_LOGN) {
+    if ((kp.program == kSSFM || kp.program == kESSFM) && kp.nc == 0)
+      kernel = dbp_block_kernel<LOGN, kProgNoFir, TWP>;
+  }
+  if (kp.program != kFFE && kp.nc > 0 && (kp.coeff_stride != 0 || !fixed_fir_nc(kp.nc)))
+    kernel = dbp_block_kernel<LOGN, kProgGenericFir, TWP>;
+  return kernel;
+}
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
-  auto* kernel = dbp_block_kernel<LOGN, kProgGeneric>;
-  if constexpr (LOGN >= DBP_FFE_KERNEL_MIN_LOGN) {
-    if (kp.program == kFFE) kernel = dbp_block_kernel<LOGN, kProgFFE>;
-  }
-  if constexpr (LOGN >= DBP_NOFIR_KERNEL_MIN_LOGN) {
-    if ((kp.program == kSSFM || kp.program == kESSFM) && kp.nc == 0) kernel = dbp_block_kernel<LOGN, kProgNoFir>;
-  }
-  if (kp.program != kFFE && kp.nc > 0 && (kp.coeff_stride != 0 || !fixed_fir_nc(kp.nc)))
-    kernel = dbp_block_kernel<LOGN, kProgGenericFir>;
+  auto* kernel = use_dit_fft(kp) ? select_block_kernel<LOGN, kTwDit>(kp)
+                                 : select_block_kernel<LOGN, DBP_TW_POWERS>(kp);
   cudaError_t e = set_smem_attrs(kernel, smem_bytes);
   if (e != cudaSuccess) return e;
   const LaunchShape sh = launch_shape<LOGN>();

@@ -204,3 +204,124 @@ def conv_model2(block: np.ndarray, table: np.ndarray, logn: int, trace=None) -> 
         for m in range(16):
             out[t + T * m] = regs[t, m]
     return out
+
+
+# ---------------------------------------------------------------------------
+# v9 forward FFT: decimation in time (input twiddles, fused into the DFT)
+# ---------------------------------------------------------------------------
+
+def dit_fwd_base_exp(g: Geo2, p: int, t: int) -> tuple[int, int]:
+    """(K, period) of the forward pass-p input twiddle base W_period^K for thread t.
+
+    Pass p >= 1 multiplies its input register e by base^e, base =
+    W_{R0 16^p}^{K_p}, K_p the thread's accumulated sub-problem index: the
+    reader's sub-problem t >> log_s(p) after a CTA exchange, and
+    (t >> 4) + (N / 256) (t & 15) after the half-warp tile transpose into the
+    last pass (NP >= 3)."""
+    period = g.R0 * 16 ** p
+    if g.NP >= 3 and p == g.NP - 1:
+        k = (t >> 4) + (g.N // 256) * (t & 15)
+    else:
+        k = t >> g.log_s(p)
+    return k % period, period
+
+
+def dit_inv_base_exp(g: Geo2, p: int, t: int, q: int = 0) -> tuple[int, int]:
+    """(K, period) of the inverse pass-p input twiddle base W_period^{-K}:
+    pass 0 group q: W_N^{-(t + T q)}; middle pass p: W_{16 S_p}^{-(t mod S_p)}."""
+    if p == 0:
+        return (t + g.T * q) % g.N, g.N
+    s = 1 << g.log_s(p)
+    return t & (s - 1), 16 * s
+
+
+def conv_model_dit(block: np.ndarray, table: np.ndarray, logn: int) -> np.ndarray:
+    """conv_block with the v9 forward (DIT, input twiddles as powers of one base
+    per thread and pass) and the unchanged inverse walk (input twiddles)."""
+    g = Geo2(logn)
+    N, T = g.N, g.T
+    tab = np.array([table[last_pass_bin(g, t, e)] for e in range(16) for t in range(T)])
+    regs = np.zeros((T, 16), dtype=np.complex128)
+    for t in range(T):
+        for m in range(16):
+            regs[t, m] = block[t + T * m]
+    plane = np.full(N + N // 8, np.nan + 0j)
+    pw = np.arange(16)
+
+    def dft(v, inv):
+        return np.fft.ifft(v) * v.size if inv else np.fft.fft(v)
+
+    def w(k, period, sign=-1):
+        return np.exp(sign * 2j * np.pi * k / period)
+
+    def read_base(t, ls1):
+        return ((t >> ls1) << (ls1 + 4)) + (t & ((1 << ls1) - 1))
+
+    def xfwd(p):
+        ls1 = g.log_s(p + 1)
+        plane[:] = np.nan
+        for t in range(T):
+            for m in range(16):
+                plane[side2(g, p, t, m)] = regs[t, m]
+        for t in range(T):
+            for e in range(16):
+                regs[t, e] = plane[xchg2(g, p, read_base(t, ls1) + (e << ls1))]
+
+    def xinv(p):
+        ls1 = g.log_s(p + 1)
+        plane[:] = np.nan
+        for t in range(T):
+            for e in range(16):
+                plane[xchg2(g, p, read_base(t, ls1) + (e << ls1))] = regs[t, e]
+        for t in range(T):
+            for m in range(16):
+                regs[t, m] = plane[side2(g, p, t, m)]
+
+    def tile(forward):
+        for h in range(T // 16):
+            blk = regs[16 * h:16 * h + 16].copy()
+            regs[16 * h:16 * h + 16] = blk.T
+
+    def fwd_dit(p):
+        for t in range(T):
+            k, period = dit_fwd_base_exp(g, p, t)
+            regs[t] = dft(regs[t] * w(k, period) ** pw, False)
+
+    def inv_dit(p):
+        for t in range(T):
+            k, period = dit_inv_base_exp(g, p, t)
+            regs[t] = dft(regs[t] * w(k, period, +1) ** pw, True)
+
+    if g.NP == 1:
+        for t in range(T):
+            regs[t] = dft(dft(regs[t], False) * tab[:16], True)
+    else:
+        for t in range(T):
+            for q in range(g.G0):
+                idx = [q + g.G0 * e for e in range(g.R0)]
+                regs[t, idx] = dft(regs[t, idx], False)
+        for p in range(1, g.NP):
+            if g.NP >= 3 and p == g.NP - 1:
+                tile(True)
+            else:
+                xfwd(p - 1)
+            fwd_dit(p)
+        for t in range(T):
+            regs[t] = dft(regs[t] * tab[t + T * pw], True)    # x table, last inverse pass (no twiddle)
+        for p in range(g.NP - 2, 0, -1):
+            if g.NP >= 3 and p == g.NP - 2:
+                tile(False)
+            else:
+                xinv(p)
+            inv_dit(p)
+        xinv(0) if not (g.NP >= 3 and g.NP - 2 == 0) else None
+        for t in range(T):
+            for q in range(g.G0):
+                idx = [q + g.G0 * e for e in range(g.R0)]
+                k, period = dit_inv_base_exp(g, 0, t, q)
+                regs[t, idx] = dft(regs[t, idx] * w(k, period, +1) ** np.arange(g.R0), True)
+    out = np.zeros(N, dtype=np.complex128)
+    for t in range(T):
+        for m in range(16):
+            out[t + T * m] = regs[t, m]
+    return out

@@ -113,3 +113,51 @@ def test_x01_paired_closed_forms_and_banks():
             assert len({((2 * t + TILE_LEN * (m // 2)) // 2) % 8 for t in range(t0, t0 + 8)}) == 8
         for e in range(8):
             assert len({((TILE_LEN * (t >> 4) + 2 * (t & 15) + 32 * e) // 2) % 8 for t in range(t0, t0 + 8)}) == 8
+
+
+# ---- v9: decimation-in-time forward with fused input twiddles ----
+
+from .layout_model import conv_model_dit, dit_fwd_base_exp, dit_inv_base_exp  # noqa: E402
+
+
+@pytest.mark.parametrize("logn", list(range(4, 14)))
+def test_dit_conv_model_equals_fft_filter(logn):
+    # the v9 forward (input twiddles W_{R0 16^p}^{K_p} as powers of one base per
+    # thread and pass) and the inverse walk give ifft(fft(x) * h) with the
+    # unchanged digit-reversed table order (last_pass_bin)
+    n = 1 << logn
+    if n > 4096:
+        pytest.skip("pure-python model too slow above 4096")
+    rng = np.random.default_rng(300 + logn)
+    x = rng.normal(size=n) + 1j * rng.normal(size=n)
+    h = np.exp(1j * rng.uniform(-np.pi, np.pi, n))
+    got = conv_model_dit(x, h / n, logn)
+    want = np.fft.ifft(np.fft.fft(x) * h)
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-11 * np.max(np.abs(want)))
+
+
+def dit_table_sizes(g):
+    """Entries of the kernel's DIT base tables (Geo::dit_fwd_size / dit_inv_size)."""
+    fwd = [g.R0 * 16 ** (p - 1) for p in range(1, g.NP)]
+    inv = [g.N // g.R0 if p == 0 else (1 << g.log_s(p)) for p in range(g.NP - 1)]
+    return fwd, inv
+
+
+@pytest.mark.parametrize("logn", list(range(5, 14)))
+def test_dit_base_indices_fit_their_tables(logn):
+    # every thread's base index lies inside its pass's table (forward: by
+    # sub-problem K, the last pass by thread t; inverse: by g = t + T q or ns)
+    g = Geo2(logn)
+    fwd, inv = dit_table_sizes(g)
+    for p in range(1, g.NP):
+        for t in range(g.T):
+            k, period = dit_fwd_base_exp(g, p, t)
+            idx = t if p == g.NP - 1 else t >> g.log_s(p)
+            assert idx < fwd[p - 1] and k < period and period == g.R0 * 16 ** p
+            if p < g.NP - 1:
+                assert k == idx
+    for p in range(g.NP - 1):
+        for t in range(g.T):
+            for q in range(g.G0 if p == 0 else 1):
+                k, period = dit_inv_base_exp(g, p, t, q)
+                assert (t + g.T * q if p == 0 else t & ((1 << g.log_s(p)) - 1)) < inv[p]

@@ -54,6 +54,10 @@ VARIANTS = {
     "pw3_1024": ["-DDBP_TW_POWERS=3", "-DDBP_THREADS_PER_SM=1024"],
     "pw3_512": ["-DDBP_TW_POWERS=3", "-DDBP_THREADS_PER_SM=512"],
     "pw3_cta256": ["-DDBP_TW_POWERS=3", "-DDBP_CTA_POSITIONS=256"],
+    # round 2
+    "pubf0": ["-DDBP_NL_PUBLISH_F=0"],
+    "nodit": ["-DDBP_DIT_MAX_STEPS=0"],
+    "dit4": ["-DDBP_DIT_MAX_STEPS=4"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
