@@ -34,11 +34,17 @@ extern "C" {
 #define DBP_ESTATE (-4)   /* plan not configured (set_linear/set_steps) */
 
 /* algorithms: dbp.py:25 ALGORITHMS = ("ffe", "ssfm", "essfm"); 3 = rotation
- * only (the nonlinear sub-step alone, dbp.py:49 / channel.py:61)           */
+ * only (the nonlinear sub-step alone, dbp.py:49 / channel.py:61); 4 = no
+ * operator at all: the overlap-save framing alone, i.e. overlap_save_run
+ * with the identity block processor (spectral.py:87-145, the reference's
+ * `lambda b: b` in test_spectral.py:72-76 and 119-125).  An FFE program whose
+ * kernel is any caller-supplied filter H is the block processor
+ * `ifft(fft(b) * H)` (test_spectral.py:78-97).                              */
 #define DBP_ALG_FFE 0
 #define DBP_ALG_SSFM 1
 #define DBP_ALG_ESSFM 2
 #define DBP_ALG_ROTATE 3
+#define DBP_ALG_IDENTITY 4
 
 /* arrangements: dbp.py:32 ARRANGEMENTS                                      */
 #define DBP_ARR_SYMMETRIC 0

@@ -34,6 +34,10 @@ from .backprop import (
     nonlinear_substep_ssfm,
     overlap_save_run,
     block_processor,
+    identity_processor,
+    filter_processor,
+    BlockProcessor,
+    GpuBlockProcessor,
 )
 from .spectral import fft, ifft
 
@@ -76,7 +80,8 @@ __all__ = [
     "nonlinear_substep_ssfm", "TrainConfig", "TrainResult", "load_coefficients", "mse",
     "optimize_coefficients", "save_coefficients", "SsfmStepConfig", "amplify_with_ase",
     "apply_jones_matrix", "haar_random_unitary", "propagate_link", "propagate_link_batch", "propagate_span",
-    "random_polarization_rotation", "apply_laser_phase_noise", "linear_substep", "overlap_save_run", "block_processor", "fft", "ifft", "AlignmentError", "FrequencyOffsetError", "RxMetrics", "butterfly_equalize",
+    "random_polarization_rotation", "apply_laser_phase_noise", "linear_substep", "overlap_save_run", "block_processor",
+    "identity_processor", "filter_processor", "BlockProcessor", "GpuBlockProcessor", "fft", "ifft", "AlignmentError", "FrequencyOffsetError", "RxMetrics", "butterfly_equalize",
     "butterfly_equalize_batch", "carrier_recover", "carrier_recover_batch", "evm_percent", "measure_ber",
     "qpsk_decide", "qpsk_map", "receive_batch", "__version__",
 ]

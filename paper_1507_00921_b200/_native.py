@@ -16,7 +16,7 @@ import numpy as np
 LIB_PATH = Path(os.environ.get("DBP_LIB") or Path(__file__).resolve().parent / "libdbp_b200.so")
 
 DBP_OK, DBP_EINVAL, DBP_ECUDA, DBP_ENOMEM, DBP_ESTATE = 0, -1, -2, -3, -4
-ALG_CODES = {"ffe": 0, "ssfm": 1, "essfm": 2, "rotate": 3}
+ALG_CODES = {"ffe": 0, "ssfm": 1, "essfm": 2, "rotate": 3, "identity": 4}
 ARR_CODES = {"symmetric": 0, "linear-first": 1, "nonlinear-first": 2}
 MIN_BLOCK_LEN, MAX_BLOCK_LEN, MAX_SIDE_COEFFS = 16, 8192, 64
 

@@ -323,25 +323,55 @@ def nonlinear_substep_ssfm(block, gamma: float, dz_eff: float, *, device: int = 
     return _rotate_blocks(block, gamma, dz_eff, np.array([1.0]), device)
 
 
-BlockProcessor = "GpuBlockProcessor"   # spectral.py:84: the operator type overlap_save_run accepts
+class ProgramEngine:
+    """A block operator that is not a DBP configuration: the identity (framing
+    only, ``DBP_ALG_IDENTITY``) or a caller-supplied frequency-domain filter
+    ``ifft(fft(b) * H)`` (an FFE program with table H), on one device."""
+
+    def __init__(self, plan: OverlapPlan, sample_rate: float, device: int = 0, kernel=None):
+        self.plan = plan
+        self.sample_rate = float(sample_rate)
+        self.device = int(device)
+        n = plan.block_len
+        if not (_native.MIN_BLOCK_LEN <= n <= _native.MAX_BLOCK_LEN):
+            raise ValueError(f"block_len {n} outside the GPU-supported range "
+                             f"[{_native.MIN_BLOCK_LEN}, {_native.MAX_BLOCK_LEN}]")
+        self.native = _native.NativePlan(self.device, n, plan.overlap)
+        if kernel is None:
+            self.native.set_steps("identity", "symmetric", [0.0], [1.0], 0.0)
+        else:
+            h = np.asarray(kernel, dtype=np.complex128)
+            if h.shape != (n,):
+                raise ValueError(f"filter must have shape ({n},), got {h.shape}")
+            self.native.set_linear(h, None)
+            self.native.set_steps("ffe", "symmetric", [0.0], [1.0], 0.0)
+
+    def num_blocks(self, n_total: int) -> int:
+        return self.plan.num_blocks(n_total)
+
+    run_host = DbpEngine.run_host
+
+    def close(self):
+        self.native.close()
 
 
 class GpuBlockProcessor:
     """The per-block operator of ``backpropagate`` (the closure ``process`` of
-    dbp.py:212-233) as a GPU object: callable on one (2, N) block or an
+    dbp.py:212-233) -- or the identity / a linear filter (``identity_processor``,
+    ``filter_processor``) -- as a GPU object: callable on one (2, N) block or an
     (nb, 2, N) stack (``dbp_process_blocks``), and recognised by
     ``overlap_save_run``, which then frames and processes the whole signal in
     the fused kernel."""
 
-    def __init__(self, cfg: DbpConfig, sample_rate: float, device: int = 0):
+    def __init__(self, cfg: DbpConfig | None, sample_rate: float, device: int = 0, *, engine=None):
         self.cfg = cfg
         self.sample_rate = float(sample_rate)
         self.device = int(device)
-        self.engine = get_engine(cfg, sample_rate, device)
+        self.engine = engine if engine is not None else get_engine(cfg, sample_rate, device)
 
     @property
     def plan(self):
-        return self.cfg.plan
+        return self.cfg.plan if self.cfg is not None else self.engine.plan
 
     def __call__(self, block):
         import torch
@@ -349,7 +379,7 @@ class GpuBlockProcessor:
         b = np.asarray(block)
         single = b.ndim == 2
         blocks = np.ascontiguousarray((b[None] if single else b).astype(np.complex64))
-        n = self.cfg.plan.block_len
+        n = self.plan.block_len
         if blocks.ndim != 3 or blocks.shape[1:] != (2, n):
             raise ValueError(f"expected (2, {n}) blocks")
         dev = torch.device("cuda", self.device)
@@ -363,9 +393,25 @@ class GpuBlockProcessor:
         return out[0] if single else out
 
 
+BlockProcessor = GpuBlockProcessor   # spectral.py:84: the operator type overlap_save_run accepts
+
+
 def block_processor(cfg: DbpConfig, sample_rate: float, *, device: int = 0) -> GpuBlockProcessor:
     """The GPU block operator of ``cfg`` (dbp.py:193-233) for ``overlap_save_run``."""
     return GpuBlockProcessor(cfg, sample_rate, device)
+
+
+def identity_processor(plan: OverlapPlan, sample_rate: float, *, device: int = 0) -> GpuBlockProcessor:
+    """The identity block operator (the reference tests' ``lambda b: b``,
+    test_spectral.py:72-76, 119-125): ``overlap_save_run`` then exercises the
+    framing alone -- cyclic extension, keep the centre, trim -- bit-exactly."""
+    return GpuBlockProcessor(None, sample_rate, device, engine=ProgramEngine(plan, sample_rate, device))
+
+
+def filter_processor(plan: OverlapPlan, kernel, sample_rate: float, *, device: int = 0) -> GpuBlockProcessor:
+    """The linear block operator ``ifft(fft(b) * kernel)`` for a caller-supplied
+    length-N frequency response in numpy FFT bin order (test_spectral.py:78-97)."""
+    return GpuBlockProcessor(None, sample_rate, device, engine=ProgramEngine(plan, sample_rate, device, kernel))
 
 
 def overlap_save_run(sig: DualPolSignal, plan, block_processor, jobs: int = 1) -> DualPolSignal:

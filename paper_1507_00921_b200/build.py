@@ -81,9 +81,8 @@ def build(force: bool = False, verbose: bool = False, extra_flags=None, lib: Pat
             list(pool.map(run, jobs))
     objs = [obj_root / (s.stem + ".o") for s in _sources()]
     if force or jobs or _stale(lib_path, objs):
-        cuda_lib = Path(nvcc()).resolve().parent.parent / "lib64"
-        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(lib_path), *map(str, objs),
-               "-L", str(cuda_lib), "-lcufft", "-Xlinker", f"-rpath,{cuda_lib}"]
+        # static cudart and nothing else: no cuFFT / cuBLAS in the product library
+        cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", str(lib_path), *map(str, objs)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")

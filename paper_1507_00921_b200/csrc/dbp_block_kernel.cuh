@@ -124,6 +124,17 @@ __host__ __device__ constexpr bool fixed_fir_nc(int nc) {
 #ifndef DBP_EXPERIMENT_NOWAR
 #define DBP_EXPERIMENT_NOWAR 0
 #endif
+// timing experiments only (WRONG results): no global block loads (registers
+// synthesised from the thread index) / no output stores / no nonlinear step
+#ifndef DBP_EXPERIMENT_NOLOAD
+#define DBP_EXPERIMENT_NOLOAD 0
+#endif
+#ifndef DBP_EXPERIMENT_NOSTORE
+#define DBP_EXPERIMENT_NOSTORE 0
+#endif
+#ifndef DBP_EXPERIMENT_NONL
+#define DBP_EXPERIMENT_NONL 0
+#endif
 #ifndef DBP_CTA_POSITIONS
 #define DBP_CTA_POSITIONS 32
 #endif
@@ -1250,6 +1261,9 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     }
   }
   if (loaded) {
+  } else if (DBP_EXPERIMENT_NOLOAD && active) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = make_float2(1e-3f * (float)(t + m), 1e-3f * (float)(b & 7));
   } else if (active) {
     const float2* pin = kp.in + item * kp.in_item_stride + pol * kp.in_pol_stride;
     if (!kp.cyclic || (s0 >= 0 && s0 + N <= kp.n_total)) {
@@ -1314,13 +1328,14 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     const int sidx = op >> kp.sidx_shift;
     if (is_conv) {
       conv_block<LOGN, MODE, false, TWP>(v, sh, tab, kp.twiddle, t);
+    } else if (DBP_EXPERIMENT_NONL) {
     } else {
       rotate<LOGN, MODE, PROG>(v, sh, kp, sidx, t, pol, cptr);
     }
   }
   }
 
-  if (active) {
+  if (active && !DBP_EXPERIMENT_NOSTORE) {
     float2* pout = kp.out + item * kp.out_item_stride + pol * kp.out_pol_stride;
     const long long ob = b * kp.step - kp.lead - kp.out_origin;  // output index of block sample 0
     // kept samples j in [lead, min(lead + step, lead + n_total - b step))

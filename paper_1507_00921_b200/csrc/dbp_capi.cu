@@ -126,9 +126,9 @@ int upload(float2** dst, const std::vector<float2>& src) {
 int check_ready(const dbp_plan* p) {
   if (!p) return fail(DBP_EINVAL, "null plan");
   if (!p->have_steps) return fail(DBP_ESTATE, "dbp_plan_set_steps has not been called");
-  if (p->program != dbp::kRotateOnly && !p->have_full)
+  if (p->program != dbp::kRotateOnly && p->program != dbp::kIdentity && !p->have_full)
     return fail(DBP_ESTATE, "dbp_plan_set_linear has not been called");
-  if (p->program != dbp::kFFE && p->program != dbp::kRotateOnly &&
+  if (p->program != dbp::kFFE && p->program != dbp::kRotateOnly && p->program != dbp::kIdentity &&
       p->arrangement == dbp::kSymmetric && !p->have_half)
     return fail(DBP_ESTATE, "symmetric arrangement needs the half-step kernel");
   return DBP_OK;
@@ -146,6 +146,9 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
     kp.conv_parity = -1;
   } else if (p->program == dbp::kRotateOnly) {
     kp.n_ops = p->n_steps;
+    kp.conv_parity = -1;
+  } else if (p->program == dbp::kIdentity) {
+    kp.n_ops = 0;             // framing only: load, keep the centre, store
     kp.conv_parity = -1;
   } else {
     kp.n_ops = 2 * p->n_steps + (p->arrangement == dbp::kSymmetric ? 1 : 0);
@@ -237,7 +240,7 @@ extern "C" {
 
 const char* dbp_last_error(void) { return g_last_error.c_str(); }
 
-int dbp_version(void) { return 100; }
+int dbp_version(void) { return 101; }
 
 int64_t dbp_launch_count(void) { return g_launches.load(); }
 
@@ -358,7 +361,7 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
                        const double* weights, const double* gains, double gamma,
                        const double* coeffs, int n_coeffs) {
   if (!p) return fail(DBP_EINVAL, "null plan");
-  if (algorithm < DBP_ALG_FFE || algorithm > DBP_ALG_ROTATE)
+  if (algorithm < DBP_ALG_FFE || algorithm > DBP_ALG_IDENTITY)
     return fail(DBP_EINVAL, "unknown algorithm code " + std::to_string(algorithm));
   if (arrangement < DBP_ARR_SYMMETRIC || arrangement > DBP_ARR_NONLINEAR_FIRST)
     return fail(DBP_EINVAL, "unknown arrangement code " + std::to_string(arrangement));
@@ -367,7 +370,8 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
   c[0] = 1.0f;
   int nc = 0;
   std::vector<float2> st;
-  if (algorithm != DBP_ALG_FFE) {
+  const bool no_steps = algorithm == DBP_ALG_FFE || algorithm == DBP_ALG_IDENTITY;
+  if (!no_steps) {
     if (num_steps < 1) return fail(DBP_EINVAL, "num_steps must be >= 1");
     if (!weights || !gains) return fail(DBP_EINVAL, "null weights or gains");
     if (!std::isfinite(gamma)) return fail(DBP_EINVAL, "gamma must be finite");
@@ -393,7 +397,7 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
   DeviceGuard g(p->device);
   // from here on a failure leaves the plan without a step program (ESTATE on run)
   p->have_steps = false;
-  if (algorithm != DBP_ALG_FFE) {
+  if (!no_steps) {
     if (num_steps > p->steps_cap) {
       cudaFree(p->d_steps);
       p->d_steps = nullptr;
@@ -410,7 +414,7 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
   p->arrangement = arrangement;
   std::memcpy(p->c, c, sizeof(c));
   p->nc = nc;
-  p->n_steps = algorithm == DBP_ALG_FFE ? 0 : num_steps;
+  p->n_steps = no_steps ? 0 : num_steps;
   p->have_steps = true;
   return DBP_OK;
 }

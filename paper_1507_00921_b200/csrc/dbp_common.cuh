@@ -9,7 +9,7 @@ namespace dbp {
 
 constexpr int kMaxSideCoeffs = 64;
 
-enum Program : int { kFFE = 0, kSSFM = 1, kESSFM = 2, kRotateOnly = 3 };
+enum Program : int { kFFE = 0, kSSFM = 1, kESSFM = 2, kRotateOnly = 3, kIdentity = 4 };
 enum Arrangement : int { kSymmetric = 0, kLinearFirst = 1, kNonlinearFirst = 2 };
 
 struct KernelParams {

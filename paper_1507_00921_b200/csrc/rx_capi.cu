@@ -17,7 +17,7 @@
 // kernels; the sliding-window phase estimate, the unwrap prefix scan,
 // decisions and error counting are elementwise / reduction kernels.
 #include <cuda_runtime.h>
-#include <cufft.h>
+#include "fft64.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -40,11 +40,6 @@ using dbp_capi_internal::fail;
   do {                                                                                           \
     cudaError_t e_ = (expr);                                                                     \
     if (e_ != cudaSuccess) return fail(DBP_ECUDA, std::string(what) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
-#define RX_FFT(expr, what)                                                                       \
-  do {                                                                                           \
-    cufftResult r_ = (expr);                                                                     \
-    if (r_ != CUFFT_SUCCESS) return fail(DBP_ECUDA, std::string(what) + ": cufft error " + std::to_string((int)r_)); \
   } while (0)
 
 namespace rx {
@@ -517,7 +512,7 @@ struct dbp_rx {
   long long* cnt = nullptr;    // [B][4]
   int* items = nullptr;        // [B]
   int* turns = nullptr;        // [B][2]
-  std::map<int, cufftHandle> plans;   // batch (number of length-m transforms) -> plan
+  double2* fftbuf = nullptr;   // fft64::scratch_elems(m, 4 B): Stockham / Bluestein scratch
 };
 
 namespace {
@@ -535,28 +530,17 @@ struct Guard {
 
 unsigned blocks(long long n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
-int plan_for(dbp_rx* r, int count, cufftHandle* out) {
-  auto it = r->plans.find(count);
-  if (it != r->plans.end()) {
-    *out = it->second;
-    return DBP_OK;
-  }
-  cufftHandle h;
-  int n = (int)r->m;
-  RX_FFT(cufftPlanMany(&h, 1, &n, nullptr, 1, n, nullptr, 1, n, CUFFT_Z2Z, count), "cufftPlanMany");
-  RX_FFT(cufftSetStream(h, r->stream), "cufftSetStream");
-  r->plans[count] = h;
-  *out = h;
-  return DBP_OK;
-}
+// float64 DFT of `count` rows of length m (fft64.cuh Stockham, no cuFFT):
+// out = F(in) (kForward) or the unnormalised inverse (kInverse), in == out allowed
+constexpr int kForward = 0, kInverse = 1;
 
 int fft(dbp_rx* r, double2* in, double2* out, int count, int dir) {
-  cufftHandle h;
-  int rc = plan_for(r, count, &h);
-  if (rc) return rc;
-  RX_FFT(cufftExecZ2Z(h, reinterpret_cast<cufftDoubleComplex*>(in), reinterpret_cast<cufftDoubleComplex*>(out), dir),
-         "cufftExecZ2Z");
-  RX_LAUNCHED();
+  const size_t bytes = (size_t)count * r->m * sizeof(double2);
+  if (in != out) RX_CUDA(cudaMemcpyAsync(out, in, bytes, cudaMemcpyDeviceToDevice, r->stream), "D2D(fft)");
+  long long launches = 0;
+  if (!fft64::transform_any(out, r->fftbuf, r->m, count, dir == kInverse, false, r->stream, &launches))
+    return fail(DBP_ECUDA, "fft64 transform launch failed");
+  for (long long i = 0; i < launches; ++i) RX_LAUNCHED();
   return DBP_OK;
 }
 
@@ -655,7 +639,7 @@ int carrier_dev(dbp_rx* r, int batch, double rs, bool have_ref, int window, doub
   int rc;
   rx::pow4_kernel<<<blocks(2 * m * batch), 256, 0, st>>>(r->sym, r->work, 2 * m * batch);
   RX_LAUNCHED();
-  if ((rc = fft(r, r->work, r->work, 2 * batch, CUFFT_FORWARD))) return rc;
+  if ((rc = fft(r, r->work, r->work, 2 * batch, kForward))) return rc;
   rx::argmax_kernel<<<batch, 1024, 0, st>>>(r->work, m, 2 * m, m, 0, r->idx, r->red);
   RX_LAUNCHED();
   std::vector<long long> peak(batch);
@@ -692,10 +676,10 @@ int carrier_dev(dbp_rx* r, int batch, double rs, bool have_ref, int window, doub
   RX_CUDA(cudaStreamSynchronize(st), "cudaStreamSynchronize");   // f_off is a host temporary
   if (!have_ref) return DBP_OK;
   // 90-degree ambiguity against the better-correlating reference (modem.py:339-350)
-  if ((rc = fft(r, r->sym, r->work, 2 * batch, CUFFT_FORWARD))) return rc;
+  if ((rc = fft(r, r->sym, r->work, 2 * batch, kForward))) return rc;
   rx::xspec_kernel<<<blocks(4 * m * batch), 256, 0, st>>>(r->work, r->refs, r->corr, m, batch);
   RX_LAUNCHED();
-  if ((rc = fft(r, r->corr, r->corr, 4 * batch, CUFFT_INVERSE))) return rc;
+  if ((rc = fft(r, r->corr, r->corr, 4 * batch, kInverse))) return rc;
   rx::argmax_kernel<<<4 * batch, 1024, 0, st>>>(r->corr, m, m, 0, 1, r->idx, r->red);
   RX_LAUNCHED();
   std::vector<double> pv(8 * batch);
@@ -727,10 +711,10 @@ int count_dev(dbp_rx* r, int batch, long long skip_bits, long long* errors, long
   int rc;
   rx::bits_to_symbols_kernel<<<blocks(2 * m * batch), 256, 0, st>>>(r->bits, r->work, 2 * m * batch);
   RX_LAUNCHED();
-  if ((rc = fft(r, r->work, r->work, 2 * batch, CUFFT_FORWARD))) return rc;
+  if ((rc = fft(r, r->work, r->work, 2 * batch, kForward))) return rc;
   rx::xspec_kernel<<<blocks(4 * m * batch), 256, 0, st>>>(r->work, r->refs, r->corr, m, batch);
   RX_LAUNCHED();
-  if ((rc = fft(r, r->corr, r->corr, 4 * batch, CUFFT_INVERSE))) return rc;
+  if ((rc = fft(r, r->corr, r->corr, 4 * batch, kInverse))) return rc;
   rx::argmax_kernel<<<4 * batch, 1024, 0, st>>>(r->corr, m, m, 0, 2, r->idx, nullptr);
   RX_LAUNCHED();
   const long long skip_sym = (skip_bits + 1) / 2;
@@ -752,7 +736,7 @@ int count_dev(dbp_rx* r, int batch, long long skip_bits, long long* errors, long
 
 int upload_ref_spectra(dbp_rx* r, const double2* h_ref) {
   RX_CUDA(cudaMemcpyAsync(r->refs, h_ref, 2 * r->m * sizeof(double2), cudaMemcpyHostToDevice, r->stream), "H2D(ref)");
-  return fft(r, r->refs, r->refs, 2, CUFFT_FORWARD);
+  return fft(r, r->refs, r->refs, 2, kForward);
 }
 
 }  // namespace
@@ -781,6 +765,7 @@ int dbp_rx_create(dbp_rx** out, int device, int64_t n_symbols, int max_batch) {
             cudaMalloc(&r->sym, B * 2 * m * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&r->work, B * 2 * m * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&r->corr, B * 4 * m * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&r->fftbuf, fft64::scratch_elems(m, 4 * B) * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&r->refs, 2 * m * sizeof(double2)) == cudaSuccess &&
             cudaMalloc(&r->bits, B * 4 * m) == cudaSuccess && cudaMalloc(&r->ref_bits, 4 * m) == cudaSuccess &&
             cudaMalloc(&r->red, B * 8 * sizeof(double)) == cudaSuccess &&
@@ -802,7 +787,7 @@ int dbp_rx_destroy(dbp_rx* r) {
   if (!r) return DBP_OK;
   Guard g(r->device);
   if (r->stream) cudaStreamSynchronize(r->stream);
-  for (auto& kv : r->plans) cufftDestroy(kv.second);
+  cudaFree(r->fftbuf);
   cudaFree(r->in);
   cudaFree(r->ext);
   cudaFree(r->sym);
@@ -882,7 +867,7 @@ int dbp_rx_count_errors(dbp_rx* r, const uint8_t* h_dec, int batch, const uint8_
   RX_CUDA(cudaMemcpyAsync(r->ref_bits, h_ref, (size_t)4 * m, cudaMemcpyHostToDevice, r->stream), "H2D(ref bits)");
   rx::bits_to_symbols_kernel<<<blocks(2 * m), 256, 0, r->stream>>>(r->ref_bits, r->refs, 2 * m);
   RX_LAUNCHED();
-  if ((rc = fft(r, r->refs, r->refs, 2, CUFFT_FORWARD))) return rc;
+  if ((rc = fft(r, r->refs, r->refs, 2, kForward))) return rc;
   std::vector<long long> e(batch);
   long long c = 0;
   if ((rc = count_dev(r, batch, skip_bits, e.data(), &c))) return rc;
@@ -932,7 +917,7 @@ int dbp_rx_chain(dbp_rx* r, const void* h_in, int in_is_c64, int batch, int taps
   RX_LAUNCHED();
   rx::bits_to_symbols_kernel<<<blocks(2 * m), 256, 0, st>>>(r->ref_bits, r->refs, 2 * m);
   RX_LAUNCHED();
-  if ((rc = fft(r, r->refs, r->refs, 2, CUFFT_FORWARD))) return rc;
+  if ((rc = fft(r, r->refs, r->refs, 2, kForward))) return rc;
   std::vector<long long> errors(batch);
   long long counted = 0;
   if ((rc = count_dev(r, batch, skip_bits, errors.data(), &counted))) return rc;

@@ -1,15 +1,15 @@
 // Float64 DFT utility (dbp_fft_c2c, include/dbp_b200.h): the reference's
 // spectral.fft / spectral.ifft (pkg/src/fiberdbp/spectral.py:37-48, numpy
-// pocketfft along the last axis, inverse scaled by 1/n) as a cuFFT Z2Z
-// library transform.  Not on the DBP path (the block kernel has its own
-// FFT); it completes the spectral module's API for callers of the drop-in.
+// pocketfft along the last axis, inverse scaled by 1/n) on the repo's own
+// float64 Stockham FFT (fft64.cuh; no cuFFT in the product library).  Not on
+// the DBP path (the block kernel has its own FFT); it completes the spectral
+// module's API for callers of the drop-in.
 #include <cuda_runtime.h>
-#include <cufft.h>
 
-#include <map>
+#include "fft64.cuh"
+
 #include <mutex>
 #include <string>
-#include <tuple>
 
 #include "../../include/dbp_b200.h"
 
@@ -20,11 +20,6 @@ void add_launches(long long n);
 using dbp_capi_internal::fail;
 
 namespace {
-
-__global__ void scale_kernel(double2* __restrict__ x, long long total, double s) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < total) x[i] = make_double2(x[i].x * s, x[i].y * s);
-}
 
 // phi = cumsum(incr) over one block of 1024 threads (contiguous chunks, then
 // a scan of the chunk sums); out = in * exp(j phi) for both polarisations
@@ -58,7 +53,6 @@ __global__ void phase_noise_kernel(const double2* __restrict__ in, const double*
 }
 
 std::mutex g_mu;
-std::map<std::tuple<int, long long, long long>, cufftHandle> g_plans;
 
 }  // namespace
 
@@ -74,36 +68,23 @@ extern "C" int dbp_fft_c2c(int device, const void* h_in, void* h_out, int64_t n,
   const size_t bytes = (size_t)batch * n * sizeof(double2);
   double2* d = nullptr;
   int rc = DBP_OK;
-  cufftHandle plan;
-  auto key = std::make_tuple(device, (long long)n, (long long)batch);
-  auto it = g_plans.find(key);
-  if (it == g_plans.end()) {
-    int nn = (int)n;
-    if (cufftPlanMany(&plan, 1, &nn, nullptr, 1, nn, nullptr, 1, nn, CUFFT_Z2Z, (int)batch) != CUFFT_SUCCESS) {
-      rc = fail(DBP_ECUDA, "cufftPlanMany failed");
-      goto done;
-    }
-    g_plans[key] = plan;
-  } else {
-    plan = it->second;
-  }
-  if (cudaMalloc(&d, bytes) != cudaSuccess) {
+  double2* res = nullptr;
+  long long launches = 0;
+  if (cudaMalloc(&d, 2 * bytes) != cudaSuccess) {
     rc = fail(DBP_ENOMEM, "device allocation failed");
     goto done;
   }
-  if (cudaMemcpy(d, h_in, bytes, cudaMemcpyHostToDevice) != cudaSuccess ||
-      cufftExecZ2Z(plan, reinterpret_cast<cufftDoubleComplex*>(d), reinterpret_cast<cufftDoubleComplex*>(d),
-                   inverse ? CUFFT_INVERSE : CUFFT_FORWARD) != CUFFT_SUCCESS) {
-    rc = fail(DBP_ECUDA, "cuFFT transform failed");
+  if (cudaMemcpy(d, h_in, bytes, cudaMemcpyHostToDevice) != cudaSuccess) {
+    rc = fail(DBP_ECUDA, "H2D failed");
     goto done;
   }
-  dbp_capi_internal::add_launches(1);
-  if (inverse) {
-    const long long total = (long long)batch * n;
-    scale_kernel<<<(unsigned)((total + 255) / 256), 256>>>(d, total, 1.0 / (double)n);
-    dbp_capi_internal::add_launches(1);
+  res = fft64::transform(d, d + (size_t)batch * n, n, batch, inverse != 0, true, 0, &launches);
+  dbp_capi_internal::add_launches(launches);
+  if (!res) {
+    rc = fail(DBP_ECUDA, "fft64 transform launch failed");
+    goto done;
   }
-  if (cudaMemcpy(h_out, d, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) rc = fail(DBP_ECUDA, "D2H failed");
+  if (cudaMemcpy(h_out, res, bytes, cudaMemcpyDeviceToHost) != cudaSuccess) rc = fail(DBP_ECUDA, "D2H failed");
 done:
   if (d) cudaFree(d);
   if (prev >= 0) cudaSetDevice(prev);

@@ -1,0 +1,261 @@
+"""GPU parity at the BASELINE configurations' stated sizes, and the reference's
+own property tests on the GPU path.
+
+* configs[0]: 2^16 PM-QPSK symbols/pol (RRC 0.1, 2 sps, 28 GBd), fine SSFM
+  (1 km steps) over 40 x 80 km SMF at 0 dBm, AWGN at OSNR 14 dB; ESSFM N_s = 1,
+  N_c = 17, 2048 / 700, symmetric and linear-first.  Bar (north_star):
+  per-block rel-L2 <= 1e-5 against the float64 oracle (oracle/dbp_port.py,
+  bit-identical to fiberdbp.dbp.backpropagate, dbp.py:160-235), identical hard
+  decisions on every symbol and |dQ| <= 0.02 dB -- through the matched-filter
+  receiver and through the reference receiver chain (butterfly_equalize ->
+  carrier_recover -> qpsk_decide, modem.py:118-125 / 230-351, restated in
+  oracle/rx_port.py).
+* configs[2]: 2^20 symbols/pol, SSFM-20 linear-first with gamma' = 8/9 * 1.3
+  on both sides, nine launch powers -4 .. +4 dBm, at 2048 / 700 and the
+  paper's 8192 / 1024.
+* configs[3]: the N_s x N_c x N grid at reduced batch (every fixed-tap FIR
+  instantiation plus a runtime-N_c one).
+* the reference's property tests: overlap-save identity for every length
+  1 .. 300 at N = 128 / M = 32 (test_spectral.py:119-125, with the identity
+  block processor), whole-signal filtering (test_spectral.py:78-97, with a
+  caller-supplied filter) and identity coefficients == plain SSFM on seeded
+  random configurations (test_dbp.py:90-114).
+
+The link waveforms come from the GPU link simulator (parity-tested against the
+reference's propagate_link in test_gpu_forward.py); both DBP implementations
+see the identical complex64 input.
+"""
+
+import math
+import warnings
+
+import numpy as np
+import pytest
+
+import paper_1507_00921_b200 as pb
+from oracle import dbp_port, pool, rx_port, waveforms
+
+from .helpers import port_config, quiet_link
+
+pytestmark = pytest.mark.gpu
+
+TOL_BLOCK = 1e-5
+RATE = 56e9
+BAUD = 28e9
+BETA2 = waveforms.d_to_beta2(17.0)
+
+
+def _dbp(x, cfg):
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        return pb.backpropagate_batch(x, RATE, cfg)
+
+
+def _link_waveforms(num_symbols, powers_dbm, gamma_link, seed=0, osnr_db=14.0):
+    """Seeded PM-QPSK (RRC 0.1) through 40 x 80 km at 1 km steps, AWGN at the receiver."""
+    txs, syms = [], []
+    for p in powers_dbm:
+        tx, sym = waveforms.qpsk_rrc(num_symbols, 2, 0.1, seed=seed, power_dbm=p)
+        txs.append(tx)
+        syms.append(sym)
+    span = pb.FiberParams(BETA2, gamma_link, 0.2, 80.0)
+    link = quiet_link(40, span)
+    rx = pb.propagate_link_batch(np.stack(txs), RATE, link, pb.SsfmStepConfig(80), [seed] * len(txs))
+    out = np.empty_like(rx)
+    for i in range(len(txs)):
+        out[i] = waveforms.add_awgn_osnr(rx[i].astype(np.complex128), RATE, osnr_db, seed=100 + i)
+    return out.astype(np.complex64), syms
+
+
+def _soft(samples):
+    """Matched filter, symbol-centre sampling, blind 4th-power phase (oracle/waveforms.py)."""
+    return waveforms.receive_symbols(np.asarray(samples, dtype=np.complex128))
+
+
+def _decisions(samples):
+    return waveforms.hard_decisions(_soft(samples))
+
+
+def _q_aligned(soft, tx_symbols):
+    """Q (dB) against the transmitted symbols after resolving the receiver's
+    90-degree phase ambiguity per polarisation (modem.py:409-412 formula)."""
+    errs, bits = 0, 0
+    for p in range(2):
+        ref = waveforms.hard_decisions(tx_symbols[p])
+        errs += min(int(np.sum(waveforms.hard_decisions(soft[p] * 1j ** k) != ref)) for k in range(4))
+        bits += ref.size
+    ber = errs / bits
+    if ber == 0.0:
+        return math.inf
+    from scipy.special import erfcinv
+    return 20.0 * math.log10(math.sqrt(2.0) * float(erfcinv(2.0 * ber)))
+
+
+def _decision_flips(soft_gpu, soft_ref):
+    """(flips, unexplained): decisions that differ, and those of them whose
+    float64 soft value is farther from the threshold than 3x the GPU-oracle
+    difference of that very symbol (a flip of a decision sitting within the
+    numerical difference of the boundary is the tolerance at work, not an error)."""
+    flips = unexplained = 0
+    for part in (np.real, np.imag):
+        g, r = part(soft_gpu), part(soft_ref)
+        f = (g < 0.0) != (r < 0.0)
+        flips += int(np.sum(f))
+        unexplained += int(np.sum(f & (np.abs(r) > 3.0 * np.abs(g - r) + 1e-12)))
+    return flips, unexplained
+
+
+@pytest.fixture(scope="module")
+def config0_link():
+    rx, syms = _link_waveforms(1 << 16, [0.0], 1.3)
+    return rx[0], syms[0]
+
+
+@pytest.mark.parametrize("arrangement", ["symmetric", "linear-first"])
+def test_config0_full_size(config0_link, arrangement):
+    rx, sym = config0_link
+    assert rx.shape == (2, 1 << 17)
+    span = pb.FiberParams(BETA2, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)), arrangement=arrangement)
+    got = _dbp(rx, cfg)[0]
+    want = dbp_port.backpropagate_arrays(rx.astype(np.complex128), RATE, port_config(cfg))
+    err = dbp_port.per_block_rel_l2(got, want, 2048, 700)
+    assert err.max() <= TOL_BLOCK, err.max()
+    # matched-filter receiver: every decision identical, Q within 0.02 dB
+    s_gpu, s_ref = _soft(got), _soft(want)
+    assert np.array_equal(waveforms.hard_decisions(s_gpu), waveforms.hard_decisions(s_ref))
+    q_gpu, q_ref = _q_aligned(s_gpu, sym), _q_aligned(s_ref, sym)
+    assert q_gpu == q_ref or abs(q_gpu - q_ref) <= 0.02
+    # the reference receiver chain (modem.py: CMA butterfly, carrier recovery, decisions)
+    eq_gpu, _, _ = rx_port.equalize(got.astype(np.complex128))
+    eq_ref, _, _ = rx_port.equalize(want)
+    rec_gpu, _, _ = rx_port.carrier(eq_gpu, BAUD, reference=sym)
+    rec_ref, _, _ = rx_port.carrier(eq_ref, BAUD, reference=sym)
+    d_gpu, d_ref = rx_port.decide(rec_gpu), rx_port.decide(rec_ref)
+    assert np.array_equal(d_gpu, d_ref)
+    e_gpu, n_gpu = rx_port.count_errors(d_gpu, rx_port.decide(sym), skip=1024)
+    e_ref, n_ref = rx_port.count_errors(d_ref, rx_port.decide(sym), skip=1024)
+    assert (e_gpu, n_gpu) == (e_ref, n_ref)
+    print(f"config0 {arrangement}: worst block {err.max():.2e}, Q {q_gpu:.3f} dB, CMA-chain errors {e_gpu}/{n_gpu}")
+
+
+@pytest.fixture(scope="module")
+def config2_links():
+    powers = [float(p) for p in range(-4, 5)]
+    rx, syms = _link_waveforms(1 << 20, powers, 1.3 * 8.0 / 9.0, seed=2)
+    return powers, rx, syms
+
+
+@pytest.mark.parametrize("n_blk,m", [(2048, 700), (8192, 1024)])
+def test_config2_full_size_power_sweep(config2_links, n_blk, m):
+    # 20-step SSFM linear-first, gamma' = 8/9 * 1.3 (Manakov average) on both sides
+    powers, rx, syms = config2_links
+    span = pb.FiberParams(BETA2, 1.3 * 8.0 / 9.0, 0.2, 80.0)
+    cfg = pb.DbpConfig("ssfm", pb.OverlapPlan(n_blk, m), quiet_link(40, span), num_steps=20,
+                       arrangement="linear-first")
+    got = _dbp(rx, cfg)
+    kw = pool.port_kwargs(cfg)
+    want = pool.backpropagate_many([(rx[i], RATE, kw) for i in range(len(powers))])
+    # 2^22 hard decisions per power: with a per-block rel-L2 of ~2e-6 and the
+    # OSNR-14 symbol cloud, ~1 decision per power sits within the numerical
+    # difference of its threshold (measured: 0-1 per power).  Every flip must be
+    # such a boundary symbol (_decision_flips), and there may be at most 4 per
+    # power; Q must agree within 0.02 dB.
+    for i, p in enumerate(powers):
+        err = dbp_port.per_block_rel_l2(got[i], want[i], n_blk, m)
+        assert err.max() <= TOL_BLOCK, (p, err.max())
+        s_gpu, s_ref = _soft(got[i]), _soft(want[i])
+        flips, unexplained = _decision_flips(s_gpu, s_ref)
+        assert unexplained == 0 and flips <= 4, (p, flips, unexplained)
+        q_gpu, q_ref = _q_aligned(s_gpu, syms[i]), _q_aligned(s_ref, syms[i])
+        assert q_gpu == q_ref or abs(q_gpu - q_ref) <= 0.02, (p, q_gpu, q_ref)
+        print(f"config2 {n_blk}/{m} {p:+.0f} dBm: worst block {err.max():.2e}, decision flips {flips} "
+              f"(all within the numerical difference of the threshold), Q {q_gpu:.4f} vs {q_ref:.4f} dB")
+
+
+GRID_M = {1024: 768, 2048: 1400, 4096: 1400, 8192: 1400}
+
+
+@pytest.mark.parametrize("n_blk", [1024, 2048, 4096, 8192])
+@pytest.mark.parametrize("nc", [1, 9, 17, 32, 33, 13])
+@pytest.mark.parametrize("ns", [1, 2, 4])
+def test_config3_grid(n_blk, nc, ns):
+    # N_s x N_c x N of configs[3] (plus N_c = 32 and the runtime-N_c path at 13):
+    # two seeded waveforms per point, ragged length, edge blocks included
+    m = GRID_M[n_blk]
+    gen = np.random.default_rng(n_blk * 100 + nc * 10 + ns)
+    n = 3 * (n_blk - m) + 101
+    x = (0.02 * (gen.normal(size=(2, 2, n)) + 1j * gen.normal(size=(2, 2, n)))).astype(np.complex64)
+    span = pb.FiberParams(BETA2, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(n_blk, m), quiet_link(40, span), num_steps=ns,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(nc)))
+    got = _dbp(x, cfg)
+    for i in range(2):
+        want = dbp_port.backpropagate_arrays(x[i].astype(np.complex128), RATE, port_config(cfg))
+        err = dbp_port.per_block_rel_l2(got[i], want, n_blk, m)
+        assert err.max() <= TOL_BLOCK, err.max()
+
+
+def test_overlap_save_identity_every_length():
+    # test_spectral.py:119-125 (hypothesis over n in [1, 300], shift in [0, 3]) and
+    # test_spectral.py:72-76: the identity block processor reproduces any length exactly
+    plan = pb.OverlapPlan(128, 32)
+    proc = pb.identity_processor(plan, 1e9)
+    for n_total in range(1, 301):
+        gen = np.random.default_rng(n_total * 7 + (n_total % 4))
+        x = gen.normal(size=n_total) + 1j * gen.normal(size=n_total)
+        y = gen.normal(size=n_total) + 1j * gen.normal(size=n_total)
+        sig = pb.DualPolSignal(x.astype(np.complex64), y.astype(np.complex64), 1e9)
+        out = pb.overlap_save_run(sig, plan, proc)
+        np.testing.assert_array_equal(out.stack(), sig.stack())
+        assert out.sample_rate == sig.sample_rate
+    big = pb.OverlapPlan(2048, 512)
+    for n_total in (1, 5, 1536, 1537, 4096, 5000):
+        gen = np.random.default_rng(n_total)
+        s = (gen.normal(size=(2, n_total)) + 1j * gen.normal(size=(2, n_total))).astype(np.complex64)
+        sig = pb.DualPolSignal(s[0], s[1], 1e9)
+        out = pb.overlap_save_run(sig, big, pb.identity_processor(big, 1e9))
+        np.testing.assert_array_equal(out.stack(), sig.stack())
+
+
+def test_overlap_save_matches_whole_signal_filtering():
+    # test_spectral.py:78-97 with the caller's filter as a GPU block processor
+    gen = np.random.default_rng(78)
+    s = (gen.normal(size=(2, 8192)) + 1j * gen.normal(size=(2, 8192)))
+    sig = pb.DualPolSignal(s[0].astype(np.complex64), s[1].astype(np.complex64), 56e9)
+
+    def cd_kernel(freqs):
+        return np.exp(1j * 2.0 * np.pi ** 2 * (-21.0 * 1e-24) * freqs ** 2 * 100.0)
+
+    stacked = sig.stack().astype(np.complex128)
+    direct = np.fft.ifft(np.fft.fft(stacked) * cd_kernel(np.fft.fftfreq(8192, 1 / 56e9)))
+    plan = pb.OverlapPlan(2048, 512)
+    proc = pb.filter_processor(plan, cd_kernel(pb.fft_frequencies(2048, 56e9)), 56e9)
+    blocked = pb.overlap_save_run(sig, plan, proc).stack()
+    err = np.sum(np.abs(blocked - direct) ** 2) / np.sum(np.abs(direct) ** 2)
+    assert err < 1e-5
+    # and per block against the oracle's filter_block framing
+    blocks = dbp_port.cut_blocks(stacked, 2048, 512)
+    h = cd_kernel(pb.fft_frequencies(2048, 56e9))
+    want = dbp_port.join_blocks(np.stack([dbp_port.filter_block(b, h) for b in blocks]), 8192, 512)
+    assert dbp_port.per_block_rel_l2(blocked, want, 2048, 512).max() <= TOL_BLOCK
+
+
+def test_identity_coefficients_degenerate_to_plain_random():
+    # test_dbp.py:90-114 (hypothesis, 10 examples): seeded draws of the same space
+    gen = np.random.default_rng(90114)
+    span = pb.FiberParams(-21.0, 1.3, 0.2, 40.0)
+    for _ in range(24):
+        spans = int(gen.integers(1, 4))
+        steps = int(gen.integers(1, 6))
+        arrangement = pb.ARRANGEMENTS[int(gen.integers(0, 3))]
+        seed = int(gen.integers(0, 2 ** 31))
+        g2 = np.random.default_rng(seed)
+        x = (g2.normal(size=(2, 1024)) + 1j * g2.normal(size=(2, 1024))).astype(np.complex64)
+        plan = pb.OverlapPlan(512, 128)
+        link = quiet_link(spans, span)
+        plain = _dbp(x, pb.DbpConfig("ssfm", plan, link, num_steps=steps, arrangement=arrangement))
+        ident = _dbp(x, pb.DbpConfig("essfm", plan, link, num_steps=steps,
+                                     coeffs=pb.EssfmCoefficients.identity(16), arrangement=arrangement))
+        np.testing.assert_array_equal(plain, ident)

@@ -58,6 +58,10 @@ VARIANTS = {
     "pubf0": ["-DDBP_NL_PUBLISH_F=0"],
     "nodit": ["-DDBP_DIT_MAX_STEPS=0"],
     "dit4": ["-DDBP_DIT_MAX_STEPS=4"],
+    "noload": ["-DDBP_EXPERIMENT_NOLOAD=1"],      # timing ceilings only: wrong results
+    "nostore": ["-DDBP_EXPERIMENT_NOSTORE=1"],
+    "nonl": ["-DDBP_EXPERIMENT_NONL=1"],
+    "noio": ["-DDBP_EXPERIMENT_NOLOAD=1", "-DDBP_EXPERIMENT_NOSTORE=1"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
