@@ -551,7 +551,12 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
     }
   } drain{p};
 
-  if (item <= slot_budget) {
+  // A block range (a multi-device shard of one waveform) stages only its
+  // halo'd span [b0 step - M/2, b1 step - M/2 + N) through the chunk path,
+  // so host-to-device traffic is shard + halo, not the whole waveform
+  // (unless that span would wrap onto itself: a short waveform).
+  const bool span_fits = (block_end - block_begin) * p->step + p->M <= n_total;
+  if (item <= slot_budget && (full_range || !span_fits)) {
     // whole items per chunk, cyclic mode, two streams ping-pong
     const int per = (int)std::min<size_t>((size_t)batch, slot_budget / item);
     rc = ensure_staging(p, per * item);

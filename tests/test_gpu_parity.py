@@ -437,3 +437,25 @@ def test_nofir_kernel_matches_oracle(alg, n_blk, m, steps, arr):
         want = dbp_port.backpropagate_arrays(x[i].astype(np.complex128), 56e9, port_config(cfg))
         assert dbp_port.per_block_rel_l2(got[i], want, n_blk, m).max() <= TOL_BLOCK
         np.testing.assert_array_equal(got[i], _run(x[i:i + 1], cfg)[0])
+
+
+@pytest.mark.parametrize("batch", [1, 3])
+def test_multi_device_split_bit_equal(rng, batch):
+    # backpropagate_batch(devices=[...]) on one GPU listed twice: B < #devices splits the
+    # waveform by block range (each shard staged as its halo'd span only), B >= #devices
+    # by whole waveforms; both must equal the single-device run bit for bit
+    # (blocks are independent, spectral.py:100-101)
+    n = 7 * 1348 + 77
+    x = (0.02 * (rng.normal(size=(batch, 2, n)) + 1j * rng.normal(size=(batch, 2, n)))).astype(np.complex64)
+    span = pb.FiberParams(-21.6826, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    one = _run(x, cfg)
+    for devs in ([0, 0], [0, 0, 0]):
+        np.testing.assert_array_equal(_run(x, cfg, devices=devs), one)
+    # and through the drop-in call
+    sig = pb.DualPolSignal(x[0, 0], x[0, 1], 56e9)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        out = pb.backpropagate(sig, cfg, devices=[0, 0])
+    np.testing.assert_array_equal(out.stack(), one[0])

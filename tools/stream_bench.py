@@ -11,7 +11,15 @@ b_g = floor(g nb / G) (multiples of N - M), builds its halo'd span
 the stream ends) and runs ``dbp_run_chunk`` -- no collective on the data
 path.  Prints one JSON line (rank 0): whole-stream Gsamples/s (max over
 ranks), per-chunk latency, and a per-rank output checksum that must be
-identical to the 1-GPU run's for the same sample ranges.
+identical to the 1-GPU run's for the same sample ranges
+(``--digest-splits K`` on a 1-rank run prints the digests of the K-way shard
+ranges of its output, for comparison with a K-rank run).
+
+``--backend gloo`` runs the collectives (barrier, max-time reduction, digest
+gather, optional final gather) on CPU tensors, so a K-rank run also works with
+several ranks on ONE GPU (ranks map to ``LOCAL_RANK % device_count``) -- the
+multi-rank correctness check on a single-GPU box; its timing is not a scaling
+number.
 """
 
 import argparse
@@ -53,6 +61,9 @@ def main():
     ap.add_argument("--log2-samples", type=int, default=30)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--backend", choices=("nccl", "gloo"), default="nccl")
+    ap.add_argument("--digest-splits", type=int, default=0,
+                    help="1-rank runs: also print the output digests of the K-way shard ranges")
     ap.add_argument("--gather", action="store_true",
                     help="after timing, assemble the whole output stream on rank 0 (NCCL point-to-point over "
                          "NVLink; not part of the timed path) and report its digest and the gather time")
@@ -67,10 +78,15 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if a.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     dev = f"cuda:{local}"
+    red_dev = dev if a.backend == "nccl" else "cpu"
     warnings.simplefilter("ignore")
     args = bench.parse_args([])
     cfg = bench.make_cfg(args)
@@ -100,7 +116,7 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     digest = hashlib.sha256(out.cpu().numpy().tobytes()).hexdigest()[:16]
@@ -109,6 +125,13 @@ def main():
         dist.all_gather_object(digests, (rank, olo, ohi, digest))
     else:
         digests = [(0, olo, ohi, digest)]
+    split_digests = None
+    if world == 1 and a.digest_splits > 1:
+        split_digests = []
+        host = out.cpu().numpy()
+        for k, (s0, s1) in enumerate(pb.shard_blocks(nb, a.digest_splits)):
+            klo, khi = cfg.plan.output_span(s0, s1, n)
+            split_digests.append([k, klo, khi, hashlib.sha256(host[:, klo - olo:khi - olo].tobytes()).hexdigest()[:16]])
     gather = None
     if a.gather:
         # optional final gather: rank r's output span [olo, ohi) -> rank 0, no data-path collective
@@ -124,21 +147,22 @@ def main():
             full[:, olo:ohi] = out
             for r in range(1, world):
                 rlo, rhi = spans[r]
-                buf = torch.empty((2, rhi - rlo, 2), device=dev)
+                buf = torch.empty((2, rhi - rlo, 2), device=red_dev)
                 dist.recv(buf, src=r)
-                full[:, rlo:rhi] = buf
+                full[:, rlo:rhi] = buf.to(dev)
             torch.cuda.synchronize()
             gather = {"seconds": time.perf_counter() - g0,
                       "digest": hashlib.sha256(full.cpu().numpy().tobytes()).hexdigest()[:16]}
         else:
-            dist.send(out.contiguous(), dst=0)
+            dist.send(out.contiguous().to(red_dev), dst=0)
     if rank == 0:
         ms_max = float(t.item())
         print(json.dumps({
             "metric": "ESSFM 1-step DBP Gsamples/s (dual-pol), configs[4] stream", "unit": "Gsamples/s",
             "value": n / (ms_max * 1e-3) / 1e9, "n_gpus": world, "stream_samples": n, "blocks": nb,
             "chunk_latency_ms": ms_max, "halo_samples": [cfg.plan.lead, cfg.plan.overlap - cfg.plan.lead],
-            "shards": [list(d) for d in digests], "device_resident": True,
+            "shards": [list(d) for d in digests], "split_digests": split_digests, "backend": a.backend,
+            "device_resident": True,
             "gather": gather,
         }), flush=True)
     if world > 1:
