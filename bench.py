@@ -207,6 +207,39 @@ class ClockSampler:
 # our arm
 # ---------------------------------------------------------------------------
 
+def time_dropin(a, cfg, dev) -> dict:
+    """The reference-facing call itself: ``backpropagate(sig, cfg)`` (dbp.py:160)
+    on a complex128 ``DualPolSignal`` in host memory, complex128 result back --
+    at the configs[0] length (2^17 samples/pol) and at 2^24 samples/pol.  Each
+    call includes the casts, the H2D / D2H copies and the synchronisation."""
+    import warnings
+
+    import numpy as np
+
+    import paper_1507_00921_b200 as pb
+    out = {}
+    for log2n, reps in ((17, 50), (24, 5)):
+        n = 1 << log2n
+        rng = np.random.default_rng(log2n)
+        amp = math.sqrt(10 ** ((POWER_DBM - 30) / 10) / 4.0)
+        xs = amp * (rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n)))
+        sig = pb.DualPolSignal(xs[0], xs[1], SAMPLE_RATE)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            pb.backpropagate(sig, cfg, device=dev)          # warm: engine, staging, host threads
+            t0 = time.perf_counter()
+            for _ in range(reps):
+                res = pb.backpropagate(sig, cfg, device=dev)
+            sec = (time.perf_counter() - t0) / reps
+        assert res.x.dtype == np.complex128 and len(res) == n
+        out[f"2^{log2n}"] = {"value": n / sec / 1e9, "unit": UNIT, "seconds_per_call": sec, "calls": reps,
+                             "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8,
+                             "host_bytes_in": 2 * n * 16, "host_bytes_out": 2 * n * 16}
+    out["path"] = ("paper_1507_00921_b200.backpropagate(DualPolSignal complex128, DbpConfig) -> "
+                   "dbp_backpropagate_c128 (host-thread casts into pinned staging, chunked H2D / kernel / D2H)")
+    return out
+
+
 def run_ours(a) -> int:
     import numpy as np
     import torch
@@ -329,6 +362,7 @@ def run_ours(a) -> int:
         e2e["matches_device_path"] = bool(ok)
         hin.free()
         hout.free()
+        e2e["dropin"] = time_dropin(a, cfg, dev)
 
     # ---- CPU baseline (rank 0, single-GPU runs only) ----
     cpu = None

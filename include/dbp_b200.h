@@ -120,6 +120,18 @@ int dbp_run_chunk(dbp_plan* plan, const void* d_in, void* d_out, int64_t n_total
 int dbp_run_host(dbp_plan* plan, const void* h_in, void* h_out, int64_t n_total, int batch,
                  int64_t block_begin, int64_t block_end);
 
+/* The drop-in call itself: backpropagate(sig, cfg) (dbp.py:160) on the
+ * reference's complex128 rows -- h_x, h_y: n_total complex128 samples of
+ * each polarisation (DualPolSignal.x / .y, sigkit.py:56-68), h_out_x,
+ * h_out_y: complex128 results of the same length.  The whole signal, cyclic
+ * framing (spectral.py:122-145).  The complex128 -> complex64 casts (numpy's
+ * astype rounding) and back run on host threads (DBP_HOST_THREADS, default
+ * min(16, cores)) into pinned staging, pipelined over block-range chunks of
+ * ~2^21 samples with halos against the H2D copy, the kernel and the D2H
+ * copy.  Synchronous; bitwise equal to dbp_run_host on the complex64 cast.   */
+int dbp_backpropagate_c128(dbp_plan* plan, const void* h_x, const void* h_y, void* h_out_x, void* h_out_y,
+                           int64_t n_total);
+
 /* Device staging budget (bytes) used by dbp_run_host (default 256 MiB: 32   
  * pipelined chunks for the configs[3] batch, so the un-overlapped first    
  * H2D and last D2H stay short).                                             */

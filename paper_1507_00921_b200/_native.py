@@ -37,6 +37,7 @@ SIGNATURES = {
                                _c_int64, _c_int64, _c_void_p]),
     "dbp_run_host": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int, _c_int64, _c_int64]),
     "dbp_plan_set_staging": (_c_int, [_c_void_p, ctypes.c_size_t]),
+    "dbp_backpropagate_c128": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_int64]),
     "dbp_process_blocks": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_void_p]),
     "dbp_plan_synchronize": (_c_int, [_c_void_p]),
     "dbp_host_alloc": (_c_int, [ctypes.POINTER(_c_void_p), ctypes.c_size_t]),
@@ -220,6 +221,15 @@ class NativePlan:
                 raise ValueError("host buffers must be C-contiguous complex64 (batch, 2, n)")
         _check(self._lib.dbp_run_host(self._h, h_in.ctypes.data, h_out.ctypes.data, int(n_total),
                                       int(batch), int(block_begin), int(block_end)), "dbp_run_host")
+
+    def backpropagate_c128(self, x: np.ndarray, y: np.ndarray, out_x: np.ndarray, out_y: np.ndarray):
+        """The drop-in call on complex128 rows (dbp_backpropagate_c128): x, y -> out_x, out_y."""
+        n = x.size
+        for a in (x, y, out_x, out_y):
+            if a.dtype != np.complex128 or not a.flags.c_contiguous or a.ndim != 1 or a.size != n:
+                raise ValueError("rows must be C-contiguous 1-D complex128 arrays of equal length")
+        _check(self._lib.dbp_backpropagate_c128(self._h, x.ctypes.data, y.ctypes.data, out_x.ctypes.data,
+                                                out_y.ctypes.data, int(n)), "dbp_backpropagate_c128")
 
     def run_host_ptr(self, p_in: int, p_out: int, n_total: int, batch: int, block_begin: int,
                      block_end: int):

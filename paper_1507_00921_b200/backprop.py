@@ -272,6 +272,16 @@ def backpropagate(sig: DualPolSignal, cfg: DbpConfig, jobs: int = 1, *,
     _warn_short_overlap(cfg, sig.sample_rate, stacklevel=2)
     if jobs < 1:
         raise ValueError("jobs must be >= 1")
+    devs = _resolve_devices(device, devices)
+    if len(devs) == 1:
+        # complex128 rows straight through the C ABI: casts on host threads,
+        # pinned staging, chunked H2D / kernel / D2H pipeline
+        eng = get_engine(cfg, sig.sample_rate, devs[0])
+        x, y = np.ascontiguousarray(sig.x, dtype=np.complex128), np.ascontiguousarray(sig.y, dtype=np.complex128)
+        out_x, out_y = np.empty_like(x), np.empty_like(y)
+        with eng.native.lock:
+            eng.native.backpropagate_c128(x, y, out_x, out_y)
+        return DualPolSignal(out_x, out_y, sig.sample_rate)
     x = np.empty((1, 2, len(sig)), dtype=np.complex64)
     x[0, 0] = sig.x
     x[0, 1] = sig.y

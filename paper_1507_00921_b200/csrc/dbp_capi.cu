@@ -7,7 +7,9 @@
 // thread-local string (dbp_last_error).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
+#include <thread>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -17,6 +19,7 @@
 #include <vector>
 
 #include "../../include/dbp_b200.h"
+#include "host_pool.h"
 #include "launch.h"
 
 namespace {
@@ -110,6 +113,12 @@ struct dbp_plan {
   cudaStream_t streams[2] = {nullptr, nullptr};
   void* d_stage[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [slot][in/out]
   size_t stage_bytes = 0;
+  // complex128 drop-in path (dbp_backpropagate_c128): pinned complex64
+  // staging per slot [in/out], its size, completion events, host threads
+  void* h_pin[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  size_t pin_bytes = 0;
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  dbp::HostPool* pool = nullptr;
 };
 
 namespace {
@@ -294,8 +303,12 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
 int dbp_plan_destroy(dbp_plan* p) {
   if (!p) return DBP_OK;
   DeviceGuard g(p->device);
+  delete p->pool;
   for (int s = 0; s < 2; ++s) {
     if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
+    for (int k = 0; k < 2; ++k)
+      if (p->h_pin[s][k]) cudaFreeHost(p->h_pin[s][k]);
+    if (p->done[s]) cudaEventDestroy(p->done[s]);
     for (int k = 0; k < 2; ++k)
       if (p->d_stage[s][k]) cudaFree(p->d_stage[s][k]);
     if (p->streams[s]) cudaStreamDestroy(p->streams[s]);
@@ -625,6 +638,139 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
     }
   }
   for (int s = 0; s < 2; ++s) DBP_CUDA(cudaStreamSynchronize(p->streams[s]), "cudaStreamSynchronize");
+  return DBP_OK;
+}
+
+namespace {
+
+int ensure_pinned(dbp_plan* p, size_t bytes) {
+  if (p->pin_bytes >= bytes) return DBP_OK;
+  for (int s = 0; s < 2; ++s)
+    for (int k = 0; k < 2; ++k) {
+      if (p->h_pin[s][k]) cudaFreeHost(p->h_pin[s][k]);
+      p->h_pin[s][k] = nullptr;
+    }
+  p->pin_bytes = 0;
+  for (int s = 0; s < 2; ++s)
+    for (int k = 0; k < 2; ++k)
+      if (cudaHostAlloc(&p->h_pin[s][k], bytes, cudaHostAllocPortable) != cudaSuccess)
+        return fail(DBP_ENOMEM, "pinned staging allocation failed");
+  p->pin_bytes = bytes;
+  for (int s = 0; s < 2; ++s)
+    if (!p->done[s]) DBP_CUDA(cudaEventCreateWithFlags(&p->done[s], cudaEventDisableTiming), "cudaEventCreate");
+  if (!p->pool) {
+    const unsigned hc = std::thread::hardware_concurrency();
+    static const int env_threads = [] {
+      const char* v = std::getenv("DBP_HOST_THREADS");
+      return v ? std::atoi(v) : 0;
+    }();
+    int t = env_threads > 0 ? env_threads : (int)std::min(16u, hc ? hc : 1u);
+    p->pool = new (std::nothrow) dbp::HostPool(std::max(1, t));
+    if (!p->pool) return fail(DBP_ENOMEM, "host thread pool");
+  }
+  return DBP_OK;
+}
+
+// dst[i] = (float2) src[(g0 + i) mod n] for i < len, over the host pool
+void narrow_span(dbp::HostPool* pool, const double2* src, int64_t n, int64_t g0, int64_t len, float2* dst) {
+  pool->parallel_for(len, [&](long long lo, long long hi) {
+    long long i = lo;
+    while (i < hi) {
+      int64_t g = (g0 + i) % n;
+      if (g < 0) g += n;
+      const long long run = std::min<long long>(hi - i, n - g);
+      const double2* s = src + g;
+      float2* d = dst + i;
+      for (long long k = 0; k < run; ++k) d[k] = make_float2((float)s[k].x, (float)s[k].y);
+      i += run;
+    }
+  });
+}
+
+void widen(dbp::HostPool* pool, const float2* src, int64_t len, double2* dst) {
+  pool->parallel_for(len, [&](long long lo, long long hi) {
+    for (long long k = lo; k < hi; ++k) dst[k] = make_double2((double)src[k].x, (double)src[k].y);
+  });
+}
+
+}  // namespace
+
+int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* h_out_x, void* h_out_y,
+                           int64_t n_total) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (!h_x || !h_y || !h_out_x || !h_out_y) return fail(DBP_EINVAL, "null host buffer");
+  if (n_total < 1) return fail(DBP_EINVAL, "signal must contain at least one sample");
+  DeviceGuard g(p->device);
+  const double2* in[2] = {static_cast<const double2*>(h_x), static_cast<const double2*>(h_y)};
+  double2* out[2] = {static_cast<double2*>(h_out_x), static_cast<double2*>(h_out_y)};
+  const int64_t nb = (n_total + p->step - 1) / p->step;
+  // chunk: a block range whose halo'd span is ~2^21 samples per polarisation
+  const int64_t per_blocks = std::max<int64_t>(1, ((int64_t(1) << 21) - p->M) / p->step);
+  const bool single = nb <= per_blocks || per_blocks * p->step + p->M > n_total;
+  const int64_t span_cap = single ? n_total : per_blocks * p->step + p->M;
+  const int64_t out_cap = single ? n_total : per_blocks * p->step;
+  const size_t in_bytes = (size_t)2 * span_cap * sizeof(float2), out_bytes = (size_t)2 * out_cap * sizeof(float2);
+  rc = ensure_staging(p, std::max(in_bytes, out_bytes));
+  if (rc) return rc;
+  rc = ensure_pinned(p, std::max(in_bytes, out_bytes));
+  if (rc) return rc;
+  struct StreamDrain {
+    dbp_plan* p;
+    ~StreamDrain() {
+      for (int s = 0; s < 2; ++s)
+        if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
+    }
+  } drain{p};
+  const int64_t n_chunks = single ? 1 : (nb + per_blocks - 1) / per_blocks;
+  // output of chunk k: [olo, ohi) per polarisation
+  auto out_range = [&](int64_t k, int64_t& olo, int64_t& ohi) {
+    if (single) {
+      olo = 0;
+      ohi = n_total;
+      return;
+    }
+    const int64_t b0 = k * per_blocks, b1 = std::min(nb, b0 + per_blocks);
+    olo = b0 * p->step;
+    ohi = std::min<int64_t>(n_total, b1 * p->step);
+  };
+  auto finish = [&](int64_t k) -> int {
+    const int slot = (int)(k & 1);
+    DBP_CUDA(cudaEventSynchronize(p->done[slot]), "cudaEventSynchronize");
+    int64_t olo, ohi;
+    out_range(k, olo, ohi);
+    const float2* pin = static_cast<const float2*>(p->h_pin[slot][1]);
+    for (int pol = 0; pol < 2; ++pol) widen(p->pool, pin + pol * (ohi - olo), ohi - olo, out[pol] + olo);
+    return DBP_OK;
+  };
+  for (int64_t k = 0; k < n_chunks; ++k) {
+    const int slot = (int)(k & 1);
+    if (k >= 2 && (rc = finish(k - 2))) return rc;
+    cudaStream_t s = p->streams[slot];
+    float2* pin_in = static_cast<float2*>(p->h_pin[slot][0]);
+    float2* pin_out = static_cast<float2*>(p->h_pin[slot][1]);
+    char* din = static_cast<char*>(p->d_stage[slot][0]);
+    char* dout = static_cast<char*>(p->d_stage[slot][1]);
+    int64_t olo, ohi;
+    out_range(k, olo, ohi);
+    if (single) {
+      for (int pol = 0; pol < 2; ++pol) narrow_span(p->pool, in[pol], n_total, 0, n_total, pin_in + pol * n_total);
+      DBP_CUDA(cudaMemcpyAsync(din, pin_in, 2 * n_total * sizeof(float2), cudaMemcpyHostToDevice, s), "H2D");
+      rc = dbp_run(p, din, dout, n_total, 1, 0, nb, s);
+      if (rc) return rc;
+    } else {
+      const int64_t b0 = k * per_blocks, b1 = std::min(nb, b0 + per_blocks);
+      const int64_t span = (b1 - b0) * p->step + p->M, g0 = b0 * p->step - p->lead;
+      for (int pol = 0; pol < 2; ++pol) narrow_span(p->pool, in[pol], n_total, g0, span, pin_in + pol * span);
+      DBP_CUDA(cudaMemcpyAsync(din, pin_in, 2 * span * sizeof(float2), cudaMemcpyHostToDevice, s), "H2D");
+      rc = dbp_run_chunk(p, din, dout, n_total, 1, b0, b1, span, ohi - olo, s);
+      if (rc) return rc;
+    }
+    DBP_CUDA(cudaMemcpyAsync(pin_out, dout, 2 * (ohi - olo) * sizeof(float2), cudaMemcpyDeviceToHost, s), "D2H");
+    DBP_CUDA(cudaEventRecord(p->done[slot], s), "cudaEventRecord");
+  }
+  for (int64_t k = std::max<int64_t>(0, n_chunks - 2); k < n_chunks; ++k)
+    if ((rc = finish(k))) return rc;
   return DBP_OK;
 }
 

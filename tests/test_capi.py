@@ -54,3 +54,15 @@ def test_invalid_geometry_rejected_before_device_lookup():
 def test_missing_library_fails_loudly(tmp_path):
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _native.load_library(tmp_path / "nope.so")
+
+
+def test_product_library_links_no_fft_or_blas_library():
+    # SURVEY 8(a) / north_star: cuFFT only as a cross-check, never in the product path;
+    # the library links static cudart and the C/C++ runtime only
+    import subprocess
+    out = subprocess.run(["ldd", str(_native.LIB_PATH)], capture_output=True, text=True).stdout
+    for lib in ("cufft", "cublas", "cudnn", "libcudart.so"):
+        assert lib not in out, out
+    syms = subprocess.run(["nm", "-D", "--undefined-only", str(_native.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    assert "cufft" not in syms.lower()

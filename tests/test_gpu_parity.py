@@ -459,3 +459,21 @@ def test_multi_device_split_bit_equal(rng, batch):
         warnings.simplefilter("ignore")
         out = pb.backpropagate(sig, cfg, devices=[0, 0])
     np.testing.assert_array_equal(out.stack(), one[0])
+
+
+@pytest.mark.parametrize("n_total", [1, 5, 1348, 4099, (1 << 17), (1 << 22) + 777])
+def test_dropin_complex128_path_bit_equal(rng, n_total):
+    # backpropagate(sig, cfg) on complex128 rows (dbp_backpropagate_c128: host-thread casts,
+    # pinned staging, block-range chunks with halos above 2^21 samples) == the batch path on
+    # the complex64 cast, bit for bit, returned as complex128 (sigkit.py:56-68)
+    x = 0.02 * (rng.normal(size=(2, n_total)) + 1j * rng.normal(size=(2, n_total)))
+    span = pb.FiberParams(-21.6826, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    sig = pb.DualPolSignal(x[0], x[1], 56e9)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        out = pb.backpropagate(sig, cfg)
+    assert out.x.dtype == np.complex128 and len(out) == n_total and out.sample_rate == 56e9
+    want = _run(x.astype(np.complex64)[None], cfg)[0]
+    np.testing.assert_array_equal(out.stack(), want.astype(np.complex128))
