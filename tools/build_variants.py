@@ -61,6 +61,9 @@ VARIANTS = {
     "noload": ["-DDBP_EXPERIMENT_NOLOAD=1"],      # timing ceilings only: wrong results
     "nostore": ["-DDBP_EXPERIMENT_NOSTORE=1"],
     "nonl": ["-DDBP_EXPERIMENT_NONL=1"],
+    "notmastore": ["-DDBP_TMA_STORE=0"],
+    "tmastore10": ["-DDBP_TMA_STORE_MIN_LOGN=10"],
+    "tmaload": ["-DDBP_TMA_LOAD=1"],
     "noio": ["-DDBP_EXPERIMENT_NOLOAD=1", "-DDBP_EXPERIMENT_NOSTORE=1"],
 }
 if __name__ == "__main__":
