@@ -118,6 +118,9 @@ __host__ __device__ constexpr bool fixed_fir_nc(int nc) {
 #ifndef DBP_TMA_LOAD
 #define DBP_TMA_LOAD 0
 #endif
+#ifndef DBP_FFE_TMA_LOAD
+#define DBP_FFE_TMA_LOAD 1
+#endif
 // Output through the TMA bulk-copy engine (Geo::TMA_STORE): the kept centre is
 // staged in shared memory and written by two cp.async.bulk stores, so the
 // CTA retires as soon as the engine has read shared memory instead of
@@ -215,7 +218,10 @@ struct Geo {
       !DB && T >= 16 &&
       (DBP_SPLIT_WAR == 2 || (DBP_SPLIT_WAR == 1 && (LOGN == 8 || LOGN == 11 || LOGN == 12)));
   // one block per CTA and one group per CTA (no persistent loop): input by TMA
-  static constexpr bool TMA_LOAD = DBP_TMA_LOAD && BPC == 1 && LOGN >= 9 && LOGN <= 12;
+  // TMA block input: measured per program (profiles/r2/ab_tmaload.txt): the FFE-only
+  // instantiation +1.6% (N = 2048) / +7.8% (4096); the split-step programs -0.4..-0.5%
+  static constexpr bool TMA_LOAD_OK = BPC == 1 && LOGN >= 9 && LOGN <= 12;
+  static constexpr bool TMA_LOAD = DBP_TMA_LOAD && TMA_LOAD_OK;
   // kept centre through shared memory and one TMA bulk store per polarisation
   // (one block per CTA, non-persistent grid): see process_group
   static constexpr bool TMA_STORE = DBP_TMA_STORE && BPC == 1 && LOGN >= DBP_TMA_STORE_MIN_LOGN && LOGN < DBP_PERSIST_MIN_LOGN;
@@ -1282,7 +1288,8 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   float2 v[16];
   const long long s0 = b * kp.step - kp.lead;  // global index of block sample 0
   bool loaded = false;
-  if constexpr (G::TMA_LOAD) {
+  constexpr bool kTmaLoad = G::TMA_LOAD || (G::TMA_LOAD_OK && PROG == kProgFFE && DBP_FFE_TMA_LOAD);
+  if constexpr (kTmaLoad) {
     // Interior block, 16-byte aligned rows (uniform per CTA): one elected
     // thread copies both polarisation rows (2 x 8N bytes) into the planes
     // with the TMA bulk engine and every thread then reads its 16 samples
@@ -1369,7 +1376,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     // ESSFM / SSFM programs lose 0.1-1.8% to a moved barrier, a runtime op == 0
     // predicate that spills, or a peeled first operator:
     // profiles/r1/ab_fresh_start.txt).
-    constexpr bool kFresh = MODE == kShmSync && !G::TMA_LOAD && LOGN < DBP_PERSIST_MIN_LOGN;
+    constexpr bool kFresh = MODE == kShmSync && !kTmaLoad && LOGN < DBP_PERSIST_MIN_LOGN;
     conv_block<LOGN, MODE, kFresh, TWP>(v, sh, kp.tab_full, kp.twiddle, t);
   } else {
   const int n_ops = kp.n_ops;
@@ -1483,6 +1490,146 @@ dbp_block_kernel(const KernelParams kp) {
       process_group<LOGN, MODE, PROG, TWP>(kp, sh, grp, n_groups, t, slice, pol);
   } else {
     process_group<LOGN, MODE, PROG, TWP>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
+  }
+}
+
+}  // namespace dbp
+
+namespace dbp {
+
+// ---------------------------------------------------------------------------
+// FFE program (dbp.py:185-191) as a persistent, software-pipelined stream:
+// each CTA strides over the blocks, and while it transforms block i the TMA
+// engine already copies block i + gridDim.x into a dedicated shared buffer
+// (both polarisation rows, 2 N float2), so every SM keeps a block's input in
+// flight at all times -- the one-shot CTA of dbp_block_kernel<.., kProgFFE>
+// left the HBM idle while its CTAs computed (HBM fraction 0.6).  The output
+// leaves through the TMA bulk store (Geo::TMA_STORE path).  Blocks that are
+// not bulk-copyable (cyclic edge blocks, odd alignment) fall back to LDG / STG.
+// Measured slower and off by default (DBP_FFE_STREAM=1 selects it): 87.5 vs
+// 100.7 GS/s at 2048/700, 80.8 vs 97.2 at 4096/700 -- the input buffer costs
+// a CTA per SM (24 instead of 32 warps at N = 2048, 16 instead of 32 at 4096)
+// and the prefetch does not win it back (profiles/r2/ffe_stream.txt).
+// ---------------------------------------------------------------------------
+// resident CTAs per SM the stream kernel is built for: shared memory allows
+// three at N = 2048 (planes 37 KB + input buffer 32 KB each), one at 4096
+__host__ __device__ constexpr int ffe_stream_ctas(int logn) { return logn <= 11 ? 3 : 1; }
+
+template <int LOGN>
+__global__ void __launch_bounds__(Geo<LOGN>::THREADS, ffe_stream_ctas(LOGN)) dbp_ffe_stream_kernel(const KernelParams kp) {
+  using G = Geo<LOGN>;
+  static_assert(G::BPC == 1, "one block per CTA");
+  constexpr int N = G::N, T = G::T;
+  extern __shared__ float4 smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int pol = lane >> 4;
+  const int t = ((threadIdx.x >> 5) << 4) + (lane & 15);
+  constexpr int MODE = G::SPLIT_WAR ? kShmSplitWar : kShmSync;
+  Shm<LOGN, MODE> sh;
+  sh.init(reinterpret_cast<float*>(smem_raw), kp.slice_floats, pol);
+  float2* inbuf = reinterpret_cast<float2*>(reinterpret_cast<float*>(smem_raw) + kp.slice_floats);  // [2][N]
+  __shared__ alignas(8) uint64_t in_bar;
+  __shared__ alignas(8) uint64_t war_bar;
+  if (threadIdx.x == 0) {
+    mbar_init(&in_bar, 1);
+    if constexpr (MODE == kShmSplitWar) mbar_init(&war_bar, T / 16);
+  }
+  __syncthreads();
+  if constexpr (MODE == kShmSplitWar) {
+    sh.war = &war_bar;
+    sh.reads_done();
+  }
+  // block blk -> (item, b, source row of polarisation x), and whether the TMA may copy it
+  auto locate = [&](long long blk, long long& item, long long& b, const float2*& src) -> bool {
+    item = kp.bpi_magic ? (long long)__umul64hi(kp.bpi_magic, (unsigned long long)blk) : blk / kp.blocks_per_item;
+    b = kp.block_begin + (blk - item * kp.blocks_per_item);
+    const long long s0 = b * kp.step - kp.lead;
+    const long long off = kp.cyclic ? s0 : s0 - kp.in_origin;
+    src = kp.in + item * kp.in_item_stride + off;
+    const bool interior = !kp.cyclic || (s0 >= 0 && s0 + N <= kp.n_total);
+    return interior && ((reinterpret_cast<uintptr_t>(src) | (uintptr_t)(kp.in_pol_stride * 8)) & 15) == 0;
+  };
+  auto issue = [&](const float2* src) {
+    mbar_expect_tx(&in_bar, 2 * N * sizeof(float2));
+    bulk_load(inbuf, src, N * sizeof(float2), &in_bar);
+    bulk_load(inbuf + N, src + kp.in_pol_stride, N * sizeof(float2), &in_bar);
+  };
+  uint32_t in_phase = 0;
+  long long blk = blockIdx.x;
+  bool pending = false;
+  if (blk < kp.total_blocks) {
+    long long item, b;
+    const float2* src;
+    pending = locate(blk, item, b, src);
+    if (pending && threadIdx.x == 0) issue(src);
+  }
+  for (; blk < kp.total_blocks; blk += gridDim.x) {
+    long long item, b;
+    const float2* src;
+    locate(blk, item, b, src);
+    float2 v[16];
+    if (pending) {
+      mbar_wait(&in_bar, in_phase);
+      in_phase ^= 1u;
+      const float2* pl = inbuf + pol * N + t;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) v[m] = pl[m * T];
+    } else {
+      const float2* pin = kp.in + item * kp.in_item_stride + pol * kp.in_pol_stride;
+      const long long s0 = b * kp.step - kp.lead;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        long long gi = s0 + m * T + t;
+        if (kp.cyclic && (gi < 0 || gi >= kp.n_total)) {
+          gi %= kp.n_total;
+          if (gi < 0) gi += kp.n_total;
+        }
+        v[m] = ld_stream(pin + (kp.cyclic ? gi : gi - kp.in_origin));
+      }
+    }
+    // every thread holds its samples: the buffer may take the next block
+    __syncthreads();
+    pending = false;
+    const long long nxt = blk + gridDim.x;
+    if (nxt < kp.total_blocks) {
+      long long ni, nb;
+      const float2* nsrc;
+      pending = locate(nxt, ni, nb, nsrc);
+      if (pending && threadIdx.x == 0) issue(nsrc);
+    }
+    conv_block<LOGN, MODE, false, kTwDit>(v, sh, kp.tab_full, kp.twiddle, t);
+    // kept centre [lead, lead + len): TMA bulk store through the planes, else STG
+    const long long rem = kp.n_total - b * kp.step;
+    const int len = rem < kp.step ? (int)rem : kp.step;
+    const long long o0 = b * kp.step - kp.out_origin;
+    float2* row0 = kp.out + item * kp.out_item_stride + o0;
+    const bool bulk = ((kp.step | len) & 1) == 0 && (kp.out_pol_stride & 1) == 0 &&
+                      (reinterpret_cast<uintptr_t>(row0) & 15) == 0;
+    if (bulk) {
+      sh.before_write();
+      float2* stg = reinterpret_cast<float2*>(sh.base) + pol * kp.step - kp.lead;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int j = m * T + t;
+        if (j >= kp.lead && j < kp.lead + len) stg[j] = v[m];
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const float2* s = reinterpret_cast<const float2*>(sh.base);
+        bulk_store(row0, s, (uint32_t)len * 8u);
+        bulk_store(row0 + kp.out_pol_stride, s + kp.step, (uint32_t)len * 8u);
+        bulk_store_commit_and_wait_read();
+      }
+      sh.reads_done();   // warp 0 arrives once the engine has read the staging rows
+    } else {
+      float2* dst = kp.out + item * kp.out_item_stride + pol * kp.out_pol_stride + (o0 - kp.lead) + t;
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int j = m * T + t;
+        if (j >= kp.lead && j < kp.lead + len) __stcs(dst + m * T, v[m]);
+      }
+    }
   }
 }
 

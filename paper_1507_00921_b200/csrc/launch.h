@@ -95,9 +95,45 @@ auto select_block_kernel(const KernelParams& kp) {
   return kernel;
 }
 
+// FFE programs at these block lengths can run the persistent TMA-prefetching
+// stream kernel (dbp_ffe_stream_kernel, DBP_FFE_STREAM=1; measured slower)
+#ifndef DBP_FFE_STREAM_MIN_LOGN
+#define DBP_FFE_STREAM_MIN_LOGN 11
+#endif
+#ifndef DBP_FFE_STREAM_MAX_LOGN
+#define DBP_FFE_STREAM_MAX_LOGN 12
+#endif
+inline bool ffe_stream_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("DBP_FFE_STREAM");
+    return v && v[0] == '1';
+  }();
+  return on;
+}
+
+template <int LOGN>
+cudaError_t launch_ffe_stream(const KernelParams& kp, size_t smem_bytes, cudaStream_t stream) {
+  auto* kernel = dbp_ffe_stream_kernel<LOGN>;
+  const size_t smem = smem_bytes + (size_t)2 * Geo<LOGN>::N * sizeof(float2);
+  cudaError_t e = set_smem_attrs(kernel, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, Geo<LOGN>::THREADS, smem);
+  if (e != cudaSuccess) return e;
+  long long grid = (long long)sms * (per_sm > 0 ? per_sm : 1);
+  if (grid > kp.total_blocks) grid = kp.total_blocks;
+  kernel<<<dim3((unsigned)grid), dim3(Geo<LOGN>::THREADS), smem, stream>>>(kp);
+  return cudaGetLastError();
+}
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
+  if constexpr (LOGN >= DBP_FFE_STREAM_MIN_LOGN && LOGN <= DBP_FFE_STREAM_MAX_LOGN) {
+    if (kp.program == kFFE && ffe_stream_enabled()) return launch_ffe_stream<LOGN>(kp, smem_bytes, stream);
+  }
   auto* kernel = use_dit_fft(kp) ? select_block_kernel<LOGN, kTwDit>(kp)
                                  : select_block_kernel<LOGN, DBP_TW_POWERS>(kp);
   cudaError_t e = set_smem_attrs(kernel, smem_bytes);
