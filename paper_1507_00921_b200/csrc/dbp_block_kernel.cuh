@@ -1031,6 +1031,13 @@ __device__ __forceinline__ float2 p_fma(float2 a, float2 b, float2 c) {
 #ifndef DBP_FIR_DIRECT
 #define DBP_FIR_DIRECT 1
 #endif
+// packed direct form (FFMA2 on output pairs, bit-identical): measured -0.9% at
+// N_c = 17 and -1.8% at 33 (profiles/r2/ab_firpacked.txt) -- the FIR is
+// FMA-pipe bound, and FFMA2 needs every coefficient moved from a uniform
+// register into a regular one (~100 MOV per lane) -- so off
+#ifndef DBP_FIR_DIRECT_PACKED
+#define DBP_FIR_DIRECT_PACKED 0
+#endif
 // DIRECT: the streamed direct form (N >= 1024, where it lets the fixed-tap
 // kernel fit 64 registers); below, the folded symmetric form measured 0.2-1%
 // faster (profiles/r1/ab_v8.txt)
@@ -1046,6 +1053,44 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
   // are live -- the same 2 N_c + 1 FP instructions per output as the folded
   // symmetric form, ~40 fewer registers at N_c = 17.
   float fd[8];
+#if DBP_FIR_DIRECT_PACKED
+  // Packed: output pairs (f[2j], f[2j+1]) take window pairs (w[u], w[u+1])
+  // with ONE tap, d = u - 2j - PW, so each FFMA2 serves two outputs -- half the
+  // FIR instructions, the same FMA-pipe time, and the same per-output
+  // summation order (increasing u) as the scalar form: bit-identical.  Pairs
+  // at even u are a float4's (x, y) / (z, w); odd u pairs (y, z) and
+  // (previous w, x) are assembled with moves.
+  unsigned long long acc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) acc[j] = f2_pack(0.f, 0.f);
+  float prev_w = 0.f;
+#pragma unroll
+  for (int m = 0; m < W / 4; ++m) {
+    DBP_CHECK(fir_phys(p0 + 4 * m) + 3 < fir_phys(n_blk + 2 * PW) + 4);
+    const float4 q = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + 4 * m));
+    const unsigned long long pr[4] = {f2_pack(prev_w, q.x), f2_pack(q.x, q.y), f2_pack(q.y, q.z),
+                                      f2_pack(q.z, q.w)};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int u = 4 * m - 1 + k;          // first window index of pair k
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int d = u - 2 * j - PW;
+        if (u >= 0 && d >= -NC && d <= NC) {
+          const float c = kp.c[d < 0 ? -d : d];
+          acc[j] = f2_fma(f2_pack(c, c), pr[k], acc[j]);
+        }
+      }
+    }
+    prev_w = q.w;
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 f2 = f2_unpack(acc[j]);
+    fd[2 * j] = f2.x;
+    fd[2 * j + 1] = f2.y;
+  }
+#else
 #pragma unroll
   for (int o = 0; o < 8; ++o) fd[o] = 0.f;
 #pragma unroll
@@ -1062,6 +1107,7 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
       }
     }
   }
+#endif
   publish8(nlbuf, p0, fd, a, g, kp.precise_sincos);
   return;
   }

@@ -64,6 +64,7 @@ VARIANTS = {
     "notmastore": ["-DDBP_TMA_STORE=0"],
     "tmastore10": ["-DDBP_TMA_STORE_MIN_LOGN=10"],
     "tmaload": ["-DDBP_TMA_LOAD=1"],
+    "firpacked": ["-DDBP_FIR_DIRECT_PACKED=1"],
     "noio": ["-DDBP_EXPERIMENT_NOLOAD=1", "-DDBP_EXPERIMENT_NOSTORE=1"],
 }
 if __name__ == "__main__":
