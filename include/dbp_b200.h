@@ -132,6 +132,14 @@ int dbp_run_host(dbp_plan* plan, const void* h_in, void* h_out, int64_t n_total,
 int dbp_backpropagate_c128(dbp_plan* plan, const void* h_x, const void* h_y, void* h_out_x, void* h_out_y,
                            int64_t n_total);
 
+/* The nonlinear sub-step alone on one (2, n) block of ANY length n > 2 N_c
+ * (dbp.py:49-75 nonlinear_substep_essfm; channel.py:61-71 is N_c = 0, c = 1):
+ * float64 like the reference, cyclic FIR indices inside the block,
+ * h_out = h_block * exp(-j gamma dz_eff F).  Host complex128 (2, n) buffers;
+ * coeffs = c_0 .. c_{n_coeffs}.  Synchronous.                                */
+int dbp_nonlinear_substep_c128(int device, const void* h_block, void* h_out, int64_t n, double gamma,
+                               double dz_eff, const double* coeffs, int n_coeffs);
+
 /* Device staging budget (bytes) used by dbp_run_host (default 256 MiB: 32   
  * pipelined chunks for the configs[3] batch, so the un-overlapped first    
  * H2D and last D2H stay short).                                             */

@@ -38,6 +38,8 @@ SIGNATURES = {
     "dbp_run_host": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_int, _c_int64, _c_int64]),
     "dbp_plan_set_staging": (_c_int, [_c_void_p, ctypes.c_size_t]),
     "dbp_backpropagate_c128": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_int64]),
+    "dbp_nonlinear_substep_c128": (_c_int, [_c_int, _c_void_p, _c_void_p, _c_int64, ctypes.c_double,
+                                            ctypes.c_double, _c_double_p, _c_int]),
     "dbp_process_blocks": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_void_p]),
     "dbp_plan_synchronize": (_c_int, [_c_void_p]),
     "dbp_host_alloc": (_c_int, [ctypes.POINTER(_c_void_p), ctypes.c_size_t]),
@@ -468,7 +470,7 @@ def fit_normal(d_out: int, n_params: int, n_total: int, d_target: int, d_base: i
 
 
 def fft_c2c(x: np.ndarray, inverse: bool, device: int = 0) -> np.ndarray:
-    """Float64 DFT along the last axis on the GPU (cuFFT Z2Z); inverse scaled by 1/n."""
+    """Float64 DFT along the last axis on the GPU (own Stockham FFT, fft64.cuh); inverse scaled by 1/n."""
     a = np.ascontiguousarray(np.asarray(x, dtype=np.complex128))
     n = a.shape[-1]
     out = np.empty_like(a)
@@ -493,4 +495,17 @@ def phase_noise(x: np.ndarray, increments: np.ndarray, device: int = 0) -> np.nd
     out = np.empty_like(a)
     _check(load_library().dbp_phase_noise(int(device), a.ctypes.data, _dptr(inc), out.ctypes.data,
                                           int(a.shape[1])), "dbp_phase_noise")
+    return out
+
+
+def nonlinear_substep(block: np.ndarray, gamma: float, dz_eff: float, coeffs, device: int = 0) -> np.ndarray:
+    """(2, n) complex128 block * exp(-j gamma dz_eff F) on the GPU, any n > 2 N_c (float64)."""
+    a = np.ascontiguousarray(np.asarray(block, dtype=np.complex128))
+    c = np.ascontiguousarray(np.asarray(coeffs, dtype=np.float64))
+    if device_count() == 0:
+        raise RuntimeError("no CUDA device visible: the GPU sub-step has no CPU fallback")
+    out = np.empty_like(a)
+    _check(load_library().dbp_nonlinear_substep_c128(int(device), a.ctypes.data, out.ctypes.data, int(a.shape[1]),
+                                                     float(gamma), float(dz_eff), _dptr(c), int(c.size - 1)),
+           "dbp_nonlinear_substep_c128")
     return out

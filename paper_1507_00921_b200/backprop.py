@@ -113,6 +113,12 @@ def _dispersion(freqs: np.ndarray, beta2: float, length: float) -> np.ndarray:
     return np.exp(1j * 2.0 * np.pi ** 2 * (beta2 * 1e-24) * freqs ** 2 * length)
 
 
+def _own_plan(plan) -> OverlapPlan:
+    """This package's OverlapPlan for any object with the reference's fields
+    (the reference's own OverlapPlan has no block-range helpers)."""
+    return plan if isinstance(plan, OverlapPlan) else OverlapPlan(int(plan.block_len), int(plan.overlap))
+
+
 class DbpEngine:
     """One DBP configuration compiled onto one device (tables resident in HBM)."""
 
@@ -120,7 +126,7 @@ class DbpEngine:
         self.cfg = cfg
         self.sample_rate = float(sample_rate)
         self.device = int(device)
-        plan = cfg.plan
+        plan = self.plan = _own_plan(cfg.plan)
         n = plan.block_len
         if not (_native.MIN_BLOCK_LEN <= n <= _native.MAX_BLOCK_LEN):
             raise ValueError(f"block_len {n} outside the GPU-supported range "
@@ -147,7 +153,7 @@ class DbpEngine:
             self.schedule = sched
 
     def num_blocks(self, n_total: int) -> int:
-        return self.cfg.plan.num_blocks(n_total)
+        return self.plan.num_blocks(n_total)
 
     def run_host(self, samples: np.ndarray, out: np.ndarray | None = None,
                  block_range: tuple[int, int] | None = None) -> np.ndarray:
@@ -247,7 +253,7 @@ def backpropagate_batch(samples: np.ndarray, sample_rate: float, cfg: DbpConfig,
             if i1 > i0:
                 jobs.append((eng, x[i0:i1], out[i0:i1], None))
     else:
-        for (b0, b1), eng in zip(shard_blocks(cfg.plan.num_blocks(n), len(devs)), engines):
+        for (b0, b1), eng in zip(shard_blocks(_own_plan(cfg.plan).num_blocks(n), len(devs)), engines):
             if b1 > b0:
                 jobs.append((eng, x, None, (b0, b1)))
     results = []
@@ -256,7 +262,7 @@ def backpropagate_batch(samples: np.ndarray, sample_rate: float, cfg: DbpConfig,
         results = [f.result() for f in futs]
     for (eng, _, dst, rng), res in zip(jobs, results):
         if rng is not None:
-            lo, hi = cfg.plan.output_span(rng[0], rng[1], n)
+            lo, hi = _own_plan(cfg.plan).output_span(rng[0], rng[1], n)
             out[..., lo:hi] = res[..., lo:hi]
     return out
 
@@ -295,42 +301,26 @@ def backpropagate(sig: DualPolSignal, cfg: DbpConfig, jobs: int = 1, *,
 # sub-step mirrors (dbp.py:49-75, channel.py:61-71) on the GPU
 # ---------------------------------------------------------------------------
 
-_ROT_PLANS: dict = {}
-
-
-def _rotate_blocks(block: np.ndarray, gamma: float, dz_eff: float, c: np.ndarray,
-                   device: int = 0) -> np.ndarray:
+def _rotate_block(block, gamma: float, dz_eff: float, c: np.ndarray, device: int = 0) -> np.ndarray:
     blk = np.asarray(block)
     if blk.ndim != 2 or blk.shape[0] != 2:
         raise ValueError("expected a (2, n) dual-polarization block")
     n = blk.shape[1]
     if n <= 2 * (c.size - 1):
         raise ValueError(f"block length {n} too short for {c.size - 1} side coefficients")
-    if not (_native.MIN_BLOCK_LEN <= n <= _native.MAX_BLOCK_LEN) or (n & (n - 1)):
-        raise ValueError(f"GPU sub-step needs a power-of-two block in "
-                         f"[{_native.MIN_BLOCK_LEN}, {_native.MAX_BLOCK_LEN}], got {n}")
-    key = (device, n)
-    plan = _ROT_PLANS.get(key)
-    if plan is None:
-        plan = _native.NativePlan(device, n, 0)
-        _ROT_PLANS[key] = plan
-    with plan.lock:
-        plan.set_steps("rotate", "symmetric", [dz_eff], [1.0], gamma, c)
-        x = np.ascontiguousarray(blk.astype(np.complex64))[None]
-        out = np.zeros_like(x)
-        plan.run_host(x, out, n, 1, 0, 1)
-    return out[0].astype(np.complex128)
+    return _native.nonlinear_substep(blk, gamma, dz_eff, c, device)
 
 
 def nonlinear_substep_essfm(block, gamma: float, dz_eff: float, coeffs: EssfmCoefficients,
                             *, device: int = 0) -> np.ndarray:
-    """GPU ESSFM rotation of one (2, n) block, cyclic FIR inside the block (dbp.py:49-75)."""
-    return _rotate_blocks(block, gamma, dz_eff, np.asarray(coeffs.c, dtype=np.float64), device)
+    """GPU ESSFM rotation of one (2, n) block of any length n > 2 N_c, cyclic FIR inside
+    the block, float64 (dbp.py:49-75; dbp_nonlinear_substep_c128)."""
+    return _rotate_block(block, gamma, dz_eff, np.asarray(coeffs.c, dtype=np.float64), device)
 
 
 def nonlinear_substep_ssfm(block, gamma: float, dz_eff: float, *, device: int = 0) -> np.ndarray:
-    """GPU plain rotation exp(-j gamma dz_eff (|x|^2 + |y|^2)) (channel.py:61-71)."""
-    return _rotate_blocks(block, gamma, dz_eff, np.array([1.0]), device)
+    """GPU plain rotation exp(-j gamma dz_eff (|x|^2 + |y|^2)) (channel.py:61-71), any length."""
+    return _rotate_block(block, gamma, dz_eff, np.array([1.0]), device)
 
 
 class ProgramEngine:
@@ -339,7 +329,7 @@ class ProgramEngine:
     ``ifft(fft(b) * H)`` (an FFE program with table H), on one device."""
 
     def __init__(self, plan: OverlapPlan, sample_rate: float, device: int = 0, kernel=None):
-        self.plan = plan
+        plan = self.plan = _own_plan(plan)
         self.sample_rate = float(sample_rate)
         self.device = int(device)
         n = plan.block_len

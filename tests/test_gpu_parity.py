@@ -92,11 +92,28 @@ def test_ffe_is_linear(rng):
 
 @pytest.mark.parametrize("nc", [0, 1, 2, 4])
 def test_substep_matches_reference(golden, nc):
-    # test_dbp.py:47-57 geometry (N = 16); float32 so rel 2e-6 instead of 1e-14
+    # test_dbp.py:47-57 geometry (N = 16): the sub-step operator runs in float64
+    # (dbp_nonlinear_substep_c128), like the reference
     blk, c = golden[f"sub{nc}_in"], golden[f"sub{nc}_c"]
     got = pb.nonlinear_substep_essfm(blk, 1.7, 0.25, pb.EssfmCoefficients(c))
     want = golden[f"sub{nc}_out"]
-    np.testing.assert_allclose(got, want, rtol=0, atol=2e-6 * np.max(np.abs(want)))
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-13 * np.max(np.abs(want)))
+
+
+@pytest.mark.parametrize("n", [3, 37, 100, 1000, 6000])
+@pytest.mark.parametrize("nc", [0, 1, 17])
+def test_substep_any_length_matches_oracle(rng, n, nc):
+    # dbp.py:63-70 accepts any n > 2 N_c (not only powers of two)
+    if n <= 2 * nc:
+        with pytest.raises(ValueError, match="too short"):
+            pb.nonlinear_substep_essfm(np.ones((2, n), complex), 1.3, 1.0, pb.EssfmCoefficients.identity(nc))
+        return
+    blk = 0.05 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))
+    c = rng.normal(size=nc + 1) * 0.1
+    c[0] = 1.0
+    got = pb.nonlinear_substep_essfm(blk, -1.3, 800.0, pb.EssfmCoefficients(c))
+    want = dbp_port.rotate_essfm(blk, -1.3, 800.0, c)
+    assert rel_l2(got, want) < 1e-13
 
 
 def test_substep_ssfm_equals_identity_essfm(rng):
@@ -106,16 +123,24 @@ def test_substep_ssfm_equals_identity_essfm(rng):
     np.testing.assert_array_equal(a, b)
 
 
-@pytest.mark.parametrize("nc", [1, 3, 9, 17, 24, 32, 33, 64])
-def test_fir_paths_match_oracle(rng, nc):
-    n = 256 if nc <= 64 else 512
-    blk = 0.03 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))
+@pytest.mark.parametrize("n_blk", [256, 1024, 2048, 8192])
+@pytest.mark.parametrize("nc", [1, 3, 9, 13, 17, 24, 32, 33, 64])
+def test_fir_paths_match_oracle(rng, n_blk, nc):
+    # every intensity-FIR path of the block kernel inside the DBP program: the
+    # folded form (N <= 512), the streamed direct form (N >= 1024) for the
+    # compiled N_c in {1, 9, 17, 32, 33}, and fir8_generic (kProgGenericFir) for
+    # the others; random taps, strong nonlinearity (ESSFM N_s = 1 symmetric)
+    m = n_blk // 4
+    n = 3 * (n_blk - m) + 55
+    x = (0.03 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))).astype(np.complex64)
     c = rng.normal(size=nc + 1) * 0.1
     c[0] = 1.0
-    got = pb.nonlinear_substep_essfm(blk, -1.3, 800.0, pb.EssfmCoefficients(c))
-    want = dbp_port.rotate_essfm(blk.astype(np.complex64).astype(np.complex128), -1.3, 800.0, c)
-    # phases reach ~10 rad with 2 nc + 1 random taps: float32 phase error ~ 1e-7 * 10 rad
-    assert rel_l2(got, want) < 5e-6
+    span = pb.FiberParams(-21.0, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(n_blk, m), quiet_link(40, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(c))
+    got = _run(x[None], cfg)[0]
+    want = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(cfg))
+    assert dbp_port.per_block_rel_l2(got, want, n_blk, m).max() <= TOL_BLOCK
 
 
 def test_process_blocks_matches_captured_closure(golden, manifest):
