@@ -93,7 +93,10 @@ __host__ __device__ constexpr int nofir_threads_per_sm(int logn) {
   return logn == 11 ? 1024 : threads_per_sm(logn);
 #endif
 }
-enum KernelProg : int { kProgGeneric = 0, kProgFFE = 1, kProgNoFir = 2, kProgGenericFir = 3 };
+enum KernelProg : int { kProgGeneric = 0, kProgFFE = 1, kProgNoFir = 2, kProgGenericFir = 3, kProgSym1 = 4 };
+// kProgSym1: the configs[0] program -- symmetric, one nonlinear step, fixed-tap
+// FIR -- compiled as a straight line (L(K^1/2) R_0 L(K^1/2), dbp.py:214-223)
+// instead of the runtime operator loop: no program decode, the SFU sincos
 // N_c with a compiled fixed-tap FIR (fir8_fixed); anything else, and per-item
 // coefficient sets, run fir8_generic in the kProgGenericFir instantiation
 __host__ __device__ constexpr bool fixed_fir_nc(int nc) {
@@ -1292,7 +1295,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
       for (int m = 0; m < 16; ++m) fv[m] = nlbuf[fir_phys(m * T + t)];
     }
     sh.reads_done();
-    if (kp.precise_sincos) rotate_by_f<true>(v, fv, sg.x, sg.y);
+    if (PROG != kProgSym1 && kp.precise_sincos) rotate_by_f<true>(v, fv, sg.x, sg.y);
     else rotate_by_f<false>(v, fv, sg.x, sg.y);
 #else
     const float2* csbuf = reinterpret_cast<const float2*>(nlbuf);
@@ -1424,6 +1427,10 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     // profiles/r1/ab_fresh_start.txt).
     constexpr bool kFresh = MODE == kShmSync && !kTmaLoad && LOGN < DBP_PERSIST_MIN_LOGN;
     conv_block<LOGN, MODE, kFresh, TWP>(v, sh, kp.tab_full, kp.twiddle, t);
+  } else if constexpr (PROG == kProgSym1) {
+    conv_block<LOGN, MODE, false, TWP>(v, sh, kp.tab_half, kp.twiddle, t);
+    if constexpr (!DBP_EXPERIMENT_NONL) rotate<LOGN, MODE, PROG>(v, sh, kp, 0, t, pol, cptr);
+    conv_block<LOGN, MODE, false, TWP>(v, sh, kp.tab_half, kp.twiddle, t);
   } else {
   const int n_ops = kp.n_ops;
   for (int op = 0; op < n_ops; ++op) {

@@ -80,6 +80,14 @@ inline bool use_dit_fft(const KernelParams& kp) {
   return kp.program == kFFE || kp.n_steps <= DBP_DIT_MAX_STEPS;
 }
 
+// Block lengths whose configs[0]-shaped program (symmetric, N_s = 1, fixed-tap
+// FIR) runs the straight-line kProgSym1 instantiation.  Measured slower and
+// off (14 = none): the two inlined convolutions spill 80 bytes at 64
+// registers, -6% at N = 2048, -9% at 4096 (profiles/r2/ab_sym1.txt)
+#ifndef DBP_SYM1_KERNEL_MIN_LOGN
+#define DBP_SYM1_KERNEL_MIN_LOGN 14
+#endif
+
 template <int LOGN, int TWP>
 auto select_block_kernel(const KernelParams& kp) {
   auto* kernel = dbp_block_kernel<LOGN, kProgGeneric, TWP>;
@@ -92,6 +100,11 @@ auto select_block_kernel(const KernelParams& kp) {
   }
   if (kp.program != kFFE && kp.nc > 0 && (kp.coeff_stride != 0 || !fixed_fir_nc(kp.nc)))
     kernel = dbp_block_kernel<LOGN, kProgGenericFir, TWP>;
+  if constexpr (LOGN >= DBP_SYM1_KERNEL_MIN_LOGN) {
+    if ((kp.program == kSSFM || kp.program == kESSFM) && kp.arrangement == kSymmetric && kp.n_steps == 1 &&
+        kp.nc > 0 && kp.coeff_stride == 0 && fixed_fir_nc(kp.nc) && !kp.precise_sincos)
+      kernel = dbp_block_kernel<LOGN, kProgSym1, TWP>;
+  }
   return kernel;
 }
 

@@ -65,6 +65,8 @@ VARIANTS = {
     "tmastore10": ["-DDBP_TMA_STORE_MIN_LOGN=10"],
     "tmaload": ["-DDBP_TMA_LOAD=1"],
     "firpacked": ["-DDBP_FIR_DIRECT_PACKED=1"],
+    "nopersist": ["-DDBP_PERSIST_MIN_LOGN=14"],
+    "sym1": ["-DDBP_SYM1_KERNEL_MIN_LOGN=10"],
     "noio": ["-DDBP_EXPERIMENT_NOLOAD=1", "-DDBP_EXPERIMENT_NOSTORE=1"],
 }
 if __name__ == "__main__":
