@@ -980,25 +980,54 @@ __device__ __forceinline__ void store_factors8(float2* __restrict__ csbuf, int p
 }
 
 // What the FIR lanes publish for the rotation (DBP_NL_PUBLISH_F):
-//  1 (default): the filtered intensity F itself, 4 bytes per position at
-//    fir_phys(p) -- each lane then evaluates the (cos, sin) of its own 16
-//    positions (twice the SFU work, which has room) and the shared-memory
-//    traffic of the factor exchange halves: 2 STS.128 + 16 LDS.32 (24
-//    wavefronts per warp) instead of 4 STS.128 + 16 LDS.64 (48);
-//  0: the rotation factors (cos, sin) g, 8 bytes per position at cs_phys(p).
+//  1 (default): programs on the SFU sincos (<= 2 steps) publish the filtered
+//    intensity F itself, 4 bytes per position at fir_phys(p) -- each lane
+//    then evaluates the (cos, sin) of its own 16 positions (twice the SFU
+//    work, which has room) and the shared-memory traffic of the factor
+//    exchange halves: 2 STS.128 + 16 LDS.32 (24 wavefronts per warp) instead
+//    of 4 STS.128 + 16 LDS.64 (48).  Programs on the polynomial sincos
+//    (>= 3 steps) publish the factors: doubling ~15 FMA-pipe operations per
+//    factor cost N_s = 4 up to 6% (profiles/r2/final/configs_v10.jsonl);
+//  0: always the rotation factors (cos, sin) g, 8 bytes per position at cs_phys(p).
 #ifndef DBP_NL_PUBLISH_F
 #define DBP_NL_PUBLISH_F 1
 #endif
+// factors: publish (cos, sin) g (the polynomial-sincos programs of the
+// exact-adjoint instantiation), else F; precise: which sincos the factors use
 __device__ __forceinline__ void publish8(float* __restrict__ nlbuf, int p0, const float (&f)[8], float a, float g,
-                                         bool precise) {
+                                         bool precise, bool factors) {
 #if DBP_NL_PUBLISH_F
-  // p0 = 16 t + 8 pol: both float4 stay inside one 16-float pad group
-  float* dst = nlbuf + fir_phys(p0);
-  *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
-  *reinterpret_cast<float4*>(dst + 4) = make_float4(f[4], f[5], f[6], f[7]);
+  if (!factors) {
+    // p0 = 16 t + 8 pol: both float4 stay inside one 16-float pad group
+    float* dst = nlbuf + fir_phys(p0);
+    *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4*>(dst + 4) = make_float4(f[4], f[5], f[6], f[7]);
+    return;
+  }
+  store_factors8(reinterpret_cast<float2*>(nlbuf), p0, f, a, g, precise);
 #else
   store_factors8(reinterpret_cast<float2*>(nlbuf), p0, f, a, g, precise);
 #endif
+}
+
+// v[m] *= the published (cos, sin) g factor of position m T + t
+template <int LOGN, class SH>
+__device__ __forceinline__ void rotate_by_factors(float2 (&v)[16], const float* __restrict__ nlbuf, SH& sh, int t) {
+  constexpr int T = Geo<LOGN>::T;
+  const float2* csbuf = reinterpret_cast<const float2*>(nlbuf);
+  if constexpr (T >= 16) {
+    const float2* cb = csbuf + cs_phys(t);  // cs_phys(m T + t) = m (9T/8) + cs_phys(t)
+    float2 cs[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) cs[m] = cb[m * (9 * T / 8)];
+    sh.reads_done();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], cs[m]);
+  } else {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], csbuf[cs_phys(m * T + t)]);
+    sh.reads_done();
+  }
 }
 
 // v[m] *= (cos, sin)(a F_m) g for the 16 published F of this lane's positions
@@ -1046,7 +1075,8 @@ __device__ __forceinline__ float2 p_fma(float2 a, float2 b, float2 c) {
 // faster (profiles/r1/ab_v8.txt)
 template <int NC, bool DIRECT>
 __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float* __restrict__ nlbuf,
-                                           int p0, float a, float g, const KernelParams& kp, int n_blk) {
+                                           int p0, float a, float g, const KernelParams& kp, int n_blk,
+                                           bool factors) {
   constexpr int PW = (NC + 3) & ~3;
   constexpr int W = 8 + 2 * PW;
   if constexpr (DIRECT) {
@@ -1111,7 +1141,7 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
     }
   }
 #endif
-  publish8(nlbuf, p0, fd, a, g, kp.precise_sincos);
+  publish8(nlbuf, p0, fd, a, g, kp.precise_sincos, factors);
   return;
   }
   float w[W];
@@ -1158,14 +1188,14 @@ __device__ __forceinline__ void fir8_fixed(const float* __restrict__ ibuf, float
     f[o] = acc;
   }
 #endif
-  publish8(nlbuf, p0, f, a, g, kp.precise_sincos);
+  publish8(nlbuf, p0, f, a, g, kp.precise_sincos, factors);
 }
 
 // any nc (and per-item coefficient sets): taps in chunks of four, scalar
 // (summation order differs from the packed fir8_fixed at the last ulp)
 __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, float* __restrict__ nlbuf,
                                              int p0, int pw, float a, float g, const KernelParams& kp,
-                                             const float* __restrict__ cptr, float c0) {
+                                             const float* __restrict__ cptr, float c0, bool factors) {
   float f[8];
   {
     const float4 u = *reinterpret_cast<const float4*>(ibuf + fir_phys(p0 + pw));
@@ -1193,14 +1223,17 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
       for (int o = 0; o < 8; ++o) f[o] = fmaf(ci, l[o + 3 - d] + r[o + 1 + d], f[o]);
     }
   }
-  publish8(nlbuf, p0, f, a, g, kp.precise_sincos);
+  publish8(nlbuf, p0, f, a, g, kp.precise_sincos, factors);
 }
 
 // PROG (KernelProg): kProgNoFir compiles the F = c0 I path only; kProgGeneric
 // the fixed-tap FIRs; kProgGenericFir adds the runtime-N_c fir8_generic
-template <int LOGN, int MODE, int PROG = kProgGenericFir>
+template <int LOGN, int MODE, int PROG = kProgGenericFir, int TWP = kTwDit>
 __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, const KernelParams& kp,
                                        int step_idx, int t, int pol, const float* __restrict__ cptr) {
+  // the fused-twiddle instantiation runs <= 2-step programs (SFU sincos): F is
+  // published; the exact-adjoint one publishes factors for polynomial sincos
+  const bool factors = DBP_NL_PUBLISH_F == 0 || (TWP != kTwDit && PROG != kProgSym1 && kp.precise_sincos);
   // per-item coefficient sets (training batches) read from global memory
   const float c0 = kp.coeff_stride ? __ldg(cptr) : kp.c[0];
   using G = Geo<LOGN>;
@@ -1273,45 +1306,36 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
     const int p0 = 16 * t + 8 * pol;
     constexpr bool kDirectFir = DBP_FIR_DIRECT && LOGN >= 10;
     switch (kp.coeff_stride ? -1 : kp.nc) {
-      case 1: fir8_fixed<1, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
-      case 9: fir8_fixed<9, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
-      case 17: fir8_fixed<17, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
-      case 32: fir8_fixed<32, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
-      case 33: fir8_fixed<33, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N); break;
+      case 1: fir8_fixed<1, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N, factors); break;
+      case 9: fir8_fixed<9, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N, factors); break;
+      case 17: fir8_fixed<17, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N, factors); break;
+      case 32: fir8_fixed<32, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N, factors); break;
+      case 33: fir8_fixed<33, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N, factors); break;
       default:
-        if constexpr (PROG == kProgGenericFir) fir8_generic(ibuf, nlbuf, p0, pw, sg.x, sg.y, kp, cptr, c0);
+        if constexpr (PROG == kProgGenericFir) fir8_generic(ibuf, nlbuf, p0, pw, sg.x, sg.y, kp, cptr, c0, factors);
         else __trap();   // the launcher routes these programs to kProgGenericFir
         break;
     }
     sh.after_write();
 #if DBP_NL_PUBLISH_F
-    float fv[16];
-    if constexpr (T >= 16) {
-      const float* fb = nlbuf + fir_phys(t);  // fir_phys(m T + t) = m (5T/4) + fir_phys(t)
+    if (!factors) {
+      float fv[16];
+      if constexpr (T >= 16) {
+        const float* fb = nlbuf + fir_phys(t);  // fir_phys(m T + t) = m (5T/4) + fir_phys(t)
 #pragma unroll
-      for (int m = 0; m < 16; ++m) fv[m] = fb[m * (5 * T / 4)];
+        for (int m = 0; m < 16; ++m) fv[m] = fb[m * (5 * T / 4)];
+      } else {
+#pragma unroll
+        for (int m = 0; m < 16; ++m) fv[m] = nlbuf[fir_phys(m * T + t)];
+      }
+      sh.reads_done();
+      if (PROG != kProgSym1 && kp.precise_sincos) rotate_by_f<true>(v, fv, sg.x, sg.y);
+      else rotate_by_f<false>(v, fv, sg.x, sg.y);
     } else {
-#pragma unroll
-      for (int m = 0; m < 16; ++m) fv[m] = nlbuf[fir_phys(m * T + t)];
+      rotate_by_factors<LOGN>(v, nlbuf, sh, t);
     }
-    sh.reads_done();
-    if (PROG != kProgSym1 && kp.precise_sincos) rotate_by_f<true>(v, fv, sg.x, sg.y);
-    else rotate_by_f<false>(v, fv, sg.x, sg.y);
 #else
-    const float2* csbuf = reinterpret_cast<const float2*>(nlbuf);
-    if constexpr (T >= 16) {
-      const float2* cb = csbuf + cs_phys(t);  // cs_phys(m T + t) = m (9T/8) + cs_phys(t)
-      float2 cs[16];
-#pragma unroll
-      for (int m = 0; m < 16; ++m) cs[m] = cb[m * (9 * T / 8)];
-      sh.reads_done();
-#pragma unroll
-      for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], cs[m]);
-    } else {
-#pragma unroll
-      for (int m = 0; m < 16; ++m) v[m] = c_mul(v[m], csbuf[cs_phys(m * T + t)]);
-      sh.reads_done();
-    }
+    rotate_by_factors<LOGN>(v, nlbuf, sh, t);
 #endif
   }
 }
@@ -1429,7 +1453,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     conv_block<LOGN, MODE, kFresh, TWP>(v, sh, kp.tab_full, kp.twiddle, t);
   } else if constexpr (PROG == kProgSym1) {
     conv_block<LOGN, MODE, false, TWP>(v, sh, kp.tab_half, kp.twiddle, t);
-    if constexpr (!DBP_EXPERIMENT_NONL) rotate<LOGN, MODE, PROG>(v, sh, kp, 0, t, pol, cptr);
+    if constexpr (!DBP_EXPERIMENT_NONL) rotate<LOGN, MODE, PROG, TWP>(v, sh, kp, 0, t, pol, cptr);
     conv_block<LOGN, MODE, false, TWP>(v, sh, kp.tab_half, kp.twiddle, t);
   } else {
   const int n_ops = kp.n_ops;
@@ -1441,7 +1465,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
       conv_block<LOGN, MODE, false, TWP>(v, sh, tab, kp.twiddle, t);
     } else if (DBP_EXPERIMENT_NONL) {
     } else {
-      rotate<LOGN, MODE, PROG>(v, sh, kp, sidx, t, pol, cptr);
+      rotate<LOGN, MODE, PROG, TWP>(v, sh, kp, sidx, t, pol, cptr);
     }
   }
   }
