@@ -1233,7 +1233,8 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
                                        int step_idx, int t, int pol, const float* __restrict__ cptr) {
   // the fused-twiddle instantiation runs <= 2-step programs (SFU sincos): F is
   // published; the exact-adjoint one publishes factors for polynomial sincos
-  const bool factors = DBP_NL_PUBLISH_F == 0 || (TWP != kTwDit && PROG != kProgSym1 && kp.precise_sincos);
+  // (N = 8192, one CTA per SM: the factors measured +1.9%, profiles/r2/ab_pubf_8192.txt)
+  const bool factors = DBP_NL_PUBLISH_F == 0 || LOGN >= 13 || (TWP != kTwDit && PROG != kProgSym1 && kp.precise_sincos);
   // per-item coefficient sets (training batches) read from global memory
   const float c0 = kp.coeff_stride ? __ldg(cptr) : kp.c[0];
   using G = Geo<LOGN>;

@@ -70,6 +70,9 @@ LaunchShape launch_shape();
 // FFT flavour per program (DBP_DIT_MAX_STEPS): the fused-twiddle FFT for the
 // linear program and split-step programs of <= DBP_DIT_MAX_STEPS steps, the
 // exact-adjoint FFT above.  DBP_FFT=dit|adjoint (env) forces one (A/B runs).
+#ifndef DBP_DIT_MAX_LOGN
+#define DBP_DIT_MAX_LOGN 12
+#endif
 inline bool use_dit_fft(const KernelParams& kp) {
   static const int forced = [] {
     const char* v = std::getenv("DBP_FFT");
@@ -147,8 +150,9 @@ cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, s
   if constexpr (LOGN >= DBP_FFE_STREAM_MIN_LOGN && LOGN <= DBP_FFE_STREAM_MAX_LOGN) {
     if (kp.program == kFFE && ffe_stream_enabled()) return launch_ffe_stream<LOGN>(kp, smem_bytes, stream);
   }
-  auto* kernel = use_dit_fft(kp) ? select_block_kernel<LOGN, kTwDit>(kp)
-                                 : select_block_kernel<LOGN, DBP_TW_POWERS>(kp);
+  // N = 8192 keeps the exact-adjoint FFT: +1% there (profiles/r2/ab_dit_by_n.txt)
+  const bool dit = LOGN <= DBP_DIT_MAX_LOGN && use_dit_fft(kp);
+  auto* kernel = dit ? select_block_kernel<LOGN, kTwDit>(kp) : select_block_kernel<LOGN, DBP_TW_POWERS>(kp);
   cudaError_t e = set_smem_attrs(kernel, smem_bytes);
   if (e != cudaSuccess) return e;
   const LaunchShape sh = launch_shape<LOGN>();
