@@ -188,6 +188,14 @@ __host__ __device__ constexpr int pad256(int i) { return i + (i >> 8) * kTilePad
 // padded exchange plane (float2): pad256 for N >= 512, pad16 below
 __host__ __device__ constexpr int plane_elems(int n) { return n + (n >= 256 ? (n >> 8) * kTilePad : n / 16); }
 
+// DIT base tables: one float2 (the base b) per entry, or with
+// DBP_DIT_TABLED four (b, b^2, b^4, b^8, each rounded from float64), so the
+// butterflies use independently rounded powers instead of a squaring chain
+#ifndef DBP_DIT_TABLED
+#define DBP_DIT_TABLED 0
+#endif
+constexpr int kDitEntry = DBP_DIT_TABLED ? 4 : 1;
+
 template <int LOGN>
 struct Geo {
   static constexpr int N = 1 << LOGN;
@@ -257,13 +265,13 @@ struct Geo {
   }
   __host__ __device__ static constexpr int dit_fwd_offset(int p) {
     int off = tw_legacy_size();
-    for (int q = 1; q < p; ++q) off += dit_fwd_size(q);
+    for (int q = 1; q < p; ++q) off += kDitEntry * dit_fwd_size(q);
     return off;
   }
   __host__ __device__ static constexpr int dit_inv_size(int p) { return p == 0 ? N / R0 : (1 << log_s(p)); }
   __host__ __device__ static constexpr int dit_inv_offset(int p) {
     int off = dit_fwd_offset(NP);
-    for (int q = 0; q < p; ++q) off += dit_inv_size(q);
+    for (int q = 0; q < p; ++q) off += kDitEntry * dit_inv_size(q);
     return off;
   }
 };
@@ -324,7 +332,14 @@ inline std::vector<float2> make_twiddles(int logn) {
     }
   }
   if (tw.empty()) tw.push_back(make_float2(1.f, 0.f));
-  // decimation-in-time bases (Geo::dit_fwd_offset / dit_inv_offset)
+  // decimation-in-time bases (Geo::dit_fwd_offset / dit_inv_offset): per
+  // index b = W^k (kDitEntry == 1) or (b, b^2, b^4, b^8) (kDitEntry == 4)
+  auto entry = [&](long long k, long long period, double sign) {
+    for (int e = 0; e < kDitEntry; ++e) {
+      const long long kk = (k << e) % period;   // b^(2^e)
+      tw.push_back(unit_float2(sign * 2.0 * M_PI * (double)kk / (double)period));
+    }
+  };
   if (np > 1) {
     const long long tt = n / 16;
     for (int p = 1; p < np; ++p) {
@@ -332,15 +347,15 @@ inline std::vector<float2> make_twiddles(int logn) {
       if (p == np - 1) {
         for (long long t = 0; t < tt; ++t) {
           const long long k = np >= 3 ? (t >> 4) + (n / 256) * (t & 15) : t;
-          tw.push_back(w(k, period));
+          entry(k, period, -1.0);
         }
       } else {
-        for (long long k = 0; k < size; ++k) tw.push_back(w(k, period));
+        for (long long k = 0; k < size; ++k) entry(k, period, -1.0);
       }
     }
     for (int p = 0; p < np - 1; ++p) {
       const long long period = p == 0 ? n : n >> (logr0 + 4 * p - 4), size = p == 0 ? n / r0 : period / 16;
-      for (long long k = 0; k < size; ++k) tw.push_back(unit_float2(2.0 * M_PI * (double)k / (double)period));
+      for (long long k = 0; k < size; ++k) entry(k, period, +1.0);
     }
   }
   return tw;
@@ -651,9 +666,22 @@ __device__ __forceinline__ void apply_table_df(float2 (&v)[16], const float2* __
 // instructions per twiddled radix-16 pass, and the radix-R0 forward pass
 // carries none (v9).  TWP == 0 (the link simulator) keeps the table-twiddle
 // decimation-in-frequency forward, whose magnitude error does not compound.
-__device__ __forceinline__ float2 dit_base(const float2* __restrict__ tw, int off, int idx) {
+#if DBP_DIT_TABLED
+using DitBase = TwPow;
+__device__ __forceinline__ DitBase dit_base(const float2* __restrict__ tw, int off, int idx) {
+  DitBase r;
+  ldg_table_pair(tw + off + 4 * idx, r.b, r.b2);
+  ldg_table_pair(tw + off + 4 * idx + 2, r.b4, r.b8);
+  return r;
+}
+__device__ __forceinline__ DitBase dit_zero() { return DitBase{}; }
+#else
+using DitBase = float2;
+__device__ __forceinline__ DitBase dit_base(const float2* __restrict__ tw, int off, int idx) {
   return ldg_table(tw + off + idx);
 }
+__device__ __forceinline__ DitBase dit_zero() { return make_float2(0.f, 0.f); }
+#endif
 
 // ---------------------------------------------------------------------------
 // Block FFT on one polarisation: fft_fwd walks the decimation-in-frequency
@@ -669,7 +697,7 @@ __device__ __forceinline__ float2 dit_base(const float2* __restrict__ tw, int of
 // behind the exchange's barrier instead of stalling the pass
 template <int LOGN, int P, int TWP = kTwDit, int MODE = kShmSync, bool CALLER_WAR = false>
 __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, const float2* __restrict__ tw,
-                                        int t, float2 pb = make_float2(0.f, 0.f)) {
+                                        int t, DitBase pb = dit_zero()) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T, NP = G::NP;
   if constexpr (NP == 1) {
@@ -689,7 +717,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     }
     // exchange into the pass-1 layout
     constexpr int LS1 = G::log_s(1);
-    float2 nb = make_float2(0.f, 0.f);
+    DitBase nb = dit_zero();
     if constexpr (TWP == kTwDit) nb = dit_base(tw, G::dit_fwd_offset(1), t >> LS1);
     // CALLER_WAR: the caller omits this exchange's write-after-read barrier
     // (the FFE kernel's single convolution in a CTA that has not read shared
@@ -743,7 +771,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     } else {
       dft_tw<16, false>(v, pb);
     }
-    float2 nb = make_float2(0.f, 0.f);
+    DitBase nb = dit_zero();
     if constexpr (TWP == kTwDit) nb = dit_base(tw, G::dit_fwd_offset(NP - 1), t);
     float2* tile = sh.template plane<(NP - 2) & 1>() + kTileLen * (t >> 4);
     const int l = t & 15;
@@ -770,7 +798,7 @@ __device__ __forceinline__ void fft_fwd(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     } else {
       dft_tw<16, false>(v, pb);
     }
-    float2 nb = make_float2(0.f, 0.f);
+    DitBase nb = dit_zero();
     if constexpr (TWP == kTwDit) nb = dit_base(tw, G::dit_fwd_offset(P + 1), t >> LS1);
     sh.before_write();
     {
@@ -813,7 +841,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     fft_inv<LOGN, 1, TWP>(v, sh, tw, t);
     // this pass's input-twiddle bases, loaded ahead of the exchange (G0 <= 2)
     constexpr bool kPre = TWP == kTwDit && G0 <= 2;
-    float2 pre[kPre ? G0 : 1];
+    DitBase pre[kPre ? G0 : 1];
     if constexpr (kPre) {
 #pragma unroll
       for (int q = 0; q < G0; ++q) pre[q] = dit_base(tw, G::dit_inv_offset(0), t + T * q);
@@ -858,7 +886,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
     }
   } else if constexpr (NP >= 3 && P == NP - 2) {
     dft<16, true>(v);  // last pass
-    float2 pb = make_float2(0.f, 0.f);
+    DitBase pb = dit_zero();
     if constexpr (TWP == kTwDit) pb = dit_base(tw, G::dit_inv_offset(P), t & 15);
     float2* tile = sh.template plane<(NP - 2) & 1>() + kTileLen * (t >> 4);
     const int l = t & 15;
@@ -883,7 +911,7 @@ __device__ __forceinline__ void fft_inv(float2 (&v)[16], Shm<LOGN, MODE>& sh, co
   } else if constexpr (P < NP - 1) {
     constexpr int LS = G::log_s(P), S = 1 << LS, LS1 = G::log_s(P + 1);
     fft_inv<LOGN, P + 1, TWP>(v, sh, tw, t);
-    float2 pb = make_float2(0.f, 0.f);
+    DitBase pb = dit_zero();
     if constexpr (TWP == kTwDit) pb = dit_base(tw, G::dit_inv_offset(P), t & (S - 1));
     sh.before_write();
     {

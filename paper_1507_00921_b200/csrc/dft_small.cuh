@@ -245,21 +245,29 @@ __device__ __forceinline__ void tw_dft4(float2& a0, float2& a1, float2& a2, floa
   pm_rt(e0m, e1m, c_rot90<INV>(g), a1, a3);
 }
 
+// a twiddle base with its first powers (DIT tables with DBP_DIT_TABLED)
+struct TwPow {
+  float2 b, b2, b4, b8;
+};
+
 template <bool INV>
 __device__ __forceinline__ void dft2_tw(float2* v, float2 b) {
   pm_rt(v[0], v[1], b, v[0], v[1]);
 }
 
 template <bool INV>
+__device__ __forceinline__ void dft4_tw_p(float2* v, float2 b, float2 b2) {
+  tw_dft4<INV>(v[0], v[1], v[2], v[3], b, b2);
+}
+template <bool INV>
 __device__ __forceinline__ void dft4_tw(float2* v, float2 b) {
-  tw_dft4<INV>(v[0], v[1], v[2], v[3], b, c_sq(b));
+  dft4_tw_p<INV>(v, b, c_sq(b));
 }
 
 // 8 = 2 x 4: n = 4 n1 + n2, k = k1 + 2 k2; stage 1 weights b^{4 n1}, stage 2
 // bases W_8^{k1} b
 template <bool INV>
-__device__ __forceinline__ void dft8_tw(float2* v, float2 b) {
-  const float2 b2 = c_sq(b), b4 = c_sq(b2);
+__device__ __forceinline__ void dft8_tw_p(float2* v, float2 b, float2 b2, float2 b4) {
   float2 y[8];
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) pm_rt(v[n2], v[n2 + 4], b4, y[n2], y[n2 + 4]);   // k1 = 0 | 1
@@ -271,12 +279,16 @@ __device__ __forceinline__ void dft8_tw(float2* v, float2 b) {
     v[2 * k2 + 1] = y[4 + k2];
   }
 }
+template <bool INV>
+__device__ __forceinline__ void dft8_tw(float2* v, float2 b) {
+  const float2 b2 = c_sq(b), b4 = c_sq(b2);
+  dft8_tw_p<INV>(v, b, b2, b4);
+}
 
 // 16 = 4 x 4: n = 4 n1 + n2, k = k1 + 4 k2; stage 1 (over n1) base b^4, stage 2
 // (over n2, row k1) base W_16^{k1} b
 template <bool INV>
-__device__ __forceinline__ void dft16_tw(float2* v, float2 b) {
-  const float2 b2 = c_sq(b), b4 = c_sq(b2), b8 = c_sq(b4);
+__device__ __forceinline__ void dft16_tw_p(float2* v, float2 b, float2 b2, float2 b4, float2 b8) {
 #pragma unroll
   for (int n2 = 0; n2 < 4; ++n2) tw_dft4<INV>(v[n2], v[4 + n2], v[8 + n2], v[12 + n2], b4, b8);
   // v[4 k1 + n2] holds Y[n2][k1]
@@ -292,6 +304,27 @@ __device__ __forceinline__ void dft16_tw(float2* v, float2 b) {
     for (int k2 = 0; k2 < 4; ++k2) x[k1 + 4 * k2] = v[4 * k1 + k2];
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = x[i];
+}
+template <bool INV>
+__device__ __forceinline__ void dft16_tw(float2* v, float2 b) {
+  const float2 b2 = c_sq(b), b4 = c_sq(b2), b8 = c_sq(b4);
+  dft16_tw_p<INV>(v, b, b2, b4, b8);
+}
+
+// the same DFTs from a tabled base with its powers
+template <int R, bool INV>
+__device__ __forceinline__ void dft_tw(float2* v, const TwPow& p) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2) {
+    dft2_tw<INV>(v, p.b);
+  } else if constexpr (R == 4) {
+    dft4_tw_p<INV>(v, p.b, p.b2);
+  } else if constexpr (R == 8) {
+    dft8_tw_p<INV>(v, p.b, p.b2, p.b4);
+  } else {
+    static_assert(R == 16, "radix must be 1, 2, 4, 8 or 16");
+    dft16_tw_p<INV>(v, p.b, p.b2, p.b4, p.b8);
+  }
 }
 
 template <int R, bool INV>

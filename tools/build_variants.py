@@ -67,6 +67,8 @@ VARIANTS = {
     "firpacked": ["-DDBP_FIR_DIRECT_PACKED=1"],
     "nopersist": ["-DDBP_PERSIST_MIN_LOGN=14"],
     "sym1": ["-DDBP_SYM1_KERNEL_MIN_LOGN=10"],
+    "dittab": ["-DDBP_DIT_TABLED=1"],
+    "dittab_all": ["-DDBP_DIT_TABLED=1", "-DDBP_DIT_MAX_STEPS=1000", "-DDBP_DIT_MAX_LOGN=13"],
     "noio": ["-DDBP_EXPERIMENT_NOLOAD=1", "-DDBP_EXPERIMENT_NOSTORE=1"],
 }
 if __name__ == "__main__":
