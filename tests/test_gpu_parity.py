@@ -502,3 +502,25 @@ def test_dropin_complex128_path_bit_equal(rng, n_total):
     assert out.x.dtype == np.complex128 and len(out) == n_total and out.sample_rate == 56e9
     want = _run(x.astype(np.complex64)[None], cfg)[0]
     np.testing.assert_array_equal(out.stack(), want.astype(np.complex128))
+
+
+def test_failed_reconfiguration_leaves_the_plan_intact(rng):
+    # a rejected dbp_plan_set_steps / set_linear must not leave a
+    # half-updated plan (new program with the old schedule, new K with old K^1/2)
+    span = pb.FiberParams(-21.6826, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(1024, 256), quiet_link(10, span), num_steps=2,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(9)))
+    eng = pb.DbpEngine(cfg, 56e9, 0)
+    x = (0.02 * (rng.normal(size=(1, 2, 5000)) + 1j * rng.normal(size=(1, 2, 5000)))).astype(np.complex64)
+    before = eng.run_host(x)
+    sched = eng.schedule
+    bad = np.full(10, np.nan)
+    with pytest.raises(ValueError, match="finite"):
+        eng.native.set_steps("essfm", "linear-first", [w for _, w, _ in sched], [g for _, _, g in sched],
+                             -1.3, bad)
+    with pytest.raises(ValueError, match="finite"):
+        eng.native.set_steps("ssfm", "symmetric", [np.nan] * 2, [1.0, 1.0], -1.3)
+    with pytest.raises(ValueError, match="finite"):
+        eng.native.set_linear(np.full(1024, np.nan + 0j), np.ones(1024, complex))
+    np.testing.assert_array_equal(eng.run_host(x), before)
+    eng.close()
