@@ -105,6 +105,15 @@ def work_per_sample(a, gains_not_one: bool = False) -> tuple[float, float]:
     return flops / (n - m), 16.0 * (2 * n - m) / (n - m)
 
 
+def kernel_twp(a) -> int:
+    """The FFT flavour the launcher picks (csrc/launch.h): 4 = fused-twiddle
+    decimation in time (FFE and programs of <= 2 steps, N <= 4096), 3 = the
+    exact-adjoint FFT."""
+    import math as _m
+    steps = 0 if a.algorithm == "ffe" else a.num_steps
+    return 4 if (a.algorithm == "ffe" or steps <= 2) and int(_m.log2(a.block_len)) <= 12 else 3
+
+
 def kernel_prog(a) -> int:
     """Which instantiation of the block kernel the launcher picks (csrc/launch.h
     launch_block_kernel_impl): 0 generic (fixed-tap FIR), 1 FFE-only, 2 no-FIR
@@ -400,7 +409,8 @@ def run_ours(a) -> int:
                          "flops_per_sample": f_s, "traffic": traffic, "traffic_unit": "bytes per launch",
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": b_s * per_launch_samples,
-                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}, {kernel_prog(a)}>"},
+                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}, {kernel_prog(a)}, "
+                                   f"{kernel_twp(a)}>"},
             "roofline_hbm": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved_gbs / hbm_peak, "bytes_per_sample": b_s,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
