@@ -118,7 +118,7 @@ struct dbp_plan {
   void* h_pin[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   size_t pin_bytes = 0;
   cudaEvent_t done[2] = {nullptr, nullptr};
-  dbp::HostPool* pool = nullptr;
+  dbp::HostPool* pool = nullptr;   // the process-wide conversion pool (not owned)
 };
 
 namespace {
@@ -303,7 +303,6 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
 int dbp_plan_destroy(dbp_plan* p) {
   if (!p) return DBP_OK;
   DeviceGuard g(p->device);
-  delete p->pool;
   for (int s = 0; s < 2; ++s) {
     if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
     for (int k = 0; k < 2; ++k)
@@ -643,6 +642,19 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
 
 namespace {
 
+// one host conversion pool for the process (DBP_HOST_THREADS threads, default
+// min(16, cores)), shared by every plan: idle threads are not multiplied by
+// the number of cached plans
+dbp::HostPool* shared_host_pool() {
+  static dbp::HostPool pool([] {
+    const char* v = std::getenv("DBP_HOST_THREADS");
+    const int env = v ? std::atoi(v) : 0;
+    const unsigned hc = std::thread::hardware_concurrency();
+    return env > 0 ? env : (int)std::min(16u, hc ? hc : 1u);
+  }());
+  return &pool;
+}
+
 int ensure_pinned(dbp_plan* p, size_t bytes) {
   if (p->pin_bytes >= bytes) return DBP_OK;
   for (int s = 0; s < 2; ++s)
@@ -658,16 +670,7 @@ int ensure_pinned(dbp_plan* p, size_t bytes) {
   p->pin_bytes = bytes;
   for (int s = 0; s < 2; ++s)
     if (!p->done[s]) DBP_CUDA(cudaEventCreateWithFlags(&p->done[s], cudaEventDisableTiming), "cudaEventCreate");
-  if (!p->pool) {
-    const unsigned hc = std::thread::hardware_concurrency();
-    static const int env_threads = [] {
-      const char* v = std::getenv("DBP_HOST_THREADS");
-      return v ? std::atoi(v) : 0;
-    }();
-    int t = env_threads > 0 ? env_threads : (int)std::min(16u, hc ? hc : 1u);
-    p->pool = new (std::nothrow) dbp::HostPool(std::max(1, t));
-    if (!p->pool) return fail(DBP_ENOMEM, "host thread pool");
-  }
+  if (!p->pool) p->pool = shared_host_pool();
   return DBP_OK;
 }
 

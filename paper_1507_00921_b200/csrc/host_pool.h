@@ -30,12 +30,15 @@ class HostPool {
   }
   int size() const { return n_; }
   // fn(lo, hi) over [0, count) split into size() contiguous pieces; the
-  // calling thread runs piece 0; returns when every piece is done
+  // calling thread runs piece 0; returns when every piece is done.  Callers
+  // on different threads (plans on different devices sharing the pool) are
+  // serialised.
   void parallel_for(long long count, const std::function<void(long long, long long)>& fn) {
     if (n_ == 1 || count < 4096) {
       fn(0, count);
       return;
     }
+    std::lock_guard<std::mutex> call(call_mu_);
     {
       std::lock_guard<std::mutex> g(mu_);
       fn_ = &fn;
@@ -73,6 +76,7 @@ class HostPool {
     }
   }
   std::vector<std::thread> workers_;
+  std::mutex call_mu_;
   std::mutex mu_;
   std::condition_variable cv_, done_cv_;
   const std::function<void(long long, long long)>* fn_ = nullptr;
