@@ -183,7 +183,11 @@ int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
   const dbp::LaunchShape sh = d.shape[p->logn]();
   const long long ctas = (kp.total_blocks + sh.slices - 1) / sh.slices;
   if (ctas > 0x7fffffffLL) return fail(DBP_EINVAL, "too many blocks for one launch");
-  const size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices;
+#ifndef DBP_EXPERIMENT_MIN_SMEM
+#define DBP_EXPERIMENT_MIN_SMEM 0   // timing experiment: pad the CTA's shared memory (bytes) to cap CTAs per SM
+#endif
+  size_t smem = (size_t)kp.slice_floats * sizeof(float) * sh.slices;
+  if (smem < (size_t)DBP_EXPERIMENT_MIN_SMEM) smem = DBP_EXPERIMENT_MIN_SMEM;
   if (smem > 227 * 1024) return fail(DBP_EINVAL, "shared memory per CTA exceeds 227 KB for this block length");
   // Persistent grid (SMs x resident CTAs, each looping over block groups with
   // an L2 prefetch of the next): only N = 8192 (one 1024-thread CTA per SM)
