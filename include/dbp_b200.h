@@ -283,7 +283,8 @@ int dbp_fit_normal(const void* d_out, int n_params, int64_t n_total, const void*
 
 /* Float64 DFT along the last axis of a [batch][n] complex128 host array
  * (spectral.py:37-48: forward unnormalised, inverse x 1/n; n a power of two),
- * a cuFFT Z2Z library transform -- API completeness, not the DBP path.       */
+ * the library's own float64 Stockham FFT (csrc/fft64.cuh) -- API
+ * completeness, not the DBP path.                                           */
 int dbp_fft_c2c(int device, const void* h_in, void* h_out, int64_t n, int64_t batch, int inverse);
 
 /* Laser phase noise (channel.py:156-171): out = in exp(j cumsum(incr)) for a

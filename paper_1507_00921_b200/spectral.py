@@ -1,6 +1,7 @@
 """Alias module: ``fiberdbp.spectral`` names (pkg/src/fiberdbp/spectral.py) on the GPU.
 
-``fft`` / ``ifft`` are float64 cuFFT transforms (``dbp_fft_c2c``) with the
+``fft`` / ``ifft`` are float64 transforms on the library's own Stockham FFT
+(``dbp_fft_c2c``, csrc/fft64.cuh) with the
 reference's power-of-two check; ``overlap_save_run`` runs GPU block
 processors (``block_processor(cfg, sample_rate)``) through the fused kernel.
 """
