@@ -91,17 +91,19 @@ def _q_aligned(soft, tx_symbols):
     return 20.0 * math.log10(math.sqrt(2.0) * float(erfcinv(2.0 * ber)))
 
 
-def _decision_flips(soft_gpu, soft_ref):
-    """(flips, unexplained): decisions that differ, and those of them whose
-    float64 soft value is farther from the threshold than 3x the GPU-oracle
-    difference of that very symbol (a flip of a decision sitting within the
-    numerical difference of the boundary is the tolerance at work, not an error)."""
+def _decision_flips(soft_gpu, soft_ref, boundary=1e-4):
+    """(flips, unexplained): decisions that differ, and those of them that are
+    NOT boundary symbols -- a flip is the tolerance at work only when the
+    float64 soft value lies within ``boundary`` of the threshold (symbols are
+    normalised to unit power, so 1e-4 is ~50x the per-symbol GPU-oracle
+    difference at a 2e-6 block error) and the GPU value differs from it by
+    less than that too."""
     flips = unexplained = 0
     for part in (np.real, np.imag):
         g, r = part(soft_gpu), part(soft_ref)
         f = (g < 0.0) != (r < 0.0)
         flips += int(np.sum(f))
-        unexplained += int(np.sum(f & (np.abs(r) > 3.0 * np.abs(g - r) + 1e-12)))
+        unexplained += int(np.sum(f & ((np.abs(r) > boundary) | (np.abs(g - r) > boundary))))
     return flips, unexplained
 
 
@@ -160,8 +162,8 @@ def test_config2_full_size_power_sweep(config2_links, n_blk, m):
     # 2^22 hard decisions per power: with a per-block rel-L2 of ~2e-6 and the
     # OSNR-14 symbol cloud, ~1 decision per power sits within the numerical
     # difference of its threshold (measured: 0-1 per power).  Every flip must be
-    # such a boundary symbol (_decision_flips), and there may be at most 4 per
-    # power; Q must agree within 0.02 dB.
+    # such a boundary symbol (|soft value| and |GPU - oracle| both < 1e-4,
+    # _decision_flips), at most 4 per power; Q must agree within 0.02 dB.
     for i, p in enumerate(powers):
         err = dbp_port.per_block_rel_l2(got[i], want[i], n_blk, m)
         assert err.max() <= TOL_BLOCK, (p, err.max())
