@@ -1372,6 +1372,13 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
 // ---------------------------------------------------------------------------
 // the kernel
 // ---------------------------------------------------------------------------
+// Programs whose interior blocks arrive through the exchange planes (TMA bulk
+// load): one block per CTA, so this never meets the persistent loop.
+template <int LOGN, int PROG>
+__device__ __host__ constexpr bool tma_load_program() {
+  return Geo<LOGN>::TMA_LOAD || (Geo<LOGN>::TMA_LOAD_OK && PROG == kProgFFE && DBP_FFE_TMA_LOAD);
+}
+
 // One CTA-sized group of blocks (block slices) through the whole program.
 template <int LOGN, int MODE, int PROG, int TWP>
 __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, MODE>& sh, long long grp,
@@ -1390,13 +1397,18 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
   float2 v[16];
   const long long s0 = b * kp.step - kp.lead;  // global index of block sample 0
   bool loaded = false;
-  constexpr bool kTmaLoad = G::TMA_LOAD || (G::TMA_LOAD_OK && PROG == kProgFFE && DBP_FFE_TMA_LOAD);
+  constexpr bool kTmaLoad = tma_load_program<LOGN, PROG>();
+  static_assert(!kTmaLoad || LOGN < DBP_PERSIST_MIN_LOGN, "TMA block input assumes one group per CTA");
   if constexpr (kTmaLoad) {
     // Interior block, 16-byte aligned rows (uniform per CTA): one elected
     // thread copies both polarisation rows (2 x 8N bytes) into the planes
     // with the TMA bulk engine and every thread then reads its 16 samples
-    // from shared memory (conflict free; the first exchange's leading
-    // barrier orders these reads before the planes are overwritten).  The
+    // from shared memory (conflict free).  The first exchange's leading
+    // barrier orders these reads before the planes are overwritten: with
+    // __syncthreads (kShmSync) directly, with split write-after-read barriers
+    // because each warp's initial arrival is made after its reads below and
+    // not at kernel start (an arrival at kernel start let a fast warp write
+    // its first exchange over rows a slow warp had not read yet).  The
     // LDG path would stage 32 KB per CTA in flight through L1, whose
     // capacity (the unified L1 / shared array) measurably limits the kernel.
     __shared__ alignas(8) uint64_t in_bar;
@@ -1450,6 +1462,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
 #pragma unroll
     for (int m = 0; m < 16; ++m) v[m] = make_float2(0.f, 0.f);
   }
+  if constexpr (kTmaLoad && MODE == kShmSplitWar) sh.reads_done();  // the deferred initial arrival
   if (grp + gridDim.x < n_groups) {
     // L2 prefetch of the next group's block: one 128-byte line per thread and polarisation
     const long long nblk = (grp + gridDim.x) * G::BPC + slice;
@@ -1583,7 +1596,9 @@ dbp_block_kernel(const KernelParams kp) {
     if (threadIdx.x < G::BPC) mbar_init(&war_bars[threadIdx.x], T / 16);
     __syncthreads();
     sh.war = &war_bars[slice];
-    sh.reads_done();   // nothing to protect before the first write phase
+    // nothing to protect before the first write phase -- unless the block
+    // input arrives through the planes (TMA load): process_group arrives then
+    if constexpr (!tma_load_program<LOGN, PROG>()) sh.reads_done();
   }
 
   // N <= 4096: one group per CTA (full-size grid).  N = 8192: a persistent
