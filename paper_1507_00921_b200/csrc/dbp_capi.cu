@@ -98,6 +98,8 @@ struct dbp_plan {
   float2* d_full = nullptr;
   float2* d_half = nullptr;
   float2* d_tw = nullptr;
+  float2* d_wtw = nullptr;   // warp FFE kernel bases (N = 1024 .. 4096)
+  float2* d_full_nat = nullptr;   // the full-step filter in natural bin order (warp FFE kernel)
   float2* d_steps = nullptr;
   int steps_cap = 0;
   float* d_coeff = nullptr;
@@ -172,6 +174,8 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   kp.tab_full = p->d_full;
   kp.tab_half = p->d_half ? p->d_half : p->d_full;
   kp.twiddle = p->d_tw;
+  kp.wtw = p->d_wtw;
+  kp.tab_nat = p->d_full_nat;
   kp.steps = p->d_steps;
   kp.coeff = p->d_coeff;
   std::memcpy(kp.c, p->c, sizeof(kp.c));
@@ -296,6 +300,7 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
   p->lead = overlap / 2;
   std::vector<float2> tw = dbp::make_twiddles(logn);
   int rc = upload(&p->d_tw, tw);
+  if (rc == DBP_OK && dbp::warp_ffe_supported(logn)) rc = upload(&p->d_wtw, dbp::make_warp_twiddles(logn, &dbp::unit_float2));
   if (rc != DBP_OK) {
     dbp_plan_destroy(p);
     return rc;
@@ -317,6 +322,8 @@ int dbp_plan_destroy(dbp_plan* p) {
     if (p->streams[s]) cudaStreamDestroy(p->streams[s]);
   }
   cudaFree(p->d_full);
+  cudaFree(p->d_wtw);
+  cudaFree(p->d_full_nat);
   cudaFree(p->d_half);
   cudaFree(p->d_tw);
   cudaFree(p->d_steps);
@@ -364,6 +371,13 @@ int dbp_plan_set_linear(dbp_plan* p, const double* kernel, const double* half_ke
   p->have_half = false;
   int rc = upload(&p->d_full, h);
   if (rc != DBP_OK) return rc;
+  if (dbp::warp_ffe_supported(p->logn)) {
+    // the warp FFE kernel reads the full-step filter in natural bin order
+    std::vector<float2> nat(p->N);
+    for (int j = 0; j < p->N; ++j) nat[bin[j]] = h[j];
+    rc = upload(&p->d_full_nat, nat);
+    if (rc != DBP_OK) return rc;
+  }
   if (half_kernel) {
     rc = upload(&p->d_half, hh);
     if (rc != DBP_OK) return rc;

@@ -46,9 +46,11 @@ struct KernelParams {
   int fir_pad;                // nc rounded up to a multiple of 4
   int slice_floats;           // shared floats per block slice
   int precise_sincos;         // 1: polynomial sincos (multi-step programs), 0: SFU
-  const float2* tab_full;     // K (or H for FFE), natural bin order, 1/N folded in
+  const float2* tab_full;     // K (or H for FFE) in the block kernel's register order, 1/N folded in
   const float2* tab_half;     // K^(1/2) (symmetric arrangement)
   const float2* twiddle;      // per-pass twiddle tables
+  const float2* wtw;          // warp FFE kernel bases (dbp_warp_kernel.cuh, N = 1024 .. 4096)
+  const float2* tab_nat;      // H in natural bin order, 1/N folded in (warp FFE kernel)
   const float2* steps;        // per step (a_j, g_j): rotation exp(+j a_j F), gain g_j
   const float* coeff;         // c_0..c_nc zero padded to nc + 4 (generic FIR path)
   int coeff_stride;           // 0: shared coefficients; > 0: item i uses coeff + i * stride

@@ -6,6 +6,7 @@
 #include <cstdlib>
 
 #include "dbp_block_kernel.cuh"
+#include "dbp_warp_kernel.cuh"
 
 namespace dbp {
 
@@ -144,9 +145,35 @@ cudaError_t launch_ffe_stream(const KernelParams& kp, size_t smem_bytes, cudaStr
   return cudaGetLastError();
 }
 
+// FFE programs at N = 1024 .. 4096 run the warp-resident kernel
+// (dbp_warp_kernel.cuh); env DBP_WARP_FFE=0 selects the block kernel (A/B runs)
+inline bool warp_ffe_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("DBP_WARP_FFE");
+    if (v && *v) return v[0] != '0';
+    return DBP_WARP_FFE != 0;
+  }();
+  return on;
+}
+
+template <int LOGL>
+cudaError_t launch_warp_ffe(const KernelParams& kp, cudaStream_t stream) {
+  using W = WGeo<LOGL>;
+  auto* kernel = dbp_warp_ffe_kernel<LOGL>;
+  cudaError_t e = set_smem_attrs(kernel, W::SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  const long long ctas = (kp.total_blocks + W::BPC - 1) / W::BPC;
+  if (ctas > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kernel<<<dim3((unsigned)ctas), dim3(W::THREADS), W::SMEM_BYTES, stream>>>(kp);
+  return cudaGetLastError();
+}
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
+  if constexpr (LOGN >= 10 && LOGN <= 12) {
+    if (kp.program == kFFE && kp.wtw != nullptr && kp.tab_nat != nullptr && warp_ffe_enabled()) return launch_warp_ffe<LOGN - 6>(kp, stream);
+  }
   if constexpr (LOGN >= DBP_FFE_STREAM_MIN_LOGN && LOGN <= DBP_FFE_STREAM_MAX_LOGN) {
     if (kp.program == kFFE && ffe_stream_enabled()) return launch_ffe_stream<LOGN>(kp, smem_bytes, stream);
   }

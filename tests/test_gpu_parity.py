@@ -550,3 +550,23 @@ def test_tma_and_split_barrier_paths_deterministic(alg, n_blk, m, n):
         np.testing.assert_array_equal(_run(x, cfg), first)
     want = dbp_port.backpropagate_arrays(x[0].astype(np.complex128), 56e9, port_config(cfg))
     assert dbp_port.per_block_rel_l2(first[0], want, n_blk, m).max() <= TOL_BLOCK
+
+
+def test_warp_ffe_kernel_matches_oracle_in_subprocess():
+    # The warp-resident FFE kernel (dbp_warp_kernel.cuh, off by default) is
+    # selected per process by env DBP_WARP_FFE=1: run the FFE parity tests --
+    # golden FFE cases, the large-block FFE cases, the determinism repeats --
+    # in a child process with it on.
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    env = dict(os.environ, DBP_WARP_FFE="1")
+    root = Path(__file__).resolve().parent.parent
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                          "tests/test_gpu_parity.py", "-k",
+                          "golden_cases or ffe_kernel_large or (deterministic and ffe) or ffe_is_linear "
+                          "or ffe_identity_filter"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]

@@ -55,6 +55,8 @@ VARIANTS = {
     "pw3_512": ["-DDBP_TW_POWERS=3", "-DDBP_THREADS_PER_SM=512"],
     "pw3_cta256": ["-DDBP_TW_POWERS=3", "-DDBP_CTA_POSITIONS=256"],
     # round 2
+    "wcta2": ["-DDBP_WARP_MIN_CTAS=2"],
+    "wcta4": ["-DDBP_WARP_MIN_CTAS=4"],
     "pubf0": ["-DDBP_NL_PUBLISH_F=0"],
     "nodit": ["-DDBP_DIT_MAX_STEPS=0"],
     "dit4": ["-DDBP_DIT_MAX_STEPS=4"],
