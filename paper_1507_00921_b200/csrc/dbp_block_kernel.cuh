@@ -377,6 +377,15 @@ __host__ __device__ inline int cs_phys(int j) { return j + ((j >> 4) << 1); }   
 
 inline int fir_floats(int n, int pw) { return fir_phys(n + 2 * pw) + 4 + 2 * (cs_phys(n) + 2); }
 
+// polarisation-split pair (PS): one polarisation's planes, the intensity
+// exchange buffer behind them (N floats), or the FIR buffers publishing F
+inline int ps_smem_floats(int n, int pw, bool fir) {
+  int total = 2 * plane_elems(n) + n;
+  const int f = fir ? fir_phys(n + 2 * pw) + 4 + fir_phys(n) + 4 : 0;
+  if (f > total) total = f;
+  return (total + 3) & ~3;
+}
+
 inline int slice_floats(int n, int pw, bool double_buffer) {
   const int planes = 4 * plane_elems(n);
   if (double_buffer) {
@@ -487,6 +496,69 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
+
+// ---------------------------------------------------------------------------
+// Polarisation-split pairs (PS, N = 8192): the two CTAs of a 2-CTA cluster
+// each hold one polarisation of the block, so two independent half-size CTAs
+// share each SM where one 1024-thread CTA did.  The only coupling is the
+// nonlinear step's total intensity |x|^2 + |y|^2: each CTA writes its 16 T
+// values of |v|^2 into the partner's shared memory with st.async (completion
+// counted on the partner's ``full`` mbarrier) and, once it no longer needs
+// the values it received, arrives on the partner's ``free`` mbarrier.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t peer_smem_addr(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_addr(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_async_v4(uint32_t raddr, float4 v, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
+                   raddr),
+               "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(rbar)
+               : "memory");
+}
+// The write-after-read handshake is relaxed: the release / acquire forms
+// cost a GPU-scope MEMBAR and an L1 invalidation per step.  Ordering instead
+// comes from data: every lane makes the arrive depend on the last value it
+// read from the buffer (so its loads have completed), the warp converges, and
+// the partner issues its st.async only after observing the phase.
+__device__ __forceinline__ uint32_t zero_after(float x) {
+  uint32_t z;
+  asm volatile("and.b32 %0, %1, 0;" : "=r"(z) : "r"(__float_as_uint(x)));
+  return z;
+}
+__device__ __forceinline__ void mbar_arrive_peer_relaxed(uint32_t rbar) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(rbar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_relaxed_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.relaxed.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_addr(bar)), "r"(parity)
+      : "memory");
+}
+
+struct PolXchg {
+  float* xbuf;          // local: the partner's |v|^2 at this CTA's positions, [t][16] swizzled
+  uint32_t peer_xbuf;   // the partner's xbuf (shared::cluster address)
+  uint64_t* full;       // local: completes when the partner's 16 T values have landed
+  uint32_t peer_full;
+  uint64_t* free_;      // local: the partner has consumed what this CTA wrote into its xbuf
+  uint32_t peer_free;
+  uint32_t step;        // nonlinear steps exchanged so far
+};
+// float offset of chunk c (4 floats) of thread t's 16 in the exchange buffer:
+// 16-byte accesses of a quarter warp land in eight distinct bank groups
+__device__ __forceinline__ int xbuf_slot(int t, int c) { return 16 * t + 4 * (c ^ ((t >> 1) & 3)); }
 
 // Shared memory of one block slice: exchange planes (x, y) and the FIR
 // buffers, aliased.  Single region: every exchange is "barrier; write;
@@ -1256,13 +1328,17 @@ __device__ __forceinline__ void fir8_generic(const float* __restrict__ ibuf, flo
 
 // PROG (KernelProg): kProgNoFir compiles the F = c0 I path only; kProgGeneric
 // the fixed-tap FIRs; kProgGenericFir adds the runtime-N_c fir8_generic
-template <int LOGN, int MODE, int PROG = kProgGenericFir, int TWP = kTwDit>
+template <int LOGN, int MODE, int PROG = kProgGenericFir, int TWP = kTwDit, int PS = 0>
 __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, const KernelParams& kp,
-                                       int step_idx, int t, int pol, const float* __restrict__ cptr) {
+                                       int step_idx, int t, int pol, const float* __restrict__ cptr,
+                                       PolXchg* px = nullptr) {
   // the fused-twiddle instantiation runs <= 2-step programs (SFU sincos): F is
   // published; the exact-adjoint one publishes factors for polynomial sincos
-  // (N = 8192, one CTA per SM: the factors measured +1.9%, profiles/r2/ab_pubf_8192.txt)
-  const bool factors = DBP_NL_PUBLISH_F == 0 || LOGN >= 13 || (TWP != kTwDit && PROG != kProgSym1 && kp.precise_sincos);
+  // (N = 8192, one CTA per SM: the factors measured +1.9%, profiles/r2/ab_pubf_8192.txt);
+  // polarisation-split pairs publish F (the factor buffer would not leave room
+  // for two CTAs per SM)
+  const bool factors = !PS && (DBP_NL_PUBLISH_F == 0 || LOGN >= 13 ||
+                               (TWP != kTwDit && PROG != kProgSym1 && kp.precise_sincos));
   // per-item coefficient sets (training batches) read from global memory
   const float c0 = kp.coeff_stride ? __ldg(cptr) : kp.c[0];
   using G = Geo<LOGN>;
@@ -1271,15 +1347,62 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
   // total dual-pol intensity of positions t + T m, m = 8 pol .. 8 pol + 7:
   // each lane of a pair forms half of the 16 (own |v|^2 plus the partner
   // lane's, one shuffle per two positions)
-  float inten[8];
+  constexpr int NI = PS ? 16 : 8;
+  float inten[NI];
+  if constexpr (PS) {
+    // this CTA's |v|^2 to the partner, the partner's to us (see PolXchg)
+    float own[16];
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const float lo = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
-    const float hi = fmaf(v[m + 8].x, v[m + 8].x, v[m + 8].y * v[m + 8].y);
-    const float other = __shfl_xor_sync(0xffffffffu, pol ? lo : hi, 16);
-    inten[m] = (pol ? hi : lo) + other;
+    for (int m = 0; m < 16; ++m) own[m] = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
+    const uint32_t s = px->step;
+    if (threadIdx.x == 0) mbar_expect_tx(px->full, 16u * T * sizeof(float));
+    if (s > 0) mbar_wait_relaxed_cluster(px->free_, (s - 1) & 1u);
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      st_async_v4(px->peer_xbuf + 4u * xbuf_slot(t, c),
+                  make_float4(own[4 * c], own[4 * c + 1], own[4 * c + 2], own[4 * c + 3]), px->peer_full);
+    mbar_wait(px->full, s & 1u);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float4 o = *reinterpret_cast<const float4*>(px->xbuf + xbuf_slot(t, c));
+      inten[4 * c] = own[4 * c] + o.x;
+      inten[4 * c + 1] = own[4 * c + 1] + o.y;
+      inten[4 * c + 2] = own[4 * c + 2] + o.z;
+      inten[4 * c + 3] = own[4 * c + 3] + o.w;
+    }
+  } else {
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const float lo = fmaf(v[m].x, v[m].x, v[m].y * v[m].y);
+      const float hi = fmaf(v[m + 8].x, v[m + 8].x, v[m + 8].y * v[m + 8].y);
+      const float other = __shfl_xor_sync(0xffffffffu, pol ? lo : hi, 16);
+      inten[m] = (pol ? hi : lo) + other;
+    }
   }
-  if (PROG == kProgNoFir || kp.nc == 0) {
+  // PS: the partner may write its next values once ours are consumed (the
+  // exchange buffer overlaps the tail of the F buffer, so after the F reads)
+  auto release_xbuf = [&](float last_read) {
+    if constexpr (PS) {
+      const uint32_t dep = zero_after(last_read);
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive_peer_relaxed(px->peer_free + dep);
+      ++px->step;
+    }
+  };
+  if constexpr (PS) {
+    if (PROG == kProgNoFir || kp.nc == 0) {
+      release_xbuf((inten[3] + inten[7]) + (inten[11] + inten[15]));   // one value per xbuf load
+      if (kp.precise_sincos) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = c_mul(v[i], rot_factor<true>(sg.x, sg.y, c0 * inten[i]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = c_mul(v[i], rot_factor<false>(sg.x, sg.y, c0 * inten[i]));
+      }
+      return;
+    }
+  }
+  if (!PS && (PROG == kProgNoFir || kp.nc == 0)) {
     // F = c0 I: each lane of the pair evaluates half the factors, then swaps
     float2 fac[8];
     if (kp.precise_sincos) {
@@ -1306,7 +1429,18 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
     // each lane stores its half of the intensities
     sh.before_write();
     const int m0 = 8 * pol;
-    if constexpr (T >= 16) {
+    if constexpr (PS) {
+      static_assert(T >= 16, "polarisation split only for large N");
+      float* ib = ibuf + fir_phys(t + pw);
+#pragma unroll
+      for (int m = 0; m < 16; ++m) ib[m * (5 * T / 4)] = inten[m];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int j = m * T + t;
+        if (j < pw) ibuf[fir_phys(j + N + pw)] = inten[m];
+        if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[m];
+      }
+    } else if constexpr (T >= 16) {
       // fir_phys(m T + t + pw) = m (5T/4) + fir_phys(t + pw) for T >= 16
       float* ib = ibuf + fir_phys(t + pw) + m0 * (5 * T / 4);
 #pragma unroll
@@ -1332,8 +1466,11 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
       }
     }
     sh.after_write();
-    const int p0 = 16 * t + 8 * pol;
     constexpr bool kDirectFir = DBP_FIR_DIRECT && LOGN >= 10;
+    // PS: each CTA filters all 16 of its positions (the partner does the same work)
+#pragma unroll 1
+    for (int h = 0; h < (PS ? 2 : 1); ++h) {
+    const int p0 = 16 * t + 8 * (PS ? h : pol);
     switch (kp.coeff_stride ? -1 : kp.nc) {
       case 1: fir8_fixed<1, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N, factors); break;
       case 9: fir8_fixed<9, kDirectFir>(ibuf, nlbuf, p0, sg.x, sg.y, kp, N, factors); break;
@@ -1344,6 +1481,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
         if constexpr (PROG == kProgGenericFir) fir8_generic(ibuf, nlbuf, p0, pw, sg.x, sg.y, kp, cptr, c0, factors);
         else __trap();   // the launcher routes these programs to kProgGenericFir
         break;
+    }
     }
     sh.after_write();
 #if DBP_NL_PUBLISH_F
@@ -1358,13 +1496,21 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
         for (int m = 0; m < 16; ++m) fv[m] = nlbuf[fir_phys(m * T + t)];
       }
       sh.reads_done();
+      if constexpr (PS) {
+        float sum = 0.f;
+#pragma unroll
+        for (int m = 0; m < 16; ++m) sum += fv[m];
+        release_xbuf(sum);   // every F read (the F buffer overlaps the exchange buffer)
+      }
       if (PROG != kProgSym1 && kp.precise_sincos) rotate_by_f<true>(v, fv, sg.x, sg.y);
       else rotate_by_f<false>(v, fv, sg.x, sg.y);
     } else {
       rotate_by_factors<LOGN>(v, nlbuf, sh, t);
+      release_xbuf(v[15].x);
     }
 #else
     rotate_by_factors<LOGN>(v, nlbuf, sh, t);
+    release_xbuf(v[15].x);
 #endif
   }
 }
@@ -1380,9 +1526,10 @@ __device__ __host__ constexpr bool tma_load_program() {
 }
 
 // One CTA-sized group of blocks (block slices) through the whole program.
-template <int LOGN, int MODE, int PROG, int TWP>
+template <int LOGN, int MODE, int PROG, int TWP, int PS = 0>
 __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, MODE>& sh, long long grp,
-                                              long long n_groups, int t, int slice, int pol) {
+                                              long long n_groups, int t, int slice, int pol,
+                                              long long gstride, PolXchg* px = nullptr) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
   const long long blk = grp * G::BPC + slice;
@@ -1463,9 +1610,9 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     for (int m = 0; m < 16; ++m) v[m] = make_float2(0.f, 0.f);
   }
   if constexpr (kTmaLoad && MODE == kShmSplitWar) sh.reads_done();  // the deferred initial arrival
-  if (grp + gridDim.x < n_groups) {
+  if (grp + gstride < n_groups) {
     // L2 prefetch of the next group's block: one 128-byte line per thread and polarisation
-    const long long nblk = (grp + gridDim.x) * G::BPC + slice;
+    const long long nblk = (grp + gstride) * G::BPC + slice;
     if (nblk < kp.total_blocks) {
       const long long nitem = kp.bpi_magic ? (long long)__umul64hi(kp.bpi_magic, (unsigned long long)nblk)
                                            : nblk / kp.blocks_per_item;
@@ -1495,7 +1642,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
     conv_block<LOGN, MODE, kFresh, TWP>(v, sh, kp.tab_full, kp.twiddle, t);
   } else if constexpr (PROG == kProgSym1) {
     conv_block<LOGN, MODE, false, TWP>(v, sh, kp.tab_half, kp.twiddle, t);
-    if constexpr (!DBP_EXPERIMENT_NONL) rotate<LOGN, MODE, PROG, TWP>(v, sh, kp, 0, t, pol, cptr);
+    if constexpr (!DBP_EXPERIMENT_NONL) rotate<LOGN, MODE, PROG, TWP, PS>(v, sh, kp, 0, t, pol, cptr, px);
     conv_block<LOGN, MODE, false, TWP>(v, sh, kp.tab_half, kp.twiddle, t);
   } else {
   const int n_ops = kp.n_ops;
@@ -1507,7 +1654,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
       conv_block<LOGN, MODE, false, TWP>(v, sh, tab, kp.twiddle, t);
     } else if (DBP_EXPERIMENT_NONL) {
     } else {
-      rotate<LOGN, MODE, PROG, TWP>(v, sh, kp, sidx, t, pol, cptr);
+      rotate<LOGN, MODE, PROG, TWP, PS>(v, sh, kp, sidx, t, pol, cptr, px);
     }
   }
   }
@@ -1573,15 +1720,54 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
 // PROG: kProgGeneric (any operator program, fixed-tap FIRs), kProgFFE (the
 // single-convolution FFE program), kProgNoFir (split-step programs without an
 // intensity FIR), kProgGenericFir (runtime N_c and per-item coefficient sets)
-template <int LOGN, int PROG = kProgGeneric, int TWP = kTwDit>
-__global__ void __launch_bounds__(Geo<LOGN>::THREADS, PROG == kProgFFE          ? Geo<LOGN>::FFE_MIN_CTAS
-                                                      : PROG == kProgNoFir      ? Geo<LOGN>::NOFIR_MIN_CTAS
-                                                      : PROG == kProgGenericFir ? Geo<LOGN>::GENFIR_MIN_CTAS
-                                                                                : Geo<LOGN>::MIN_CTAS)
+// PS = 1: polarisation-split pair (N = 8192, launched as 2-CTA clusters of
+// T threads, see PolXchg); every other argument as the pol-pair kernel
+template <int LOGN, int PROG = kProgGeneric, int TWP = kTwDit, int PS = 0>
+__global__ void __launch_bounds__(PS ? Geo<LOGN>::T : Geo<LOGN>::THREADS,
+                                  PS                        ? 2
+                                  : PROG == kProgFFE        ? Geo<LOGN>::FFE_MIN_CTAS
+                                  : PROG == kProgNoFir      ? Geo<LOGN>::NOFIR_MIN_CTAS
+                                  : PROG == kProgGenericFir ? Geo<LOGN>::GENFIR_MIN_CTAS
+                                                            : Geo<LOGN>::MIN_CTAS)
 dbp_block_kernel(const KernelParams kp) {
   using G = Geo<LOGN>;
   constexpr int N = G::N, T = G::T;
   extern __shared__ float4 smem_raw[];
+  if constexpr (PS) {
+    static_assert(!PS || (G::BPC == 1 && LOGN >= DBP_PERSIST_MIN_LOGN), "polarisation split: N = 8192 only");
+    constexpr int MODE = kShmSync;
+    const int t = threadIdx.x;
+    Shm<LOGN, MODE> sh;
+    sh.init(reinterpret_cast<float*>(smem_raw), kp.slice_floats, 0);   // this CTA's planes only
+    const long long n_groups = (kp.total_blocks + G::BPC - 1) / G::BPC;
+    const long long gstride = gridDim.x >> 1;
+    if constexpr (PROG == kProgFFE) {
+      // the linear program never couples the polarisations: independent CTAs, no cluster
+      for (long long grp = blockIdx.x >> 1; grp < n_groups; grp += gstride)
+        process_group<LOGN, MODE, PROG, TWP, 1>(kp, sh, grp, n_groups, t, 0, blockIdx.x & 1, gstride);
+      return;
+    }
+    const uint32_t rank = cluster_ctarank();
+    const int pol = (int)rank;
+    __shared__ alignas(8) uint64_t xbars[2];   // full, free
+    PolXchg px;
+    px.xbuf = reinterpret_cast<float*>(smem_raw) + 2 * plane_elems(N);   // behind this CTA's planes
+    px.full = &xbars[0];
+    px.free_ = &xbars[1];
+    if (threadIdx.x == 0) {
+      mbar_init(px.full, 1);
+      mbar_init(px.free_, T / 32);
+    }
+    px.peer_xbuf = peer_smem_addr(px.xbuf, rank ^ 1u);
+    px.peer_full = peer_smem_addr(px.full, rank ^ 1u);
+    px.peer_free = peer_smem_addr(px.free_, rank ^ 1u);
+    px.step = 0;
+    cluster_sync_all();   // both CTAs' mbarriers initialised before any remote operation
+    for (long long grp = blockIdx.x >> 1; grp < n_groups; grp += gstride)
+      process_group<LOGN, MODE, PROG, TWP, 1>(kp, sh, grp, n_groups, t, 0, pol, gstride, &px);
+    cluster_sync_all();   // no CTA leaves while its partner may still signal it
+    return;
+  } else {
   const int lane = threadIdx.x & 31;
   const int pol = lane >> 4;
   const int q = ((threadIdx.x >> 5) << 4) + (lane & 15);  // position-thread index within the CTA
@@ -1608,9 +1794,10 @@ dbp_block_kernel(const KernelParams kp) {
   const long long n_groups = (kp.total_blocks + G::BPC - 1) / G::BPC;
   if constexpr (LOGN >= DBP_PERSIST_MIN_LOGN) {
     for (long long grp = blockIdx.x; grp < n_groups; grp += gridDim.x)
-      process_group<LOGN, MODE, PROG, TWP>(kp, sh, grp, n_groups, t, slice, pol);
+      process_group<LOGN, MODE, PROG, TWP>(kp, sh, grp, n_groups, t, slice, pol, gridDim.x);
   } else {
-    process_group<LOGN, MODE, PROG, TWP>(kp, sh, blockIdx.x, n_groups, t, slice, pol);
+    process_group<LOGN, MODE, PROG, TWP>(kp, sh, blockIdx.x, n_groups, t, slice, pol, gridDim.x);
+  }
   }
 }
 

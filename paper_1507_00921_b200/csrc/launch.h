@@ -168,9 +168,74 @@ cudaError_t launch_warp_ffe(const KernelParams& kp, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// N = 8192: polarisation-split pairs (dbp_block_kernel<13, PROG, TWP, 1>, one
+// 512-thread CTA per polarisation, two CTAs per SM; split-step programs as
+// 2-CTA clusters exchanging the intensity).  Measured against the 1024-thread
+// pol-pair CTA (profiles/r2/ab_ps1.txt): FFE 8192/1024 +4.4%, but the
+// per-step intensity handshake locks the pair together: ESSFM 8192/1400
+// -17%, SSFM-20 8192/1024 -21%.  Default: the FFE program only; env
+// DBP_POLSPLIT=1 (every program) / 0 (none) overrides.
+inline int polsplit_mode() {
+  static const int mode = [] {
+    const char* v = std::getenv("DBP_POLSPLIT");
+    if (v && *v) return v[0] == '0' ? 0 : 2;
+    return 1;
+  }();
+  return mode;
+}
+inline bool polsplit_enabled(const KernelParams& kp) {
+  const int m = polsplit_mode();
+  return m == 2 || (m == 1 && kp.program == kFFE);
+}
+
+template <int LOGN, int TWP>
+auto select_ps_kernel(const KernelParams& kp) {
+  auto* kernel = dbp_block_kernel<LOGN, kProgGeneric, TWP, 1>;
+  if (kp.program == kFFE) kernel = dbp_block_kernel<LOGN, kProgFFE, TWP, 1>;
+  if ((kp.program == kSSFM || kp.program == kESSFM) && kp.nc == 0) kernel = dbp_block_kernel<LOGN, kProgNoFir, TWP, 1>;
+  if (kp.program != kFFE && kp.nc > 0 && (kp.coeff_stride != 0 || !fixed_fir_nc(kp.nc)))
+    kernel = dbp_block_kernel<LOGN, kProgGenericFir, TWP, 1>;
+  return kernel;
+}
+
+template <int LOGN>
+cudaError_t launch_polsplit(const KernelParams& kp0, cudaStream_t stream) {
+  using G = Geo<LOGN>;
+  KernelParams kp = kp0;
+  const bool fir = kp.program != kFFE && kp.nc > 0;
+  kp.slice_floats = ps_smem_floats(G::N, kp.fir_pad, fir);
+  const size_t smem = (size_t)kp.slice_floats * sizeof(float);
+  auto* kernel = select_ps_kernel<LOGN, DBP_TW_POWERS>(kp);
+  cudaError_t e = set_smem_attrs(kernel, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long clusters = kp.total_blocks;   // one block (group) per cluster, persistent
+  if (clusters > sms) clusters = sms;     // two CTAs per SM
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * clusters));
+  cfg.blockDim = dim3(G::T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kp.program == kFFE ? 0 : 1;   // the FFE pairs never communicate
+  e = cudaLaunchKernelEx(&cfg, kernel, kp);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
+  if constexpr (LOGN == 13) {
+    if (polsplit_enabled(kp)) return launch_polsplit<LOGN>(kp, stream);
+  }
   if constexpr (LOGN >= 10 && LOGN <= 12) {
     if (kp.program == kFFE && kp.wtw != nullptr && kp.tab_nat != nullptr && warp_ffe_enabled()) return launch_warp_ffe<LOGN - 6>(kp, stream);
   }

@@ -570,3 +570,23 @@ def test_warp_ffe_kernel_matches_oracle_in_subprocess():
                           "or ffe_identity_filter"],
                          cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+
+
+def test_polsplit_pairs_match_oracle_in_subprocess():
+    # N = 8192 polarisation-split pairs (launch.h polsplit_mode): the FFE program
+    # runs them by default; DBP_POLSPLIT=1 forces them for every program (the
+    # split-step programs as 2-CTA clusters exchanging |v|^2 through distributed
+    # shared memory).  Run the N = 8192 parity tests with them forced.
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    env = dict(os.environ, DBP_POLSPLIT="1")
+    root = Path(__file__).resolve().parent.parent
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                          "tests/test_gpu_parity.py", "-k",
+                          "golden_cases or (ffe_kernel_large and 8192) or (nofir and 8192) "
+                          "or (fir_paths and 8192) or random_configurations"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
