@@ -379,8 +379,8 @@ inline int fir_floats(int n, int pw) { return fir_phys(n + 2 * pw) + 4 + 2 * (cs
 
 // polarisation-split pair (PS): one polarisation's planes, the intensity
 // exchange buffer behind them (N floats), or the FIR buffers publishing F
-inline int ps_smem_floats(int n, int pw, bool fir) {
-  int total = 2 * plane_elems(n) + n;
+inline int ps_smem_floats(int n, int pw, bool fir, bool xchg) {
+  int total = 2 * plane_elems(n) + (xchg ? n : 0);
   const int f = fir ? fir_phys(n + 2 * pw) + 4 + fir_phys(n) + 4 : 0;
   if (f > total) total = f;
   return (total + 3) & ~3;
@@ -1568,12 +1568,17 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
       __syncthreads();
       float2* dst0 = reinterpret_cast<float2*>(sh.base);
       if (threadIdx.x == 0) {
-        mbar_expect_tx(&in_bar, 2 * N * sizeof(float2));
-        bulk_load(dst0, src, N * sizeof(float2), &in_bar);
-        bulk_load(dst0 + sh.plane_len(), src + kp.in_pol_stride, N * sizeof(float2), &in_bar);
+        if constexpr (PS) {   // this CTA's polarisation only
+          mbar_expect_tx(&in_bar, N * sizeof(float2));
+          bulk_load(dst0, src + pol * kp.in_pol_stride, N * sizeof(float2), &in_bar);
+        } else {
+          mbar_expect_tx(&in_bar, 2 * N * sizeof(float2));
+          bulk_load(dst0, src, N * sizeof(float2), &in_bar);
+          bulk_load(dst0 + sh.plane_len(), src + kp.in_pol_stride, N * sizeof(float2), &in_bar);
+        }
       }
       mbar_wait(&in_bar, 0);
-      const float2* pl = dst0 + pol * sh.plane_len() + t;
+      const float2* pl = dst0 + (PS ? 0 : pol) * sh.plane_len() + t;
 #pragma unroll
       for (int m = 0; m < 16; ++m) v[m] = pl[m * T];
       loaded = true;
@@ -1681,7 +1686,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
                         (reinterpret_cast<uintptr_t>(row0) & 15) == 0;
       if (bulk) {
         sh.before_write();
-        float2* stg = reinterpret_cast<float2*>(sh.base) + pol * kp.step - kp.lead;
+        float2* stg = reinterpret_cast<float2*>(sh.base) + (PS ? 0 : pol) * kp.step - kp.lead;
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
           const int j = m * T + t;
@@ -1691,8 +1696,12 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
         __syncthreads();
         if (threadIdx.x == 0) {
           const float2* src = reinterpret_cast<const float2*>(sh.base);
-          bulk_store(row0, src, (uint32_t)len * 8u);
-          bulk_store(row0 + kp.out_pol_stride, src + kp.step, (uint32_t)len * 8u);
+          if constexpr (PS) {
+            bulk_store(row0 + pol * kp.out_pol_stride, src, (uint32_t)len * 8u);
+          } else {
+            bulk_store(row0, src, (uint32_t)len * 8u);
+            bulk_store(row0 + kp.out_pol_stride, src + kp.step, (uint32_t)len * 8u);
+          }
           bulk_store_commit_and_wait_read();
         }
         return;
@@ -1724,7 +1733,7 @@ __device__ __forceinline__ void process_group(const KernelParams& kp, Shm<LOGN, 
 // T threads, see PolXchg); every other argument as the pol-pair kernel
 template <int LOGN, int PROG = kProgGeneric, int TWP = kTwDit, int PS = 0>
 __global__ void __launch_bounds__(PS ? Geo<LOGN>::T : Geo<LOGN>::THREADS,
-                                  PS                        ? 2
+                                  PS                        ? (1024 / Geo<LOGN>::T > 0 ? 1024 / Geo<LOGN>::T : 1)
                                   : PROG == kProgFFE        ? Geo<LOGN>::FFE_MIN_CTAS
                                   : PROG == kProgNoFir      ? Geo<LOGN>::NOFIR_MIN_CTAS
                                   : PROG == kProgGenericFir ? Geo<LOGN>::GENFIR_MIN_CTAS
@@ -1734,7 +1743,8 @@ dbp_block_kernel(const KernelParams kp) {
   constexpr int N = G::N, T = G::T;
   extern __shared__ float4 smem_raw[];
   if constexpr (PS) {
-    static_assert(!PS || (G::BPC == 1 && LOGN >= DBP_PERSIST_MIN_LOGN), "polarisation split: N = 8192 only");
+    static_assert(G::BPC == 1 && (LOGN >= DBP_PERSIST_MIN_LOGN || (PROG == kProgFFE && LOGN >= 10)),
+                  "polarisation split: N = 8192, or the FFE program from N = 1024");
     constexpr int MODE = kShmSync;
     const int t = threadIdx.x;
     Shm<LOGN, MODE> sh;

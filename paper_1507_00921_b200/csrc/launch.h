@@ -183,8 +183,18 @@ inline int polsplit_mode() {
   }();
   return mode;
 }
+// FFE programs from this block length run the split (env DBP_POLSPLIT_FFE_MIN_LOGN)
+inline int polsplit_ffe_min_logn() {
+  static const int v = [] {
+    const char* e = std::getenv("DBP_POLSPLIT_FFE_MIN_LOGN");
+    return e && *e ? std::atoi(e) : 11;
+  }();
+  return v;
+}
+template <int LOGN>
 inline bool polsplit_enabled(const KernelParams& kp) {
   const int m = polsplit_mode();
+  if (LOGN < 13) return m != 0 && kp.program == kFFE && LOGN >= polsplit_ffe_min_logn();
   return m == 2 || (m == 1 && kp.program == kFFE);
 }
 
@@ -203,16 +213,18 @@ cudaError_t launch_polsplit(const KernelParams& kp0, cudaStream_t stream) {
   using G = Geo<LOGN>;
   KernelParams kp = kp0;
   const bool fir = kp.program != kFFE && kp.nc > 0;
-  kp.slice_floats = ps_smem_floats(G::N, kp.fir_pad, fir);
+  kp.slice_floats = ps_smem_floats(G::N, kp.fir_pad, fir, kp.program != kFFE);
   const size_t smem = (size_t)kp.slice_floats * sizeof(float);
-  auto* kernel = select_ps_kernel<LOGN, DBP_TW_POWERS>(kp);
+  auto* kernel = dbp_block_kernel<LOGN, kProgFFE, kTwDit, 1>;   // N = 1024 .. 4096: FFE only, DIT FFT
+  if constexpr (LOGN >= DBP_PERSIST_MIN_LOGN) kernel = select_ps_kernel<LOGN, DBP_TW_POWERS>(kp);
   cudaError_t e = set_smem_attrs(kernel, smem);
   if (e != cudaSuccess) return e;
   int dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  long long clusters = kp.total_blocks;   // one block (group) per cluster, persistent
-  if (clusters > sms) clusters = sms;     // two CTAs per SM
+  long long clusters = kp.total_blocks;   // one block (group) per pair
+  if (LOGN >= DBP_PERSIST_MIN_LOGN && clusters > sms) clusters = sms;   // persistent: two CTAs per SM
+  if (2 * clusters > 0x7fffffffLL) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(2 * clusters));
   cfg.blockDim = dim3(G::T);
@@ -234,7 +246,9 @@ template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
   if constexpr (LOGN == 13) {
-    if (polsplit_enabled(kp)) return launch_polsplit<LOGN>(kp, stream);
+    if (polsplit_enabled<LOGN>(kp)) return launch_polsplit<LOGN>(kp, stream);
+  } else if constexpr (LOGN >= 10 && LOGN <= 12) {
+    if (polsplit_enabled<LOGN>(kp)) return launch_polsplit<LOGN>(kp, stream);
   }
   if constexpr (LOGN >= 10 && LOGN <= 12) {
     if (kp.program == kFFE && kp.wtw != nullptr && kp.tab_nat != nullptr && warp_ffe_enabled()) return launch_warp_ffe<LOGN - 6>(kp, stream);
