@@ -114,6 +114,15 @@ def kernel_twp(a) -> int:
     return 4 if (a.algorithm == "ffe" or steps <= 2) and int(_m.log2(a.block_len)) <= 12 else 3
 
 
+def kernel_name(a) -> str:
+    """The instantiation the launcher picks (csrc/launch.h): the FFE program
+    from N = 2048 runs as polarisation-split pairs (template argument PS = 1,
+    one CTA per polarisation)."""
+    logn = int(math.log2(a.block_len))
+    ps = a.algorithm == "ffe" and logn >= 11
+    return f"dbp::dbp_block_kernel<{logn}, {kernel_prog(a)}, {kernel_twp(a)}{', 1' if ps else ''}>"
+
+
 def kernel_prog(a) -> int:
     """Which instantiation of the block kernel the launcher picks (csrc/launch.h
     launch_block_kernel_impl): 0 generic (fixed-tap FIR), 1 FFE-only, 2 no-FIR
@@ -409,8 +418,7 @@ def run_ours(a) -> int:
                          "flops_per_sample": f_s, "traffic": traffic, "traffic_unit": "bytes per launch",
                          "traffic_source": traffic_src,
                          "algorithmic_bytes_per_launch": b_s * per_launch_samples,
-                         "kernel": f"dbp::dbp_block_kernel<{int(math.log2(a.block_len))}, {kernel_prog(a)}, "
-                                   f"{kernel_twp(a)}>"},
+                         "kernel": kernel_name(a)},
             "roofline_hbm": {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": achieved_gbs / hbm_peak, "bytes_per_sample": b_s,
                              "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)"},
