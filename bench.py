@@ -111,7 +111,10 @@ def kernel_twp(a) -> int:
     exact-adjoint FFT."""
     import math as _m
     steps = 0 if a.algorithm == "ffe" else a.num_steps
-    return 4 if (a.algorithm == "ffe" or steps <= 2) and int(_m.log2(a.block_len)) <= 12 else 3
+    logn = int(_m.log2(a.block_len))
+    dit = a.algorithm == "ffe" or steps <= 2
+    # the R2 kernel's 4096-point transforms follow the N = 4096 rule
+    return 4 if dit and (logn <= 12 or (logn == 13 and a.algorithm != "ffe")) else 3
 
 
 def kernel_name(a) -> str:
@@ -119,6 +122,9 @@ def kernel_name(a) -> str:
     from N = 2048 runs as polarisation-split pairs (template argument PS = 1,
     one CTA per polarisation)."""
     logn = int(math.log2(a.block_len))
+    if logn == 13 and a.algorithm != "ffe":
+        # N = 8192 split-step programs: the radix-2-around-4096 kernel (csrc/dbp_r2_kernel.cuh)
+        return f"dbp::dbp_r2_kernel<{kernel_prog(a)}, {kernel_twp(a)}>"
     ps = a.algorithm == "ffe" and logn >= 11
     return f"dbp::dbp_block_kernel<{logn}, {kernel_prog(a)}, {kernel_twp(a)}{', 1' if ps else ''}>"
 

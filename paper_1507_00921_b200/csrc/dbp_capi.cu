@@ -100,6 +100,10 @@ struct dbp_plan {
   float2* d_tw = nullptr;
   float2* d_wtw = nullptr;   // warp FFE kernel bases (N = 1024 .. 4096)
   float2* d_full_nat = nullptr;   // the full-step filter in natural bin order (warp FFE kernel)
+  float2* d_r2_full = nullptr;    // N = 8192 radix-2 step tables (dbp_r2_kernel.cuh)
+  float2* d_r2_half = nullptr;
+  float2* d_r2_tw = nullptr;      // N = 8192: the 4096-point twiddles
+  bool have_r2_half = false;
   float2* d_steps = nullptr;
   int steps_cap = 0;
   float* d_coeff = nullptr;
@@ -176,6 +180,9 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   kp.twiddle = p->d_tw;
   kp.wtw = p->d_wtw;
   kp.tab_nat = p->d_full_nat;
+  kp.r2_full = p->d_r2_full;
+  kp.r2_half = p->have_r2_half ? p->d_r2_half : nullptr;
+  kp.r2_tw = p->d_r2_tw;
   kp.steps = p->d_steps;
   kp.coeff = p->d_coeff;
   std::memcpy(kp.c, p->c, sizeof(kp.c));
@@ -301,6 +308,7 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
   std::vector<float2> tw = dbp::make_twiddles(logn);
   int rc = upload(&p->d_tw, tw);
   if (rc == DBP_OK && dbp::warp_ffe_supported(logn)) rc = upload(&p->d_wtw, dbp::make_warp_twiddles(logn, &dbp::unit_float2));
+  if (rc == DBP_OK && logn == 13) rc = upload(&p->d_r2_tw, dbp::make_twiddles(12));
   if (rc != DBP_OK) {
     dbp_plan_destroy(p);
     return rc;
@@ -324,6 +332,9 @@ int dbp_plan_destroy(dbp_plan* p) {
   cudaFree(p->d_full);
   cudaFree(p->d_wtw);
   cudaFree(p->d_full_nat);
+  cudaFree(p->d_r2_full);
+  cudaFree(p->d_r2_half);
+  cudaFree(p->d_r2_tw);
   cudaFree(p->d_half);
   cudaFree(p->d_tw);
   cudaFree(p->d_steps);
@@ -381,6 +392,17 @@ int dbp_plan_set_linear(dbp_plan* p, const double* kernel, const double* half_ke
   if (half_kernel) {
     rc = upload(&p->d_half, hh);
     if (rc != DBP_OK) return rc;
+  }
+  if (p->logn == 13) {
+    // the R2 kernel's step tables, from the float64 filters
+    p->have_r2_half = false;
+    rc = upload(&p->d_r2_full, dbp::make_r2_tables(kernel));
+    if (rc != DBP_OK) return rc;
+    if (half_kernel) {
+      rc = upload(&p->d_r2_half, dbp::make_r2_tables(half_kernel));
+      if (rc != DBP_OK) return rc;
+      p->have_r2_half = true;
+    }
   }
   p->have_full = true;
   p->have_half = half_kernel != nullptr;

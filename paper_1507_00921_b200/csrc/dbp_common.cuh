@@ -51,6 +51,9 @@ struct KernelParams {
   const float2* twiddle;      // per-pass twiddle tables
   const float2* wtw;          // warp FFE kernel bases (dbp_warp_kernel.cuh, N = 1024 .. 4096)
   const float2* tab_nat;      // H in natural bin order, 1/N folded in (warp FFE kernel)
+  const float2* r2_full;      // N = 8192 radix-2 step tables [A | C | D] (dbp_r2_kernel.cuh), full step
+  const float2* r2_half;      //   ... half step (symmetric arrangement)
+  const float2* r2_tw;        //   ... the 4096-point transforms' twiddles
   const float2* steps;        // per step (a_j, g_j): rotation exp(+j a_j F), gain g_j
   const float* coeff;         // c_0..c_nc zero padded to nc + 4 (generic FIR path)
   int coeff_stride;           // 0: shared coefficients; > 0: item i uses coeff + i * stride

@@ -7,6 +7,7 @@
 
 #include "dbp_block_kernel.cuh"
 #include "dbp_warp_kernel.cuh"
+#include "dbp_r2_kernel.cuh"
 
 namespace dbp {
 
@@ -242,9 +243,50 @@ cudaError_t launch_polsplit(const KernelParams& kp0, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// N = 8192 as a radix-2 step around two 4096-point transforms per thread
+// (dbp_r2_kernel.cuh); env DBP_R2=0|1 overrides the default
+inline bool r2_enabled(const KernelParams& kp) {
+  static const int mode = [] {   // 0 off, 1 split-step programs, 2 every program
+    const char* v = std::getenv("DBP_R2");
+    if (v && *v) return v[0] == '0' ? 0 : 2;
+    return DBP_R2 != 0 ? 1 : 0;
+  }();
+  return mode == 2 || (mode == 1 && kp.program != kFFE);
+}
+
+template <int TWP>
+auto select_r2_kernel(const KernelParams& kp) {
+  auto* kernel = dbp_r2_kernel<kProgGeneric, TWP>;
+  if (kp.program == kFFE) kernel = dbp_r2_kernel<kProgFFE, TWP>;
+  if ((kp.program == kSSFM || kp.program == kESSFM) && kp.nc == 0) kernel = dbp_r2_kernel<kProgNoFir, TWP>;
+  if (kp.program != kFFE && kp.nc > 0 && (kp.coeff_stride != 0 || !fixed_fir_nc(kp.nc)))
+    kernel = dbp_r2_kernel<kProgGenericFir, TWP>;
+  return kernel;
+}
+
+inline cudaError_t launch_r2(const KernelParams& kp0, cudaStream_t stream) {
+  KernelParams kp = kp0;
+  kp.slice_floats = r2_slice_floats(kp.fir_pad);
+  const size_t smem = (size_t)kp.slice_floats * sizeof(float);
+  auto* kernel = use_dit_fft(kp) ? select_r2_kernel<kTwDit>(kp) : select_r2_kernel<DBP_TW_POWERS>(kp);
+  cudaError_t e = set_smem_attrs(kernel, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long grid = kp.total_blocks < sms ? kp.total_blocks : sms;   // persistent, one CTA per SM
+  kernel<<<dim3((unsigned)grid), dim3(R2Geo::THREADS), smem, stream>>>(kp);
+  return cudaGetLastError();
+}
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
+  if constexpr (LOGN == 13) {
+    if (kp.r2_full != nullptr && kp.r2_tw != nullptr && r2_enabled(kp) &&
+        (kp.half_ends == 0 || kp.r2_half != nullptr))
+      return launch_r2(kp, stream);
+  }
   if constexpr (LOGN == 13) {
     if (polsplit_enabled<LOGN>(kp)) return launch_polsplit<LOGN>(kp, stream);
   } else if constexpr (LOGN >= 10 && LOGN <= 12) {

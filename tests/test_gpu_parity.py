@@ -582,7 +582,7 @@ def test_polsplit_pairs_match_oracle_in_subprocess():
     import sys
     from pathlib import Path
 
-    env = dict(os.environ, DBP_POLSPLIT="1")
+    env = dict(os.environ, DBP_POLSPLIT="1", DBP_R2="0")
     root = Path(__file__).resolve().parent.parent
     res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
                           "tests/test_gpu_parity.py", "-k",
@@ -590,3 +590,24 @@ def test_polsplit_pairs_match_oracle_in_subprocess():
                           "or (fir_paths and 8192) or random_configurations"],
                          cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+
+
+def test_r2_off_and_on_everywhere_match_oracle_in_subprocess():
+    # N = 8192 split-step programs run the radix-2-around-4096 kernel
+    # (dbp_r2_kernel.cuh) by default.  DBP_R2=0 brings back the pol-pair block
+    # kernel, DBP_R2=1 also routes the FFE program through R2: run the N = 8192
+    # parity tests both ways so every instantiation stays checked.
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    for val in ("0", "1"):
+        env = dict(os.environ, DBP_R2=val)
+        res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                              "tests/test_gpu_parity.py", "-k",
+                              "golden_cases or (ffe_kernel_large and 8192) or (nofir and 8192) "
+                              "or (fir_paths and 8192) or random_configurations"],
+                             cwd=root, env=env, capture_output=True, text=True, timeout=900)
+        assert res.returncode == 0, (val, res.stdout[-3000:] + res.stderr[-2000:])
