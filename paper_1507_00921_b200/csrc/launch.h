@@ -8,6 +8,7 @@
 #include "dbp_block_kernel.cuh"
 #include "dbp_warp_kernel.cuh"
 #include "dbp_r2_kernel.cuh"
+#include "dbp_r2t_kernel.cuh"
 
 namespace dbp {
 
@@ -279,13 +280,51 @@ inline cudaError_t launch_r2(const KernelParams& kp0, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// N = 8192 split-step programs with the parked subsequence in TMEM, two CTAs
+// per SM (dbp_r2t_kernel.cuh); env DBP_R2T=0|1 overrides the default
+inline bool r2t_enabled(const KernelParams& kp) {
+  static const int mode = [] {   // 0 off, 1 split-step programs, 2 every program
+    const char* v = std::getenv("DBP_R2T");
+    if (v && *v) return v[0] == '0' ? 0 : (v[0] == '2' ? 2 : 1);
+    return DBP_R2T != 0 ? 1 : 0;
+  }();
+  return mode == 2 || (mode == 1 && kp.program != kFFE);
+}
+
+template <int TWP>
+auto select_r2t_kernel(const KernelParams& kp) {
+  auto* kernel = dbp_r2t_kernel<kProgGeneric, TWP>;
+  if (kp.program == kFFE) kernel = dbp_r2t_kernel<kProgFFE, TWP>;
+  if ((kp.program == kSSFM || kp.program == kESSFM) && kp.nc == 0) kernel = dbp_r2t_kernel<kProgNoFir, TWP>;
+  if (kp.program != kFFE && kp.nc > 0 && (kp.coeff_stride != 0 || !fixed_fir_nc(kp.nc)))
+    kernel = dbp_r2t_kernel<kProgGenericFir, TWP>;
+  return kernel;
+}
+
+inline cudaError_t launch_r2t(const KernelParams& kp0, cudaStream_t stream) {
+  KernelParams kp = kp0;
+  kp.slice_floats = r2t_slice_floats(kp.fir_pad);
+  const size_t smem = (size_t)kp.slice_floats * sizeof(float);
+  auto* kernel = use_dit_fft(kp) ? select_r2t_kernel<kTwDit>(kp) : select_r2t_kernel<DBP_TW_POWERS>(kp);
+  cudaError_t e = set_smem_attrs(kernel, smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  // persistent, two CTAs per SM (each holds half the SM's TMEM columns)
+  long long grid = kp.total_blocks < 2LL * sms ? kp.total_blocks : 2LL * sms;
+  kernel<<<dim3((unsigned)grid), dim3(R2TGeo::THREADS), smem, stream>>>(kp);
+  return cudaGetLastError();
+}
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
   if constexpr (LOGN == 13) {
-    if (kp.r2_full != nullptr && kp.r2_tw != nullptr && r2_enabled(kp) &&
-        (kp.half_ends == 0 || kp.r2_half != nullptr))
-      return launch_r2(kp, stream);
+    if (kp.r2_full != nullptr && kp.r2_tw != nullptr && (kp.half_ends == 0 || kp.r2_half != nullptr)) {
+      if (r2t_enabled(kp)) return launch_r2t(kp, stream);
+      if (r2_enabled(kp)) return launch_r2(kp, stream);
+    }
   }
   if constexpr (LOGN == 13) {
     if (polsplit_enabled<LOGN>(kp)) return launch_polsplit<LOGN>(kp, stream);

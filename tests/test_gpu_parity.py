@@ -611,3 +611,22 @@ def test_r2_off_and_on_everywhere_match_oracle_in_subprocess():
                               "or (fir_paths and 8192) or random_configurations"],
                              cwd=root, env=env, capture_output=True, text=True, timeout=900)
         assert res.returncode == 0, (val, res.stdout[-3000:] + res.stderr[-2000:])
+
+
+def test_r2t_matches_oracle_in_subprocess():
+    # N = 8192 with the parked subsequence in tensor memory, two CTAs per SM
+    # (dbp_r2t_kernel.cuh).  DBP_R2T=2 routes every program (FFE included)
+    # through it: run the N = 8192 parity tests that way.
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DBP_R2T="2")
+    res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", "-m", "gpu",
+                          "tests/test_gpu_parity.py", "-k",
+                          "golden_cases or (ffe_kernel_large and 8192) or (nofir and 8192) "
+                          "or (fir_paths and 8192) or random_configurations"],
+                         cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
