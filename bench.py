@@ -92,17 +92,11 @@ def make_cfg(a):
 
 
 def work_per_sample(a, gains_not_one: bool = False) -> tuple[float, float]:
-    """(FP32 flops, HBM bytes) per output sample, FFTW 5 N log2 N convention."""
-    n, m = a.block_len, a.overlap
-    lg = math.log2(n)
-    if a.algorithm == "ffe":
-        pairs, ns, nc = 1, 0, 0
-    else:
-        ns = a.num_steps
-        pairs = ns + 1 if a.arrangement == "symmetric" else ns
-        nc = a.nc if a.algorithm == "essfm" else 0
-    flops = 20 * pairs * n * lg + 12 * pairs * n + ns * n * (3 * nc + 21) + (4 * n * ns if gains_not_one else 0)
-    return flops / (n - m), 16.0 * (2 * n - m) / (n - m)
+    """(FP32 flops, HBM bytes) per output sample, FFTW 5 N log2 N convention
+    (paper_1507_00921_b200.costmodel.work_per_sample)."""
+    from paper_1507_00921_b200.costmodel import work_per_sample as wps
+
+    return wps(a.algorithm, a.block_len, a.overlap, a.nc, a.num_steps, a.arrangement, gains_not_one)
 
 
 def kernel_twp(a) -> int:

@@ -68,6 +68,7 @@ from .rx import (
     receive_batch,
 )
 from .training import TrainConfig, TrainResult, load_coefficients, mse, optimize_coefficients, save_coefficients
+from . import costmodel
 
 __version__ = "0.1.0"
 
