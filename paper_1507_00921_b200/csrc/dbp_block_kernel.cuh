@@ -150,6 +150,11 @@ __host__ __device__ constexpr bool fixed_fir_nc(int nc) {
 #ifndef DBP_EXPERIMENT_NOSTORE
 #define DBP_EXPERIMENT_NOSTORE 0
 #endif
+// timing experiment only: the nonlinear step's two CTA-wide __syncthreads
+// removed (its write-after-read barrier kept: the split mbarrier protocol) -- WRONG results
+#ifndef DBP_EXPERIMENT_NONLBAR
+#define DBP_EXPERIMENT_NONLBAR 0
+#endif
 #ifndef DBP_EXPERIMENT_NONL
 #define DBP_EXPERIMENT_NONL 0
 #endif
@@ -1465,7 +1470,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
         if (j >= N - pw) ibuf[fir_phys(j - N + pw)] = inten[m];
       }
     }
-    sh.after_write();
+    if (DBP_EXPERIMENT_NONLBAR) __syncwarp(); else sh.after_write();
     constexpr bool kDirectFir = DBP_FIR_DIRECT && LOGN >= 10;
     // PS: each CTA filters all 16 of its positions (the partner does the same work)
 #pragma unroll 1
@@ -1483,7 +1488,7 @@ __device__ __forceinline__ void rotate(float2 (&v)[16], Shm<LOGN, MODE>& sh, con
         break;
     }
     }
-    sh.after_write();
+    if (DBP_EXPERIMENT_NONLBAR) __syncwarp(); else sh.after_write();
 #if DBP_NL_PUBLISH_F
     if (!factors) {
       float fv[16];
