@@ -52,15 +52,21 @@ extern "C" {
 #define DBP_ARR_NONLINEAR_FIRST 2
 
 #define DBP_MAX_SIDE_COEFFS 64   /* EssfmCoefficients.n_coeffs supported   */
-#define DBP_MIN_BLOCK_LEN 16     /* OverlapPlan.block_len range on the GPU */
+/* OverlapPlan.block_len: any power of two up to 2^DBP_MAX_LOG2_BLOCK (the
+ * reference accepts any power of two, spectral.py:72-76).  Lengths in
+ * [DBP_MIN_BLOCK_LEN, DBP_MAX_BLOCK_LEN] run the fused block kernel; shorter
+ * and longer blocks the float64 multi-kernel path (dbp_general.cuh), with
+ * the same entry points and results within the same tolerance.             */
+#define DBP_MIN_BLOCK_LEN 16
 #define DBP_MAX_BLOCK_LEN 8192
+#define DBP_MAX_LOG2_BLOCK 22
 
 typedef struct dbp_plan dbp_plan;
 
 /* Message of the last failure on this thread ("" if none). */
 const char* dbp_last_error(void);
 
-/* ABI version (major * 100 + minor). */
+/* ABI version (major * 100 + minor): 102 adds the general block-length path. */
 int dbp_version(void);
 
 /* Number of visible CUDA devices (0 when none). */

@@ -18,7 +18,11 @@ LIB_PATH = Path(os.environ.get("DBP_LIB") or Path(__file__).resolve().parent / "
 DBP_OK, DBP_EINVAL, DBP_ECUDA, DBP_ENOMEM, DBP_ESTATE = 0, -1, -2, -3, -4
 ALG_CODES = {"ffe": 0, "ssfm": 1, "essfm": 2, "rotate": 3, "identity": 4}
 ARR_CODES = {"symmetric": 0, "linear-first": 1, "nonlinear-first": 2}
-MIN_BLOCK_LEN, MAX_BLOCK_LEN, MAX_SIDE_COEFFS = 16, 8192, 64
+# any power-of-two block length in [MIN_BLOCK_LEN, MAX_BLOCK_LEN]; the fused
+# block kernel covers [FUSED_MIN_BLOCK_LEN, FUSED_MAX_BLOCK_LEN], the rest runs
+# the float64 multi-kernel path (csrc/dbp_general.cuh)
+MIN_BLOCK_LEN, MAX_BLOCK_LEN, MAX_SIDE_COEFFS = 1, 1 << 22, 64
+FUSED_MIN_BLOCK_LEN, FUSED_MAX_BLOCK_LEN = 16, 8192
 
 # every symbol include/dbp_b200.h declares, with (restype, argtypes)
 _c_int, _c_void_p, _c_int64, _c_double_p = ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double)

@@ -19,6 +19,8 @@
 #include <vector>
 
 #include "../../include/dbp_b200.h"
+#include "dbp_general.cuh"
+#include "fft64.cuh"
 #include "host_pool.h"
 #include "launch.h"
 
@@ -125,6 +127,17 @@ struct dbp_plan {
   size_t pin_bytes = 0;
   cudaEvent_t done[2] = {nullptr, nullptr};
   dbp::HostPool* pool = nullptr;   // the process-wide conversion pool (not owned)
+  // block lengths outside the fused kernel's [16, 8192]: the float64
+  // multi-kernel path (dbp_general.cuh) with natural-order float64 tables
+  bool general = false;
+  double2* d_full64 = nullptr;
+  double2* d_half64 = nullptr;
+  std::vector<double2> steps64;   // (a_j, g_j) in float64
+  double c64[dbp::kMaxSideCoeffs + 1] = {};
+  double2* d_ws = nullptr;        // [block][pol][N] complex128 workspace ...
+  double2* d_work = nullptr;      // ... the FFT's ping-pong partner ...
+  double* d_inten = nullptr;      // ... and [block][N] intensities
+  long long ws_blocks = 0;
 };
 
 namespace {
@@ -173,7 +186,7 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   }
   kp.nc = p->nc;
   kp.fir_pad = (p->nc + 3) & ~3;
-  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().double_buffer);
+  kp.slice_floats = p->general ? 0 : dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().double_buffer);
   kp.precise_sincos = p->n_steps >= 3 ? 1 : 0;
   kp.tab_full = p->d_full;
   kp.tab_half = p->d_half ? p->d_half : p->d_full;
@@ -188,8 +201,82 @@ void base_params(const dbp_plan* p, dbp::KernelParams& kp) {
   std::memcpy(kp.c, p->c, sizeof(kp.c));
 }
 
+// The float64 multi-kernel path for block lengths outside [16, 8192]
+// (dbp_general.cuh): the same KernelParams contract as the fused kernel.
+int launch_general(const dbp_plan* cp, const dbp::KernelParams& kp, cudaStream_t s) {
+  dbp_plan* p = const_cast<dbp_plan*>(cp);   // workspace grows lazily
+  namespace dg = dbp_general;
+  const long long n = p->N;
+  // chunk of blocks whose workspace (2 x 2 N complex128 + N float64 per block) fits ~768 MB
+  const long long per_block = 2 * 2 * n * (long long)sizeof(double2) + n * (long long)sizeof(double);
+  static const long long budget = [] {   // DBP_GENERAL_WS_MB: workspace budget (tests force small chunks)
+    const char* v = std::getenv("DBP_GENERAL_WS_MB");
+    const long long mb = v && *v ? std::atoll(v) : 768;
+    return (mb > 0 ? mb : 768) << 20;
+  }();
+  long long chunk = budget / per_block;
+  if (chunk < 1) chunk = 1;
+  if (chunk > kp.total_blocks) chunk = kp.total_blocks;
+  if (p->ws_blocks < chunk) {
+    cudaFree(p->d_ws);
+    cudaFree(p->d_work);
+    cudaFree(p->d_inten);
+    p->d_ws = p->d_work = nullptr;
+    p->d_inten = nullptr;
+    p->ws_blocks = 0;
+    if (cudaMalloc(&p->d_ws, chunk * 2 * n * sizeof(double2)) != cudaSuccess ||
+        cudaMalloc(&p->d_work, chunk * 2 * n * sizeof(double2)) != cudaSuccess ||
+        cudaMalloc(&p->d_inten, chunk * n * sizeof(double)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(DBP_ENOMEM, "workspace cudaMalloc failed for the general block-length path");
+    }
+    p->ws_blocks = chunk;
+  }
+  dg::Taps taps{};
+  for (int i = 0; i <= p->nc && i < dg::kMaxTaps; ++i) taps.c[i] = p->c64[i];
+  long long launches = 0;
+  for (long long blk0 = 0; blk0 < kp.total_blocks; blk0 += chunk) {
+    const long long nblk = std::min(chunk, kp.total_blocks - blk0);
+    const long long rows = 2 * nblk;
+    double2* cur = p->d_ws;
+    double2* oth = p->d_work;
+    dg::frame_kernel<<<dg::grid_for(rows * n), dg::kThreads, 0, s>>>(kp, blk0, nblk, n, cur);
+    ++launches;
+    for (int op = 0; op < kp.n_ops; ++op) {
+      const bool is_conv = kp.conv_all || (op & 1) == kp.conv_parity;
+      if (is_conv) {
+        const bool half = kp.half_ends && (op == 0 || op == kp.n_ops - 1);
+        const double2* tab = half && p->d_half64 ? p->d_half64 : p->d_full64;
+        double2* r = fft64::transform(cur, oth, n, rows, false, false, s, &launches);
+        if (!r) return cuda_fail(cudaGetLastError(), "general path forward FFT");
+        if (r != cur) std::swap(cur, oth);
+        dg::mul_kernel<<<dg::grid_for(rows * n), dg::kThreads, 0, s>>>(cur, tab, rows * n, n);
+        ++launches;
+        r = fft64::transform(cur, oth, n, rows, true, false, s, &launches);   // 1/N is in the table
+        if (!r) return cuda_fail(cudaGetLastError(), "general path inverse FFT");
+        if (r != cur) std::swap(cur, oth);
+      } else {
+        const int sidx = op >> kp.sidx_shift;
+        if (sidx < 0 || sidx >= (int)p->steps64.size()) return fail(DBP_ESTATE, "step index outside the program");
+        const int nc = kp.coeff_stride ? kp.nc : p->nc;
+        dg::intensity_kernel<<<dg::grid_for(nblk * n), dg::kThreads, 0, s>>>(cur, p->d_inten, nblk, n);
+        dg::rotate_kernel<<<dg::grid_for(nblk * n), dg::kThreads, 0, s>>>(
+            cur, p->d_inten, nblk, n, kp, blk0, taps, nc, p->steps64[sidx].x, p->steps64[sidx].y);
+        launches += 2;
+      }
+    }
+    dg::store_kernel<<<dg::grid_for(rows * (long long)kp.step), dg::kThreads, 0, s>>>(cur, kp, blk0, nblk, n);
+    ++launches;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "general block-length path launch");
+  g_launches.fetch_add(launches, std::memory_order_relaxed);
+  return DBP_OK;
+}
+
 int launch(const dbp_plan* p, const dbp::KernelParams& kp, cudaStream_t s) {
   if (kp.total_blocks <= 0) return DBP_OK;
+  if (p->general) return launch_general(p, kp, s);
   const Dispatch& d = dispatch();
   const dbp::LaunchShape sh = d.shape[p->logn]();
   const long long ctas = (kp.total_blocks + sh.slices - 1) / sh.slices;
@@ -264,7 +351,7 @@ extern "C" {
 
 const char* dbp_last_error(void) { return g_last_error.c_str(); }
 
-int dbp_version(void) { return 101; }
+int dbp_version(void) { return 102; }
 
 int64_t dbp_launch_count(void) { return g_launches.load(); }
 
@@ -287,8 +374,9 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
   const int logn = ilog2_exact(block_len);
   if (logn < 0) return fail(DBP_EINVAL, "block_len must be a power of two, got " + std::to_string(block_len));
   if (!(0 <= overlap && overlap < block_len)) return fail(DBP_EINVAL, "overlap must satisfy 0 <= overlap < block_len");
-  if (logn < dbp::kMinLogN || logn > dbp::kMaxLogN)
-    return fail(DBP_EINVAL, "block_len " + std::to_string(block_len) + " outside the GPU range [16, 8192]");
+  if (logn > DBP_MAX_LOG2_BLOCK)
+    return fail(DBP_EINVAL, "block_len " + std::to_string(block_len) + " above the supported 2^" +
+                                std::to_string(DBP_MAX_LOG2_BLOCK));
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
     cudaGetLastError();
@@ -305,6 +393,11 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
   p->logn = logn;
   p->step = block_len - overlap;
   p->lead = overlap / 2;
+  p->general = logn < dbp::kMinLogN || logn > dbp::kMaxLogN;
+  if (p->general) {   // the float64 path needs no block-FFT tables
+    *out = p;
+    return DBP_OK;
+  }
   std::vector<float2> tw = dbp::make_twiddles(logn);
   int rc = upload(&p->d_tw, tw);
   if (rc == DBP_OK && dbp::warp_ffe_supported(logn)) rc = upload(&p->d_wtw, dbp::make_warp_twiddles(logn, &dbp::unit_float2));
@@ -340,6 +433,11 @@ int dbp_plan_destroy(dbp_plan* p) {
   cudaFree(p->d_steps);
   cudaFree(p->d_coeff);
   cudaFree(p->d_coeff_batch);
+  cudaFree(p->d_full64);
+  cudaFree(p->d_half64);
+  cudaFree(p->d_ws);
+  cudaFree(p->d_work);
+  cudaFree(p->d_inten);
   delete p;
   return DBP_OK;
 }
@@ -356,6 +454,37 @@ int dbp_plan_set_linear(dbp_plan* p, const double* kernel, const double* half_ke
   if (!kernel) return fail(DBP_EINVAL, "null kernel");
   DeviceGuard g(p->device);
   const double inv_n = 1.0 / (double)p->N;
+  if (p->general) {
+    // natural bin order, float64, 1/N folded in (the inverse FFT is unscaled)
+    auto convert64 = [&](const double* src, std::vector<double2>& h) {
+      h.resize(p->N);
+      for (int k = 0; k < p->N; ++k) {
+        if (!std::isfinite(src[2 * k]) || !std::isfinite(src[2 * k + 1])) return false;
+        h[k] = make_double2(src[2 * k] * inv_n, src[2 * k + 1] * inv_n);
+      }
+      return true;
+    };
+    std::vector<double2> h, hh;
+    if (!convert64(kernel, h)) return fail(DBP_EINVAL, "kernel must be finite");
+    if (half_kernel && !convert64(half_kernel, hh)) return fail(DBP_EINVAL, "half kernel must be finite");
+    p->have_full = false;
+    p->have_half = false;
+    auto up = [&](double2** dst, const std::vector<double2>& src) -> int {
+      if (!*dst) DBP_CUDA(cudaMalloc(dst, src.size() * sizeof(double2)), "cudaMalloc(table64)");
+      DBP_CUDA(cudaMemcpy(*dst, src.data(), src.size() * sizeof(double2), cudaMemcpyHostToDevice),
+               "cudaMemcpy(table64)");
+      return DBP_OK;
+    };
+    int rc = up(&p->d_full64, h);
+    if (rc != DBP_OK) return rc;
+    if (half_kernel) {
+      rc = up(&p->d_half64, hh);
+      if (rc != DBP_OK) return rc;
+    }
+    p->have_full = true;
+    p->have_half = half_kernel != nullptr;
+    return DBP_OK;
+  }
   const int T = p->N / 16;
   // stored in the kernel's register order: entry tab_index(t, e) holds the bin
   // that register e of thread t carries after the last forward FFT pass
@@ -420,8 +549,11 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
   // validate everything into locals; the plan changes only once every check passed
   float c[dbp::kMaxSideCoeffs + 4] = {};
   c[0] = 1.0f;
+  double c64[dbp::kMaxSideCoeffs + 1] = {};
+  c64[0] = 1.0;
   int nc = 0;
   std::vector<float2> st;
+  std::vector<double2> st64;
   const bool no_steps = algorithm == DBP_ALG_FFE || algorithm == DBP_ALG_IDENTITY;
   if (!no_steps) {
     if (num_steps < 1) return fail(DBP_EINVAL, "num_steps must be >= 1");
@@ -438,12 +570,15 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
       // trailing zero side taps contribute fma(0, s, acc) == acc: drop them (bit-identical)
       while (nc > 0 && (float)coeffs[nc] == 0.0f) --nc;
       for (int i = 0; i <= nc; ++i) c[i] = (float)coeffs[i];
+      for (int i = 0; i <= nc; ++i) c64[i] = coeffs[i];
     }
     st.resize(num_steps);
+    st64.resize(num_steps);
     for (int j = 0; j < num_steps; ++j) {
       if (!std::isfinite(weights[j]) || !std::isfinite(gains[j])) return fail(DBP_EINVAL, "schedule must be finite");
       // reference rotation exp(-j * gamma * w * F)  ==  exp(+j * a * F), a = -gamma * w
       st[j] = make_float2((float)(-gamma * weights[j]), (float)gains[j]);
+      st64[j] = make_double2(-gamma * weights[j], gains[j]);
     }
   }
   DeviceGuard g(p->device);
@@ -465,6 +600,8 @@ int dbp_plan_set_steps(dbp_plan* p, int algorithm, int arrangement, int num_step
   p->program = algorithm;
   p->arrangement = arrangement;
   std::memcpy(p->c, c, sizeof(c));
+  std::memcpy(p->c64, c64, sizeof(c64));
+  p->steps64 = st64;
   p->nc = nc;
   p->n_steps = no_steps ? 0 : num_steps;
   p->have_steps = true;
@@ -861,7 +998,7 @@ int dbp_run_coeff_batch(dbp_plan* p, const void* d_in, void* d_out, int64_t n_to
   base_params(p, kp);
   kp.nc = p->batch_nc;
   kp.fir_pad = (p->batch_nc + 3) & ~3;
-  kp.slice_floats = dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().double_buffer);
+  kp.slice_floats = p->general ? 0 : dbp::slice_floats(p->N, kp.fir_pad, dispatch().shape[p->logn]().double_buffer);
   kp.coeff = p->d_coeff_batch;
   kp.coeff_stride = p->batch_stride;
   kp.in = static_cast<const float2*>(d_in);

@@ -47,8 +47,10 @@ def test_invalid_geometry_rejected_before_device_lookup():
     assert lib.dbp_plan_create(ctypes.byref(h), 0, 1000, 100) == _native.DBP_EINVAL
     assert b"power of two" in lib.dbp_last_error()
     assert lib.dbp_plan_create(ctypes.byref(h), 0, 1024, 1024) == _native.DBP_EINVAL
-    assert lib.dbp_plan_create(ctypes.byref(h), 0, 16384, 0) == _native.DBP_EINVAL
-    assert b"GPU range" in lib.dbp_last_error()
+    # any power of two up to 2^22 (the general path beyond the fused kernel's 8192)
+    assert lib.dbp_plan_create(ctypes.byref(h), 0, 1 << 23, 0) == _native.DBP_EINVAL
+    assert b"above the supported" in lib.dbp_last_error()
+    assert lib.dbp_version() >= 102
 
 
 def test_missing_library_fails_loudly(tmp_path):

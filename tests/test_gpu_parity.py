@@ -630,3 +630,76 @@ def test_r2t_matches_oracle_in_subprocess():
                           "or (fir_paths and 8192) or random_configurations"],
                          cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-2000:]
+
+
+# ---------------------------------------------------------------------------
+# Block lengths outside the fused kernel's [16, 8192]: the float64
+# multi-kernel path (csrc/dbp_general.cuh).  The reference accepts any
+# power-of-two block (spectral.py:72-76); same API, same parity bar.
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n_blk,m", [(1, 0), (2, 1), (4, 2), (8, 3), (16384, 2048), (32768, 700)])
+@pytest.mark.parametrize("alg,arr,steps", [("essfm", "symmetric", 1), ("ssfm", "linear-first", 3),
+                                           ("essfm", "nonlinear-first", 2), ("ffe", "symmetric", 1)])
+def test_general_block_lengths_match_oracle(n_blk, m, alg, arr, steps):
+    rng = np.random.default_rng(n_blk * 7 + steps)
+    n = 3 * n_blk + 77 if n_blk >= 16384 else 301
+    span = pb.FiberParams(-21.68, 1.3, 0.2, 80.0)
+    link = quiet_link(3, span)   # 3 spans: N_s = 2 puts a step boundary mid-span (gain != 1)
+    nc = 0 if n_blk <= 2 else min(3, (n_blk - 1) // 2) if n_blk < 16384 else 17
+    coeffs = None if alg != "essfm" else pb.EssfmCoefficients(np.r_[1.0, 0.05 * rng.normal(size=nc)])
+    cfg = pb.DbpConfig(alg, pb.OverlapPlan(n_blk, m), link, num_steps=steps, coeffs=coeffs, arrangement=arr)
+    x = (0.01 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))).astype(np.complex64)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        got = pb.backpropagate(pb.DualPolSignal(x[0], x[1], 56e9), cfg).stack()
+    want = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(cfg))
+    if n_blk - m >= 16:
+        err = dbp_port.per_block_rel_l2(got, want, n_blk, m).max()
+    else:   # tiny kept segments: whole-signal bar (a 1-sample segment has no meaningful norm)
+        err = rel_l2(got, want)
+    assert err <= 1e-6, (n_blk, m, alg, arr, err)   # float64 inside: only the complex64 I/O rounding
+
+
+def test_general_block_length_multi_chunk_and_chunk_mode_in_subprocess():
+    # a small workspace budget (DBP_GENERAL_WS_MB) forces many block chunks;
+    # the chunk-mode entry (dbp_run_chunk over two halves) must equal the
+    # whole-signal run bit for bit, and the identity program must frame exactly
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    code = r'''
+import numpy as np, torch, warnings
+import paper_1507_00921_b200 as pb
+from oracle import dbp_port
+from tests.helpers import quiet_link, port_config
+rng = np.random.default_rng(5)
+N, M, n = 16384, 1000, 16384 * 9 + 5
+span = pb.FiberParams(-21.68, 1.3, 0.2, 80.0)
+cfg = pb.DbpConfig("essfm", pb.OverlapPlan(N, M), quiet_link(40, span), num_steps=1,
+                   coeffs=pb.EssfmCoefficients(np.r_[1.0, 0.1, -0.02]))
+x = (0.02 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))).astype(np.complex64)
+with warnings.catch_warnings():
+    warnings.simplefilter("ignore")
+    eng = pb.get_engine(cfg, 56e9)
+got = eng.run_host(x[None])[0]
+want = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(cfg))
+err = dbp_port.per_block_rel_l2(got, want, N, M).max()
+assert err <= 1e-6, err
+nb = eng.num_blocks(n)
+h = nb // 2
+parts = [eng.run_host(x[None], block_range=(0, h))[0], eng.run_host(x[None], block_range=(h, nb))[0]]
+step = N - M
+joined = np.concatenate([parts[0][:, :h * step], parts[1][:, h * step:]], axis=1)
+assert np.array_equal(joined, got)
+ident = pb.overlap_save_run(pb.DualPolSignal(x[0], x[1], 56e9), pb.OverlapPlan(N, M),
+                            pb.identity_processor(pb.OverlapPlan(N, M), 56e9))
+assert np.array_equal(ident.stack(), x.astype(np.complex128))
+print("ok", err)
+'''
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, DBP_GENERAL_WS_MB="3")
+    res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0 and "ok" in res.stdout, res.stdout[-2000:] + res.stderr[-3000:]
