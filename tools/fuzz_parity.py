@@ -1,6 +1,6 @@
 """Randomised parity sweep of the GPU paths against the CPU oracle (evidence run).
 
-    python tools/fuzz_parity.py [--dbp 600] [--sim 60] [--rx 24] [--out profiles/r1/fuzz_parity.json]
+    python tools/fuzz_parity.py [--dbp 600] [--general 0] [--sim 60] [--rx 24] [--out profiles/r1/fuzz_parity.json]
 
 DBP: random block length 16..8192, overlap, ragged length, algorithm,
 arrangement, 1..8 steps, 1..8 spans of 20..100 km, N_c 0..64, batch 1..3,
@@ -30,6 +30,8 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--dbp", type=int, default=1500)
+    ap.add_argument("--general", type=int, default=0,
+                    help="extra DBP items at N = 1 .. 8, 16384, 32768 (the general block-length path)")
     ap.add_argument("--sim", type=int, default=60)
     ap.add_argument("--rx", type=int, default=24)
     ap.add_argument("--seed", type=int, default=20261020)
@@ -43,8 +45,12 @@ def main():
     res = {"dbp": {"cases": 0, "worst": 0.0, "violations": 0, "worst_case": None},
            "sim": {"cases": 0, "worst_ratio": 0.0, "violations": 0},
            "rx": {"cases": 0, "worst_eq_diff": 0.0, "count_mismatches": 0}}
-    for case in range(a.dbp):
-        logn = int(gen.integers(4, 14))
+    for case in range(a.dbp + a.general):
+        if case < a.dbp:
+            logn = int(gen.integers(4, 14))
+        else:   # block lengths outside the fused kernel (the float64 general path)
+            logn = (0, 1, 2, 3, 14, 15)[int(gen.integers(0, 6))]
+            res["dbp"]["general_cases"] = res["dbp"].get("general_cases", 0) + 1
         nb = 1 << logn
         m = int(gen.integers(0, nb))
         n = int(gen.integers(1, 4 * nb + 2))
