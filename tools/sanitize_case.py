@@ -19,6 +19,9 @@ cases = [
     ("ffe", 4096, 1024, 1, 0, "symmetric", 4100),
     ("essfm", 16, 4, 1, 3, "symmetric", 37),
     ("essfm", 256, 60, 3, 23, "symmetric", 700),
+    # the float64 general path (N outside [16, 8192])
+    ("essfm", 8, 3, 2, 3, "linear-first", 29),
+    ("essfm", 16384, 2000, 1, 17, "symmetric", 20000),
 ]
 for alg, n_blk, m, steps, nc, arr, n in cases:
     c = None
