@@ -703,3 +703,31 @@ print("ok", err)
     res = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True,
                          timeout=600)
     assert res.returncode == 0 and "ok" in res.stdout, res.stdout[-2000:] + res.stderr[-3000:]
+
+
+def test_general_block_length_coefficient_batch_matches_oracle():
+    # per-item coefficient sets (the training batch, dbp_run_host_coeff_batch)
+    # on the general path: each set against the oracle with that set
+    # (the batch entry carries float32 coefficients, so the oracle gets them rounded)
+    rng = np.random.default_rng(11)
+    N, M, n = 16384, 1500, 40000
+    span = pb.FiberParams(-21.68, 1.3, 0.2, 80.0)
+    sets = np.stack([np.r_[1.0, 0.1 * rng.normal(size=5)] for _ in range(3)])
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(N, M), quiet_link(10, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(sets[0]))
+    x = (0.02 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))).astype(np.complex64)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        eng = pb.DbpEngine(cfg, 56e9)
+    try:
+        eng.native.set_coeff_batch(sets)
+        out = np.zeros((3, 2, n), np.complex64)
+        eng.native.run_host_coeff_batch(x, out, n)
+    finally:
+        eng.close()
+    for i in range(3):
+        c32 = sets[i].astype(np.float32).astype(np.float64)
+        ci = pb.DbpConfig("essfm", pb.OverlapPlan(N, M), quiet_link(10, span), num_steps=1,
+                          coeffs=pb.EssfmCoefficients(c32))
+        want = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(ci))
+        assert dbp_port.per_block_rel_l2(out[i], want, N, M).max() <= 1e-6, i
