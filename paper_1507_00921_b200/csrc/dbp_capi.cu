@@ -247,12 +247,12 @@ int launch_general(const dbp_plan* cp, const dbp::KernelParams& kp, cudaStream_t
       if (is_conv) {
         const bool half = kp.half_ends && (op == 0 || op == kp.n_ops - 1);
         const double2* tab = half && p->d_half64 ? p->d_half64 : p->d_full64;
-        double2* r = fft64::transform(cur, oth, n, rows, false, false, s, &launches);
+        double2* r = dg::transform16(cur, oth, n, rows, false, s, &launches);
         if (!r) return cuda_fail(cudaGetLastError(), "general path forward FFT");
         if (r != cur) std::swap(cur, oth);
         dg::mul_kernel<<<dg::grid_for(rows * n), dg::kThreads, 0, s>>>(cur, tab, rows * n, n);
         ++launches;
-        r = fft64::transform(cur, oth, n, rows, true, false, s, &launches);   // 1/N is in the table
+        r = dg::transform16(cur, oth, n, rows, true, s, &launches);   // 1/N is in the table
         if (!r) return cuda_fail(cudaGetLastError(), "general path inverse FFT");
         if (r != cur) std::swap(cur, oth);
       } else {
