@@ -118,7 +118,7 @@ def kernel_name(a) -> str:
     logn = int(math.log2(a.block_len))
     if logn < 4 or logn > 13:
         # outside the fused kernel's range: the float64 multi-kernel path (csrc/dbp_general.cuh)
-        return "dbp_general::* + fft64::stockham_pass (float64 multi-kernel path)"
+        return "dbp_general::stockham_pass16 + frame/mul/rotate/store (float64 multi-kernel path)"
     if logn == 13 and a.algorithm != "ffe":
         # N = 8192 split-step programs: the radix-2-around-4096 kernel (csrc/dbp_r2_kernel.cuh)
         return f"dbp::dbp_r2_kernel<{kernel_prog(a)}, {kernel_twp(a)}>"
