@@ -31,6 +31,12 @@
 #ifndef DBP_R2
 #define DBP_R2 1
 #endif
+#ifndef DBP_R2_TMA_STORE
+#define DBP_R2_TMA_STORE 1    // kept centres out through shared memory and the TMA bulk engine
+#endif
+#ifndef DBP_R2_PAIR_STORE
+#define DBP_R2_PAIR_STORE 1   // 16-byte (even, odd) output pairs; 0: 8-byte stores
+#endif
 
 namespace dbp {
 
@@ -352,13 +358,54 @@ __global__ void __launch_bounds__(R2Geo::THREADS, 1) dbp_r2_kernel(const KernelP
     const long long ob = b * kp.step - kp.lead - kp.out_origin;
     const long long rem = kp.n_total - b * kp.step;
     const int hi = kp.lead + (rem < kp.step ? (int)rem : kp.step);
+    // positions 2 (t + 256 m) + a: the even / odd pair is adjacent in the output
+    // row, so it leaves as one coalesced 16-byte store when the kept range and
+    // the row are pair-aligned (8-byte stores, half a warp's sectors each, held
+    // the LSU queue: lg_throttle was the top memory stall, profiles/r2/r2/)
+    const bool pairs = DBP_R2_PAIR_STORE && ((ob | kp.lead | hi) & 1) == 0 &&
+                       (reinterpret_cast<uintptr_t>(pout + ob) & 15) == 0;
+    // TMA bulk store (CTA-uniform condition): the kept centres of both
+    // polarisations staged in the free exchange planes as [pol][step], two
+    // bulk copies issued by one thread, which alone waits for the engine to
+    // have read them (the loop's closing barrier then frees the planes)
+    float2* row_x = kp.out + item * kp.out_item_stride + (b * kp.step - kp.out_origin);
+    const int len = hi - kp.lead;
+    // (step even: the y row's staging starts 16-byte aligned; len even: whole 16-byte units)
+    const bool bulk = DBP_R2_TMA_STORE && ((len | kp.lead | kp.step) & 1) == 0 && (kp.out_pol_stride & 1) == 0 &&
+                      (reinterpret_cast<uintptr_t>(row_x) & 15) == 0;
+    if (bulk) {
+      __syncthreads();   // every warp has left the planes
+      float2* stg = reinterpret_cast<float2*>(smem) + pol * kp.step - kp.lead;
 #pragma unroll
-    for (int m = 0; m < 16; ++m)
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int j = 2 * (t + T * m) + a;
-        if (j >= kp.lead && j < hi) __stcs(pout + ob + j, v[a][m]);
+      for (int m = 0; m < 16; ++m) {
+        const int j = 2 * (t + T * m);
+        if (j >= kp.lead && j < hi)
+          *reinterpret_cast<float4*>(stg + j) = make_float4(v[0][m].x, v[0][m].y, v[1][m].x, v[1][m].y);
       }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const float2* src = reinterpret_cast<const float2*>(smem);
+        bulk_store(row_x, src, (uint32_t)len * 8u);
+        bulk_store(row_x + kp.out_pol_stride, src + kp.step, (uint32_t)len * 8u);
+        bulk_store_commit_and_wait_read();
+      }
+    } else if (pairs) {
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int j = 2 * (t + T * m);
+        if (j >= kp.lead && j < hi)
+          __stcs(reinterpret_cast<float4*>(pout + ob + j), make_float4(v[0][m].x, v[0][m].y, v[1][m].x, v[1][m].y));
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 16; ++m)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          const int j = 2 * (t + T * m) + a;
+          if (j >= kp.lead && j < hi) __stcs(pout + ob + j, v[a][m]);
+        }
+    }
     __syncthreads();   // the next block's first exchange reuses the planes
   }
 }

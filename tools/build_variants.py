@@ -59,6 +59,8 @@ VARIANTS = {
     "wcta4": ["-DDBP_WARP_MIN_CTAS=4"],
     "pubf0": ["-DDBP_NL_PUBLISH_F=0"],
     "nonlbar": ["-DDBP_EXPERIMENT_NONLBAR=1"],   # timing ceiling only: wrong results
+    "r2nopair": ["-DDBP_R2_PAIR_STORE=0", "-DDBP_R2_TMA_STORE=0"],
+    "r2pair": ["-DDBP_R2_TMA_STORE=0"],
     "nodit": ["-DDBP_DIT_MAX_STEPS=0"],
     "dit4": ["-DDBP_DIT_MAX_STEPS=4"],
     "noload": ["-DDBP_EXPERIMENT_NOLOAD=1"],      # timing ceilings only: wrong results
