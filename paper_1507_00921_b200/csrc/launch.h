@@ -265,7 +265,8 @@ auto select_r2_kernel(const KernelParams& kp) {
   return kernel;
 }
 
-inline cudaError_t launch_r2(const KernelParams& kp0, cudaStream_t stream) {
+template <int LOGN>
+cudaError_t launch_r2(const KernelParams& kp0, cudaStream_t stream) {
   KernelParams kp = kp0;
   kp.slice_floats = r2_slice_floats(kp.fir_pad);
   const size_t smem = (size_t)kp.slice_floats * sizeof(float);
@@ -301,7 +302,10 @@ auto select_r2t_kernel(const KernelParams& kp) {
   return kernel;
 }
 
-inline cudaError_t launch_r2t(const KernelParams& kp0, cudaStream_t stream) {
+// (templates on the block length so only the N = 8192 translation unit
+// instantiates the R2 / R2T kernels)
+template <int LOGN>
+cudaError_t launch_r2t(const KernelParams& kp0, cudaStream_t stream) {
   KernelParams kp = kp0;
   kp.slice_floats = r2t_slice_floats(kp.fir_pad);
   const size_t smem = (size_t)kp.slice_floats * sizeof(float);
@@ -322,8 +326,8 @@ cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, s
                                      cudaStream_t stream) {
   if constexpr (LOGN == 13) {
     if (kp.r2_full != nullptr && kp.r2_tw != nullptr && (kp.half_ends == 0 || kp.r2_half != nullptr)) {
-      if (r2t_enabled(kp)) return launch_r2t(kp, stream);
-      if (r2_enabled(kp)) return launch_r2(kp, stream);
+      if (r2t_enabled(kp)) return launch_r2t<LOGN>(kp, stream);
+      if (r2_enabled(kp)) return launch_r2<LOGN>(kp, stream);
     }
   }
   if constexpr (LOGN == 13) {
