@@ -31,6 +31,9 @@
 #ifndef DBP_R2
 #define DBP_R2 1
 #endif
+#ifndef DBP_R2_LOOP_BARRIER
+#define DBP_R2_LOOP_BARRIER 0
+#endif
 #ifndef DBP_R2_TMA_STORE
 #define DBP_R2_TMA_STORE 1    // kept centres out through shared memory and the TMA bulk engine
 #endif
@@ -406,7 +409,13 @@ __global__ void __launch_bounds__(R2Geo::THREADS, 1) dbp_r2_kernel(const KernelP
           if (j >= kp.lead && j < hi) __stcs(pout + ob + j, v[a][m]);
         }
     }
+#if DBP_R2_LOOP_BARRIER
     __syncthreads();   // the next block's first exchange reuses the planes
+#endif
+    // (no barrier needed here: every first shared-memory write of the next
+    // block -- the forward exchange, the FIR buffers, the store staging --
+    // sits behind its own __syncthreads, which thread 0 reaches only after
+    // its bulk store has read the staging)
   }
 }
 

@@ -61,6 +61,7 @@ VARIANTS = {
     "nonlbar": ["-DDBP_EXPERIMENT_NONLBAR=1"],   # timing ceiling only: wrong results
     "r2nopair": ["-DDBP_R2_PAIR_STORE=0", "-DDBP_R2_TMA_STORE=0"],
     "r2pair": ["-DDBP_R2_TMA_STORE=0"],
+    "r2loopbar": ["-DDBP_R2_LOOP_BARRIER=1"],
     "nodit": ["-DDBP_DIT_MAX_STEPS=0"],
     "dit4": ["-DDBP_DIT_MAX_STEPS=4"],
     "noload": ["-DDBP_EXPERIMENT_NOLOAD=1"],      # timing ceilings only: wrong results
