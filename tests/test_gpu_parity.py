@@ -731,3 +731,33 @@ def test_general_block_length_coefficient_batch_matches_oracle():
                           coeffs=pb.EssfmCoefficients(c32))
         want = dbp_port.backpropagate_arrays(x.astype(np.complex128), 56e9, port_config(ci))
         assert dbp_port.per_block_rel_l2(out[i], want, N, M).max() <= 1e-6, i
+
+
+@pytest.mark.parametrize("n_blk,m,alg", [(8192, 1400, "essfm"), (8192, 1023, "ssfm"), (8192, 1024, "ffe"),
+                                         (4096, 701, "essfm"), (16384, 2000, "essfm")])
+def test_chunk_mode_and_block_ranges_bit_equal_whole_every_kernel(rng, n_blk, m, alg):
+    # the multi-GPU contract on the N = 8192 R2 kernel (its TMA / paired / 8-byte
+    # output stores: odd M makes the kept ranges odd), the FFE pairs, the
+    # 4096 kernel and the general path: chunk mode and host block ranges
+    # reproduce the whole-signal result bit for bit
+    torch = pytest.importorskip("torch")
+    coeffs = pb.EssfmCoefficients(waveforms.gaussian_coeffs(9)) if alg == "essfm" else None
+    cfg = pb.DbpConfig(alg, pb.OverlapPlan(n_blk, m), quiet_link(20, STD), num_steps=2 if alg == "ssfm" else 1,
+                       coeffs=coeffs, arrangement="linear-first" if alg == "ssfm" else "symmetric")
+    n = 5 * n_blk + 333
+    x = (0.03 * (rng.normal(size=(2, n)) + 1j * rng.normal(size=(2, n)))).astype(np.complex64)
+    whole = _run(x, cfg)[0]
+    eng = pb.get_engine(cfg, 56e9, 0)
+    nb = eng.num_blocks(n)
+    cuts = [(0, 2), (2, nb - 1), (nb - 1, nb)]
+    for b0, b1 in cuts:
+        lo, hi = cfg.plan.input_span(b0, b1)
+        span = np.ascontiguousarray(pb.framing.gather_span(x, lo, hi))
+        olo, ohi = cfg.plan.output_span(b0, b1, n)
+        d_in = torch.from_numpy(span.view(np.float32)).cuda()
+        d_out = torch.zeros((2, (ohi - olo) * 2), dtype=torch.float32, device="cuda")
+        eng.native.run_chunk(d_in.data_ptr(), d_out.data_ptr(), n, 1, b0, b1, hi - lo, ohi - olo)
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(d_out.cpu().numpy().view(np.complex64), whole[:, olo:ohi])
+        part = eng.run_host(x[None], block_range=(b0, b1))[0]
+        np.testing.assert_array_equal(part[:, olo:ohi], whole[:, olo:ohi])
