@@ -261,6 +261,50 @@ def time_dropin(a, cfg, dev) -> dict:
     return out
 
 
+def pcie_roof(dev, nbytes: int = 1 << 30, reps: int = 3) -> dict:
+    """The host link's ceiling for the e2e leg, measured on this box: pinned
+    H2D alone, D2H alone and both at once on two streams (the e2e pipeline
+    overlaps the two directions), best of ``reps``, CUDA-event timed."""
+    import torch
+    h_a = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_b = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev}")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{dev}")
+    s1, s2 = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
+
+    def timed(h2d: bool, d2h: bool) -> float:
+        best = float("inf")
+        for _ in range(reps + 1):
+            torch.cuda.synchronize(dev)
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            cur = torch.cuda.current_stream(dev)
+            e0.record(cur)
+            s1.wait_event(e0)
+            s2.wait_event(e0)
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d_a.copy_(h_a, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h_b.copy_(d_b, non_blocking=True)
+            e1.record(s1)
+            e2.record(s2)
+            cur.wait_event(e1)
+            cur.wait_event(e2)
+            e3 = torch.cuda.Event(enable_timing=True)
+            e3.record(cur)
+            torch.cuda.synchronize(dev)
+            best = min(best, e0.elapsed_time(e3) * 1e-3)
+        return best
+
+    timed(True, True)  # warm
+    h2d = nbytes / timed(True, False) / 1e9
+    d2h = nbytes / timed(False, True) / 1e9
+    both = nbytes / timed(True, True) / 1e9   # per direction, both directions at once
+    del h_a, h_b, d_a, d_b
+    return {"h2d_gbs": h2d, "d2h_gbs": d2h, "bidir_gbs_per_direction": both, "bytes_per_copy": nbytes}
+
+
 def run_ours(a) -> int:
     import numpy as np
     import torch
@@ -383,6 +427,16 @@ def run_ours(a) -> int:
         e2e["matches_device_path"] = bool(ok)
         hin.free()
         hout.free()
+        # the e2e leg's own roofline: every step moves Bi host->device and Bo
+        # device->host over the host link, overlapped by the 2-stream pipeline
+        link = pcie_roof(dev)
+        moved = max(e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"])
+        per_dir = moved * a.e2e_steps / e2e_s / 1e9
+        e2e["roofline"] = {"bound": "pcie", "achieved": per_dir, "peak": link["bidir_gbs_per_direction"],
+                           "unit": "GB/s per direction", "frac": per_dir / link["bidir_gbs_per_direction"],
+                           "link": link,
+                           "note": "achieved = bytes copied each way per step / e2e step time; peak = pinned "
+                                   "H2D and D2H copies running at once on this box (measured in this run)"}
         e2e["dropin"] = time_dropin(a, cfg, dev)
 
     # ---- CPU baseline (rank 0, single-GPU runs only) ----

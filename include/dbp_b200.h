@@ -157,6 +157,25 @@ int dbp_plan_set_staging(dbp_plan* plan, size_t bytes);
 int dbp_process_blocks(dbp_plan* plan, const void* d_blocks, void* d_out, int64_t n_blocks,
                        void* stream);
 
+/* Overlap-save framing alone, for block processors the fused kernel cannot
+ * run (spectral.py:84-92 accepts any callable; replaces the cyclic extension
+ * and block cut of overlap_save_run, spectral.py:122-131, and its keep-centre
+ * assembly, spectral.py:138-145).  Pure data movement, bit-exact for either
+ * element width: elem_bytes 8 (complex64) or 16 (complex128).
+ *   dbp_frame_blocks:   d_sig [batch][2][n_total] -> d_blocks
+ *                       [batch][block_end-block_begin][2][block_len], block b
+ *                       holding samples (b step - overlap/2 + j) mod n_total.
+ *   dbp_unframe_blocks: d_blocks (same layout) -> d_out [batch][2][n_total],
+ *                       writing samples [block_begin step, min(n_total,
+ *                       block_end step)) from each block's centre
+ *                       [overlap/2, overlap/2 + step).
+ * Asynchronous on ``stream``; block_len a power of two, 0 <= overlap <
+ * block_len (spectral.py:72-76).                                             */
+int dbp_frame_blocks(const void* d_sig, void* d_blocks, int64_t n_total, int batch, int block_len,
+                     int overlap, int64_t block_begin, int64_t block_end, int elem_bytes, void* stream);
+int dbp_unframe_blocks(const void* d_blocks, void* d_out, int64_t n_total, int batch, int block_len,
+                       int overlap, int64_t block_begin, int64_t block_end, int elem_bytes, void* stream);
+
 /* Per-item coefficient sets for ESSFM training batches (the reference's
  * finite-difference Jacobian evaluates N_c+1 perturbed sets on one
  * waveform, train.py:153-158): ``coeffs`` is [n_sets][n_coeffs + 1]

@@ -38,6 +38,7 @@ from .backprop import (
     filter_processor,
     BlockProcessor,
     GpuBlockProcessor,
+    DeviceBlockProcessor,
 )
 from .spectral import fft, ifft
 
@@ -82,7 +83,7 @@ __all__ = [
     "optimize_coefficients", "save_coefficients", "SsfmStepConfig", "amplify_with_ase",
     "apply_jones_matrix", "haar_random_unitary", "propagate_link", "propagate_link_batch", "propagate_span",
     "random_polarization_rotation", "apply_laser_phase_noise", "linear_substep", "overlap_save_run", "block_processor",
-    "identity_processor", "filter_processor", "BlockProcessor", "GpuBlockProcessor", "fft", "ifft", "AlignmentError", "FrequencyOffsetError", "RxMetrics", "butterfly_equalize",
+    "identity_processor", "filter_processor", "BlockProcessor", "GpuBlockProcessor", "DeviceBlockProcessor", "fft", "ifft", "AlignmentError", "FrequencyOffsetError", "RxMetrics", "butterfly_equalize",
     "butterfly_equalize_batch", "carrier_recover", "carrier_recover_batch", "evm_percent", "measure_ber",
     "qpsk_decide", "qpsk_map", "receive_batch", "__version__",
 ]

@@ -45,6 +45,10 @@ SIGNATURES = {
     "dbp_nonlinear_substep_c128": (_c_int, [_c_int, _c_void_p, _c_void_p, _c_int64, ctypes.c_double,
                                             ctypes.c_double, _c_double_p, _c_int]),
     "dbp_process_blocks": (_c_int, [_c_void_p, _c_void_p, _c_void_p, _c_int64, _c_void_p]),
+    "dbp_frame_blocks": (_c_int, [_c_void_p, _c_void_p, _c_int64, _c_int, _c_int, _c_int, _c_int64, _c_int64,
+                                  _c_int, _c_void_p]),
+    "dbp_unframe_blocks": (_c_int, [_c_void_p, _c_void_p, _c_int64, _c_int, _c_int, _c_int, _c_int64, _c_int64,
+                                    _c_int, _c_void_p]),
     "dbp_plan_synchronize": (_c_int, [_c_void_p]),
     "dbp_host_alloc": (_c_int, [ctypes.POINTER(_c_void_p), ctypes.c_size_t]),
     "dbp_host_free": (_c_int, [_c_void_p]),
@@ -471,6 +475,22 @@ def fit_normal(d_out: int, n_params: int, n_total: int, d_target: int, d_base: i
                                          float(scale), float(fd_step), _dptr(ata), _dptr(atr), stream or None),
            "dbp_fit_normal")
     return ata, atr
+
+
+def frame_blocks(d_sig: int, d_blocks: int, n_total: int, batch: int, block_len: int, overlap: int,
+                 block_begin: int, block_end: int, elem_bytes: int, stream: int = 0):
+    """[batch][2][n] -> [batch][nblk][2][N] cyclic overlap-save blocks (device pointers, async)."""
+    _check(load_library().dbp_frame_blocks(d_sig, d_blocks, int(n_total), int(batch), int(block_len), int(overlap),
+                                           int(block_begin), int(block_end), int(elem_bytes), stream or None),
+           "dbp_frame_blocks")
+
+
+def unframe_blocks(d_blocks: int, d_out: int, n_total: int, batch: int, block_len: int, overlap: int,
+                   block_begin: int, block_end: int, elem_bytes: int, stream: int = 0):
+    """Kept block centres -> output samples [begin step, min(n, end step)) (device pointers, async)."""
+    _check(load_library().dbp_unframe_blocks(d_blocks, d_out, int(n_total), int(batch), int(block_len),
+                                             int(overlap), int(block_begin), int(block_end), int(elem_bytes),
+                                             stream or None), "dbp_unframe_blocks")
 
 
 def fft_c2c(x: np.ndarray, inverse: bool, device: int = 0) -> np.ndarray:

@@ -414,20 +414,102 @@ def filter_processor(plan: OverlapPlan, kernel, sample_rate: float, *, device: i
     return GpuBlockProcessor(None, sample_rate, device, engine=ProgramEngine(plan, sample_rate, device, kernel))
 
 
-def overlap_save_run(sig: DualPolSignal, plan, block_processor, jobs: int = 1) -> DualPolSignal:
-    """spectral.py:87-145 with a GPU block processor: cyclic extension, per-block
-    operator, keep the central ``plan.usable`` samples -- all inside the fused
-    kernel.  Arbitrary Python callables have no GPU path (and there is no CPU
-    fallback): pass ``block_processor(cfg, sample_rate)``."""
+class DeviceBlockProcessor:
+    """A caller-written block operator that runs on the device: ``fn`` maps an
+    (nb, 2, N) complex torch tensor on ``cuda:device`` (every block of the
+    signal at once -- the batched form of spectral.py:84's ``(2, N) -> (2, N)``
+    callable) to a tensor of the same shape.  ``overlap_save_run`` frames the
+    signal into that stack on the GPU (``dbp_frame_blocks``), calls ``fn`` once
+    and assembles the kept centres on the GPU (``dbp_unframe_blocks``).
+    ``dtype``: ``"complex128"`` (the reference's own, default) or
+    ``"complex64"``."""
+
+    def __init__(self, fn, *, device: int = 0, dtype: str = "complex128"):
+        if dtype not in ("complex64", "complex128"):
+            raise ValueError("dtype must be 'complex64' or 'complex128'")
+        self.fn = fn
+        self.device = int(device)
+        self.dtype = dtype
+
+    def __call__(self, blocks):
+        return self.fn(blocks)
+
+
+def _framed_run(sig: DualPolSignal, plan, apply, device: int, dtype: str) -> DualPolSignal:
+    """Overlap-save around ``apply`` (a function of the (nb, 2, N) device block
+    stack): cyclic extension + block cut and keep-centre assembly by the
+    framing kernels -- pure copies, so bit-exact to spectral.py:122-145."""
+    import torch
+
+    from . import _native
+
+    n_total = len(sig)
+    n_blk, m = plan.block_len, plan.overlap
+    nb = -(-n_total // (n_blk - m))   # spectral.py:126 (foreign OverlapPlan objects welcome)
+    wide = dtype == "complex128"
+    np_dt, t_dt, elem = ((np.complex128, torch.complex128, 16) if wide else (np.complex64, torch.complex64, 8))
+    dev = torch.device("cuda", device)
+    x = torch.from_numpy(np.ascontiguousarray(np.stack([np.asarray(sig.x), np.asarray(sig.y)]).astype(np_dt))).to(dev)
+    blocks = torch.empty((nb, 2, n_blk), dtype=t_dt, device=dev)
+    stream = torch.cuda.current_stream(dev).cuda_stream
+    _native.frame_blocks(x.data_ptr(), blocks.data_ptr(), n_total, 1, n_blk, m, 0, nb, elem, stream)
+    proc = apply(blocks)
+    if not isinstance(proc, torch.Tensor) or tuple(proc.shape) != (nb, 2, n_blk):
+        shape = tuple(proc.shape) if hasattr(proc, "shape") else type(proc).__name__
+        raise ValueError(f"block processor returned shape {shape}, expected ({nb}, 2, {n_blk})")
+    proc = proc.to(device=dev, dtype=t_dt).contiguous()
+    out = torch.empty((2, n_total), dtype=t_dt, device=dev)
+    _native.unframe_blocks(proc.data_ptr(), out.data_ptr(), n_total, 1, n_blk, m, 0, nb, elem, stream)
+    o = out.cpu().numpy()
+    return DualPolSignal(o[0].astype(np.complex128), o[1].astype(np.complex128), sig.sample_rate)
+
+
+def overlap_save_run(sig: DualPolSignal, plan, block_processor, jobs: int = 1, *, device: int = 0) -> DualPolSignal:
+    """spectral.py:87-145 on the GPU, for three kinds of block processor:
+
+    * a ``GpuBlockProcessor`` (``block_processor(cfg, fs)``, the identity or a
+      filter): framing, the per-block operator and the keep-centre assembly
+      all inside the fused kernel;
+    * a ``DeviceBlockProcessor``: GPU framing into one (nb, 2, N) device stack,
+      the caller's torch operator on it, GPU assembly;
+    * any other callable on (2, N) numpy blocks (the reference's
+      ``BlockProcessor``): GPU framing in complex128, the caller's function on
+      each block on the host (the caller's own code -- ``jobs`` threads, as in
+      spectral.py:132-136), GPU assembly; bit-identical to the reference for a
+      deterministic callable.  A result of the wrong shape raises the
+      reference's ``ValueError`` (spectral.py:141-142)."""
     if jobs < 1:
         raise ValueError("jobs must be >= 1")
-    if not isinstance(block_processor, GpuBlockProcessor):
-        raise TypeError("overlap_save_run needs a GPU block processor (paper_1507_00921_b200.block_processor); "
-                        "a Python callable cannot run on the GPU path")
-    if (plan.block_len, plan.overlap) != (block_processor.plan.block_len, block_processor.plan.overlap):
-        raise ValueError("plan does not match the block processor's plan")
-    if float(sig.sample_rate) != block_processor.sample_rate:
-        raise ValueError("signal sample rate does not match the block processor's")
-    out = block_processor.engine.run_host(np.stack([np.asarray(sig.x), np.asarray(sig.y)]))[0]
-    return DualPolSignal(out[0].astype(np.complex128), out[1].astype(np.complex128), sig.sample_rate)
+    if isinstance(block_processor, GpuBlockProcessor):
+        if (plan.block_len, plan.overlap) != (block_processor.plan.block_len, block_processor.plan.overlap):
+            raise ValueError("plan does not match the block processor's plan")
+        if float(sig.sample_rate) != block_processor.sample_rate:
+            raise ValueError("signal sample rate does not match the block processor's")
+        out = block_processor.engine.run_host(np.stack([np.asarray(sig.x), np.asarray(sig.y)]))[0]
+        return DualPolSignal(out[0].astype(np.complex128), out[1].astype(np.complex128), sig.sample_rate)
+    if isinstance(block_processor, DeviceBlockProcessor):
+        return _framed_run(sig, plan, block_processor.fn, block_processor.device, block_processor.dtype)
+    if not callable(block_processor):
+        raise TypeError("block_processor must be callable")
+    n_blk = plan.block_len
 
+    def on_host(blocks):
+        import torch
+
+        host = blocks.cpu().numpy()
+        views = [host[b] for b in range(host.shape[0])]
+        if jobs == 1:
+            processed = [block_processor(b) for b in views]
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(max_workers=jobs) as pool:
+                processed = list(pool.map(block_processor, views))
+        res = np.empty_like(host)
+        for b, blk in enumerate(processed):
+            blk = np.asarray(blk)
+            if blk.shape != (2, n_blk):
+                raise ValueError(f"block processor returned shape {blk.shape}, expected (2, {n_blk})")
+            res[b] = blk
+        return torch.from_numpy(res).to(blocks.device)
+
+    return _framed_run(sig, plan, on_host, device, "complex128")

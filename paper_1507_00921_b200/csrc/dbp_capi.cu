@@ -126,6 +126,10 @@ struct dbp_plan {
   void* h_pin[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
   size_t pin_bytes = 0;
   cudaEvent_t done[2] = {nullptr, nullptr};
+  // dbp_run_host's whole-item pipeline: copy-in, compute and copy-out
+  // streams joined per slot by events, so each copy engine runs back to back
+  cudaStream_t pipe[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t ev_in[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr}, ev_out[2] = {nullptr, nullptr};
   dbp::HostPool* pool = nullptr;   // the process-wide conversion pool (not owned)
   // block lengths outside the fused kernel's [16, 8192]: the float64
   // multi-kernel path (dbp_general.cuh) with natural-order float64 tables
@@ -345,6 +349,31 @@ int ensure_staging(dbp_plan* p, size_t bytes) {
   return DBP_OK;
 }
 
+int ensure_pipeline(dbp_plan* p) {
+  for (int s = 0; s < 3; ++s)
+    if (!p->pipe[s]) DBP_CUDA(cudaStreamCreateWithFlags(&p->pipe[s], cudaStreamNonBlocking), "cudaStreamCreate");
+  for (int s = 0; s < 2; ++s) {
+    if (!p->ev_in[s]) DBP_CUDA(cudaEventCreateWithFlags(&p->ev_in[s], cudaEventDisableTiming), "cudaEventCreate");
+    if (!p->ev_k[s]) DBP_CUDA(cudaEventCreateWithFlags(&p->ev_k[s], cudaEventDisableTiming), "cudaEventCreate");
+    if (!p->ev_out[s]) DBP_CUDA(cudaEventCreateWithFlags(&p->ev_out[s], cudaEventDisableTiming), "cudaEventCreate");
+  }
+  return DBP_OK;
+}
+
+// bytes of one pipelined chunk of dbp_run_host (DBP_HOST_CHUNK_MB, default
+// 64 MiB, capped by the staging budget / 4).  Measured on the configs[3]
+// batch (profiles/r2/session4/ab_host_chunk.txt): 64 MiB reaches 0.93 of the
+// bidirectional pinned-copy rate, 32 / 16 / 8 / 4 MiB 0.92 / 0.90 / 0.85 /
+// 0.75 -- per-chunk costs outweigh the shorter pipeline fill and drain
+size_t host_chunk_bytes() {
+  static const size_t b = [] {
+    const char* v = std::getenv("DBP_HOST_CHUNK_MB");
+    const long long mb = v && *v ? std::atoll(v) : 64;
+    return (size_t)(mb > 0 ? mb : 64) << 20;
+  }();
+  return b;
+}
+
 }  // namespace
 
 extern "C" {
@@ -413,6 +442,16 @@ int dbp_plan_create(dbp_plan** out, int device, int block_len, int overlap) {
 int dbp_plan_destroy(dbp_plan* p) {
   if (!p) return DBP_OK;
   DeviceGuard g(p->device);
+  for (int s = 0; s < 3; ++s)
+    if (p->pipe[s]) {
+      cudaStreamSynchronize(p->pipe[s]);
+      cudaStreamDestroy(p->pipe[s]);
+    }
+  for (int s = 0; s < 2; ++s) {
+    if (p->ev_in[s]) cudaEventDestroy(p->ev_in[s]);
+    if (p->ev_k[s]) cudaEventDestroy(p->ev_k[s]);
+    if (p->ev_out[s]) cudaEventDestroy(p->ev_out[s]);
+  }
   for (int s = 0; s < 2; ++s) {
     if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
     for (int k = 0; k < 2; ++k)
@@ -707,6 +746,8 @@ int dbp_plan_synchronize(dbp_plan* p) {
   DeviceGuard g(p->device);
   for (int s = 0; s < 2; ++s)
     if (p->streams[s]) DBP_CUDA(cudaStreamSynchronize(p->streams[s]), "cudaStreamSynchronize");
+  for (int s = 0; s < 3; ++s)
+    if (p->pipe[s]) DBP_CUDA(cudaStreamSynchronize(p->pipe[s]), "cudaStreamSynchronize");
   return DBP_OK;
 }
 
@@ -737,6 +778,8 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
     ~StreamDrain() {
       for (int s = 0; s < 2; ++s)
         if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
+      for (int s = 0; s < 3; ++s)
+        if (p->pipe[s]) cudaStreamSynchronize(p->pipe[s]);
     }
   } drain{p};
 
@@ -746,30 +789,45 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
   // (unless that span would wrap onto itself: a short waveform).
   const bool span_fits = (block_end - block_begin) * p->step + p->M <= n_total;
   if (item <= slot_budget && (full_range || !span_fits)) {
-    // whole items per chunk, cyclic mode, two streams ping-pong
-    const int per = (int)std::min<size_t>((size_t)batch, slot_budget / item);
+    // whole items per chunk, cyclic mode: copy-in / compute / copy-out
+    // streams, two buffer slots, per-slot events guarding buffer reuse
+    const size_t chunk = std::min(slot_budget, std::max(item, host_chunk_bytes()));
+    const int per = (int)std::min<size_t>((size_t)batch, std::max<size_t>(1, chunk / item));
     rc = ensure_staging(p, per * item);
     if (rc) return rc;
-    int slot = 0;
-    for (int i0 = 0; i0 < batch; i0 += per, slot ^= 1) {
+    rc = ensure_pipeline(p);
+    if (rc) return rc;
+    cudaStream_t s_in = p->pipe[0], s_k = p->pipe[1], s_out = p->pipe[2];
+    int k = 0;
+    for (int i0 = 0; i0 < batch; i0 += per, ++k) {
+      const int slot = k & 1;
       const int cnt = std::min(per, batch - i0);
-      cudaStream_t s = p->streams[slot];
       void* din = p->d_stage[slot][0];
       void* dout = p->d_stage[slot][1];
-      DBP_CUDA(cudaMemcpyAsync(din, src + (size_t)i0 * item, cnt * item, cudaMemcpyHostToDevice, s), "H2D");
-      rc = dbp_run(p, din, dout, n_total, cnt, block_begin, block_end, s);
+      // din[slot] was last read by the kernel of chunk k - 2
+      if (k >= 2) DBP_CUDA(cudaStreamWaitEvent(s_in, p->ev_k[slot], 0), "cudaStreamWaitEvent");
+      DBP_CUDA(cudaMemcpyAsync(din, src + (size_t)i0 * item, cnt * item, cudaMemcpyHostToDevice, s_in), "H2D");
+      DBP_CUDA(cudaEventRecord(p->ev_in[slot], s_in), "cudaEventRecord");
+      DBP_CUDA(cudaStreamWaitEvent(s_k, p->ev_in[slot], 0), "cudaStreamWaitEvent");
+      // dout[slot] was last read by the copy-out of chunk k - 2
+      if (k >= 2) DBP_CUDA(cudaStreamWaitEvent(s_k, p->ev_out[slot], 0), "cudaStreamWaitEvent");
+      rc = dbp_run(p, din, dout, n_total, cnt, block_begin, block_end, s_k);
       if (rc) return rc;
+      DBP_CUDA(cudaEventRecord(p->ev_k[slot], s_k), "cudaEventRecord");
+      DBP_CUDA(cudaStreamWaitEvent(s_out, p->ev_k[slot], 0), "cudaStreamWaitEvent");
       if (full_range) {
-        DBP_CUDA(cudaMemcpyAsync(dst + (size_t)i0 * item, dout, cnt * item, cudaMemcpyDeviceToHost, s), "D2H");
+        DBP_CUDA(cudaMemcpyAsync(dst + (size_t)i0 * item, dout, cnt * item, cudaMemcpyDeviceToHost, s_out), "D2H");
       } else {
         for (int it = 0; it < cnt; ++it)
           for (int pol = 0; pol < 2; ++pol) {
             const size_t off = (size_t)it * item + pol * row + out_lo * sizeof(float2);
             DBP_CUDA(cudaMemcpyAsync(dst + (size_t)i0 * item + off, static_cast<char*>(dout) + off,
-                                     (out_hi - out_lo) * sizeof(float2), cudaMemcpyDeviceToHost, s), "D2H");
+                                     (out_hi - out_lo) * sizeof(float2), cudaMemcpyDeviceToHost, s_out), "D2H");
           }
       }
+      DBP_CUDA(cudaEventRecord(p->ev_out[slot], s_out), "cudaEventRecord");
     }
+    for (int s = 0; s < 3; ++s) DBP_CUDA(cudaStreamSynchronize(p->pipe[s]), "cudaStreamSynchronize");
   } else {
     // one item larger than a staging slot: block-range chunks with halos
     const int64_t span_budget = (int64_t)(slot_budget / (2 * sizeof(float2)));

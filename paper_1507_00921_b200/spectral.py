@@ -10,7 +10,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native
-from .backprop import BlockProcessor, GpuBlockProcessor, block_processor, overlap_save_run  # noqa: F401
+from .backprop import BlockProcessor, DeviceBlockProcessor, GpuBlockProcessor, block_processor, overlap_save_run  # noqa: F401
 from .framing import OverlapPlan, fft_frequencies, is_power_of_two, next_power_of_two  # noqa: F401
 from .params import DualPolSignal  # noqa: F401
 

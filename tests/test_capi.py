@@ -53,6 +53,23 @@ def test_invalid_geometry_rejected_before_device_lookup():
     assert lib.dbp_version() >= 102
 
 
+def test_framing_validates_before_touching_the_device():
+    lib = _native.load_library()
+    f, u = lib.dbp_frame_blocks, lib.dbp_unframe_blocks
+    assert f(None, None, 100, 1, 1000, 100, 0, 1, 8, None) == _native.DBP_EINVAL
+    assert b"power of two" in lib.dbp_last_error()
+    assert f(None, None, 100, 1, 1024, 1024, 0, 1, 8, None) == _native.DBP_EINVAL
+    assert u(None, None, 100, 1, 1024, 100, 0, 1, 12, None) == _native.DBP_EINVAL
+    assert b"elem_bytes" in lib.dbp_last_error()
+    assert u(None, None, 100, 1, 1024, 100, 0, 2, 8, None) == _native.DBP_EINVAL   # one block only
+    assert b"block range" in lib.dbp_last_error()
+    assert f(None, None, 0, 1, 1024, 100, 0, 0, 8, None) == _native.DBP_EINVAL
+    # nothing to do: no device needed
+    assert f(None, None, 100, 0, 1024, 100, 0, 1, 16, None) == _native.DBP_OK
+    assert f(None, None, 100, 1, 1024, 100, 0, 1, 8, None) == _native.DBP_EINVAL   # null buffers
+    assert b"null" in lib.dbp_last_error()
+
+
 def test_missing_library_fails_loudly(tmp_path):
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         _native.load_library(tmp_path / "nope.so")
