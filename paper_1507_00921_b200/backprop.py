@@ -15,6 +15,8 @@ is returned as the reference's complex128 ``DualPolSignal``.
 from __future__ import annotations
 
 import math
+import os
+import sys
 import threading
 import warnings
 from collections import OrderedDict
@@ -206,6 +208,75 @@ def get_engine(cfg: DbpConfig, sample_rate: float, device: int = 0) -> DbpEngine
     return eng
 
 
+class _RowArena:
+    """Recycled complex128 output rows for ``backpropagate``.
+
+    The reference returns freshly allocated rows (sigkit.py:56-68); a fresh
+    numpy row of this size is an anonymous mapping whose first write faults
+    in every 4 KiB page -- at the configs[0] length that costs more than the
+    whole GPU round trip (`profiles/r2/final/session5/dropin_latency_*.txt`).
+    The arena keeps the rows it handed out and gives one out again only once
+    nothing outside the arena refers to it any more (every view, slice or
+    ``DualPolSignal`` of a row holds a reference to it through ``.base``), so
+    callers still own distinct, non-aliased results.  ``DBP_HOST_ARENA_MB``
+    bounds the bytes the arena tracks (default 2048, 0 disables it).
+    """
+
+    _MIN_BYTES = 1 << 16      # smaller rows come from the heap and never fault
+
+    def __init__(self, cap_bytes: int):
+        self._cap = int(cap_bytes)
+        self._lock = threading.Lock()
+        self._rows: list[np.ndarray] = []    # least recently handed out first
+
+    def _idle(self, i: int) -> bool:
+        # the list's reference plus getrefcount's argument
+        return sys.getrefcount(self._rows[i]) == 2
+
+    def take(self, n: int) -> np.ndarray:
+        nbytes = 16 * n
+        if nbytes < self._MIN_BYTES or 2 * nbytes > self._cap:
+            return np.empty(n, dtype=np.complex128)
+        with self._lock:
+            rows = self._rows
+            for i in range(len(rows)):
+                if rows[i].size == n and self._idle(i):
+                    row = rows.pop(i)
+                    rows.append(row)
+                    return row[:]
+            total = sum(r.nbytes for r in rows)
+            i = 0
+            while total + nbytes > self._cap and i < len(rows):
+                if self._idle(i):
+                    total -= rows[i].nbytes
+                    del rows[i]
+                else:
+                    i += 1
+            row = np.empty(n, dtype=np.complex128)
+            if total + nbytes <= self._cap:
+                rows.append(row)
+            return row[:]
+
+    def tracked_bytes(self) -> int:
+        with self._lock:
+            return sum(r.nbytes for r in self._rows)
+
+    def clear(self) -> None:
+        with self._lock:
+            self._rows.clear()
+
+
+def _arena_cap_bytes() -> int:
+    try:
+        mb = int(os.environ.get("DBP_HOST_ARENA_MB", "2048"))
+    except ValueError:
+        mb = 2048
+    return max(0, mb) << 20
+
+
+_OUT_ROWS = _RowArena(_arena_cap_bytes())
+
+
 def _warn_short_overlap(cfg: DbpConfig, sample_rate: float, stacklevel: int):
     span = cfg.link.span
     memory = (channel_memory_samples(span.beta2, cfg.link.total_length, sample_rate)
@@ -284,7 +355,7 @@ def backpropagate(sig: DualPolSignal, cfg: DbpConfig, jobs: int = 1, *,
         # pinned staging, chunked H2D / kernel / D2H pipeline
         eng = get_engine(cfg, sig.sample_rate, devs[0])
         x, y = np.ascontiguousarray(sig.x, dtype=np.complex128), np.ascontiguousarray(sig.y, dtype=np.complex128)
-        out_x, out_y = np.empty_like(x), np.empty_like(y)
+        out_x, out_y = _OUT_ROWS.take(x.size), _OUT_ROWS.take(y.size)
         with eng.native.lock:
             eng.native.backpropagate_c128(x, y, out_x, out_y)
         return DualPolSignal(out_x, out_y, sig.sample_rate)

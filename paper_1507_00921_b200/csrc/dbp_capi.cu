@@ -909,26 +909,46 @@ int ensure_pinned(dbp_plan* p, size_t bytes) {
   return DBP_OK;
 }
 
-// dst[i] = (float2) src[(g0 + i) mod n] for i < len, over the host pool
-void narrow_span(dbp::HostPool* pool, const double2* src, int64_t n, int64_t g0, int64_t len, float2* dst) {
+// dst[pol][i] = (float2) src[pol][(g0 + i) mod n] for i < len (rows of pitch len), both
+// polarisations in one pass over the host pool
+void narrow_span(dbp::HostPool* pool, const double2* const src[2], int64_t n, int64_t g0, int64_t len, float2* dst) {
   pool->parallel_for(len, [&](long long lo, long long hi) {
-    long long i = lo;
-    while (i < hi) {
-      int64_t g = (g0 + i) % n;
-      if (g < 0) g += n;
-      const long long run = std::min<long long>(hi - i, n - g);
-      const double2* s = src + g;
-      float2* d = dst + i;
-      for (long long k = 0; k < run; ++k) d[k] = make_float2((float)s[k].x, (float)s[k].y);
-      i += run;
+    for (int pol = 0; pol < 2; ++pol) {
+      long long i = lo;
+      while (i < hi) {
+        int64_t g = (g0 + i) % n;
+        if (g < 0) g += n;
+        const long long run = std::min<long long>(hi - i, n - g);
+        const double2* s = src[pol] + g;
+        float2* d = dst + pol * len + i;
+        for (long long k = 0; k < run; ++k) d[k] = make_float2((float)s[k].x, (float)s[k].y);
+        i += run;
+      }
     }
   });
 }
 
-void widen(dbp::HostPool* pool, const float2* src, int64_t len, double2* dst) {
+// dst[pol][k] = (double2) src[pol][k] for k < len (src rows of pitch len)
+void widen(dbp::HostPool* pool, const float2* src, int64_t len, double2* const dst[2]) {
   pool->parallel_for(len, [&](long long lo, long long hi) {
-    for (long long k = lo; k < hi; ++k) dst[k] = make_double2((double)src[k].x, (double)src[k].y);
+    for (int pol = 0; pol < 2; ++pol) {
+      const float2* s = src + pol * len;
+      double2* d = dst[pol];
+      for (long long k = lo; k < hi; ++k) d[k] = make_double2((double)s[k].x, (double)s[k].y);
+    }
   });
+}
+
+// samples per polarisation and chunk of the complex128 drop-in pipeline: a
+// quarter of the signal, so that even one configs[0] waveform overlaps its
+// casts with its copies, within [2^16, 2^21] (DBP_C128_CHUNK overrides)
+int64_t c128_chunk_samples(int64_t n_total) {
+  static const int64_t forced = [] {
+    const char* v = std::getenv("DBP_C128_CHUNK");
+    return v && *v ? std::atoll(v) : 0LL;
+  }();
+  if (forced > 0) return forced;
+  return std::min<int64_t>(int64_t(1) << 21, std::max<int64_t>(int64_t(1) << 16, n_total / 4));
 }
 
 }  // namespace
@@ -943,8 +963,11 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
   const double2* in[2] = {static_cast<const double2*>(h_x), static_cast<const double2*>(h_y)};
   double2* out[2] = {static_cast<double2*>(h_out_x), static_cast<double2*>(h_out_y)};
   const int64_t nb = (n_total + p->step - 1) / p->step;
-  // chunk: a block range whose halo'd span is ~2^21 samples per polarisation
-  const int64_t per_blocks = std::max<int64_t>(1, ((int64_t(1) << 21) - p->M) / p->step);
+  // chunk: a block range whose halo'd span is c128_chunk_samples() per polarisation
+  // (balanced: the nearest whole number of equal chunks)
+  const int64_t per0 = std::max<int64_t>(1, (c128_chunk_samples(n_total) - p->M) / p->step);
+  const int64_t want_chunks = std::max<int64_t>(1, (nb + per0 / 2) / per0);
+  const int64_t per_blocks = (nb + want_chunks - 1) / want_chunks;
   const bool single = nb <= per_blocks || per_blocks * p->step + p->M > n_total;
   const int64_t span_cap = single ? n_total : per_blocks * p->step + p->M;
   const int64_t out_cap = single ? n_total : per_blocks * p->step;
@@ -978,7 +1001,8 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
     int64_t olo, ohi;
     out_range(k, olo, ohi);
     const float2* pin = static_cast<const float2*>(p->h_pin[slot][1]);
-    for (int pol = 0; pol < 2; ++pol) widen(p->pool, pin + pol * (ohi - olo), ohi - olo, out[pol] + olo);
+    double2* const dst[2] = {out[0] + olo, out[1] + olo};
+    widen(p->pool, pin, ohi - olo, dst);
     return DBP_OK;
   };
   for (int64_t k = 0; k < n_chunks; ++k) {
@@ -992,14 +1016,14 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
     int64_t olo, ohi;
     out_range(k, olo, ohi);
     if (single) {
-      for (int pol = 0; pol < 2; ++pol) narrow_span(p->pool, in[pol], n_total, 0, n_total, pin_in + pol * n_total);
+      narrow_span(p->pool, in, n_total, 0, n_total, pin_in);
       DBP_CUDA(cudaMemcpyAsync(din, pin_in, 2 * n_total * sizeof(float2), cudaMemcpyHostToDevice, s), "H2D");
       rc = dbp_run(p, din, dout, n_total, 1, 0, nb, s);
       if (rc) return rc;
     } else {
       const int64_t b0 = k * per_blocks, b1 = std::min(nb, b0 + per_blocks);
       const int64_t span = (b1 - b0) * p->step + p->M, g0 = b0 * p->step - p->lead;
-      for (int pol = 0; pol < 2; ++pol) narrow_span(p->pool, in[pol], n_total, g0, span, pin_in + pol * span);
+      narrow_span(p->pool, in, n_total, g0, span, pin_in);
       DBP_CUDA(cudaMemcpyAsync(din, pin_in, 2 * span * sizeof(float2), cudaMemcpyHostToDevice, s), "H2D");
       rc = dbp_run_chunk(p, din, dout, n_total, 1, b0, b1, span, ohi - olo, s);
       if (rc) return rc;

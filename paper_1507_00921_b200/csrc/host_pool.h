@@ -33,8 +33,14 @@ class HostPool {
   // calling thread runs piece 0; returns when every piece is done.  Callers
   // on different threads (plans on different devices sharing the pool) are
   // serialised.
-  void parallel_for(long long count, const std::function<void(long long, long long)>& fn) {
-    if (n_ == 1 || count < 4096) {
+  //
+  // Only as many threads take part as the work pays for (`grain` items per
+  // piece): waking a sleeping worker costs tens of microseconds, more than
+  // converting a few thousand samples on the calling thread.
+  void parallel_for(long long count, const std::function<void(long long, long long)>& fn,
+                    long long grain = 8192) {
+    const int pieces = (int)std::max<long long>(1, std::min<long long>(n_, count / std::max<long long>(1, grain)));
+    if (pieces == 1) {
       fn(0, count);
       return;
     }
@@ -43,32 +49,36 @@ class HostPool {
       std::lock_guard<std::mutex> g(mu_);
       fn_ = &fn;
       count_ = count;
-      pending_ = n_ - 1;
+      pieces_ = pieces;
+      pending_ = pieces - 1;
       ++gen_;
     }
     cv_.notify_all();
-    run_piece(0);
+    run_piece(0, pieces);
     std::unique_lock<std::mutex> lk(mu_);
     done_cv_.wait(lk, [this] { return pending_ == 0; });
     fn_ = nullptr;
   }
 
  private:
-  void run_piece(int i) {
-    const long long per = (count_ + n_ - 1) / n_;
+  void run_piece(int i, int pieces) {
+    const long long per = (count_ + pieces - 1) / pieces;
     const long long lo = std::min<long long>(count_, per * i), hi = std::min<long long>(count_, lo + per);
     if (hi > lo) (*fn_)(lo, hi);
   }
   void loop(int i) {
     unsigned long long seen = 0;
     for (;;) {
+      int pieces;
       {
         std::unique_lock<std::mutex> lk(mu_);
         cv_.wait(lk, [&] { return gen_ != seen; });
         seen = gen_;
         if (stop_) return;
+        pieces = pieces_;
       }
-      run_piece(i);
+      if (i >= pieces) continue;   // this call does not need worker i (the caller waits for pieces - 1)
+      run_piece(i, pieces);
       {
         std::lock_guard<std::mutex> g(mu_);
         if (--pending_ == 0) done_cv_.notify_one();
@@ -81,7 +91,7 @@ class HostPool {
   std::condition_variable cv_, done_cv_;
   const std::function<void(long long, long long)>* fn_ = nullptr;
   long long count_ = 0;
-  int pending_ = 0, n_ = 1;
+  int pending_ = 0, pieces_ = 1, n_ = 1;
   unsigned long long gen_ = 0;
   bool stop_ = false;
 };

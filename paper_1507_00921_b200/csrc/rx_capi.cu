@@ -13,8 +13,8 @@
 // feeding that output); one symbol costs a 4-level half-warp butterfly
 // reduction plus the tap update, with the next symbol's inputs prefetched.
 // Spectral searches (4th-power frequency peak, reference and bit-alignment
-// correlations) are cuFFT double-precision transforms followed by arg-max
-// kernels; the sliding-window phase estimate, the unwrap prefix scan,
+// correlations) are float64 Stockham transforms (fft64.cuh, no cuFFT) followed
+// by arg-max kernels; the sliding-window phase estimate, the unwrap prefix scan,
 // decisions and error counting are elementwise / reduction kernels.
 #include <cuda_runtime.h>
 #include "fft64.cuh"

@@ -486,6 +486,31 @@ def test_multi_device_split_bit_equal(rng, batch):
     np.testing.assert_array_equal(out.stack(), one[0])
 
 
+def test_dropin_results_are_distinct_arrays_across_calls(rng):
+    # the recycled output rows (backprop._RowArena) never alias a result the caller still
+    # holds, and a recycled row is fully rewritten (spectral.py:145: the output is a new array)
+    n_total = 1 << 16
+    span = pb.FiberParams(-21.6826, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    sigs = [pb.DualPolSignal(*(0.02 * (rng.normal(size=(2, n_total)) + 1j * rng.normal(size=(2, n_total)))), 56e9)
+            for _ in range(3)]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        kept = [pb.backpropagate(s, cfg) for s in sigs]
+        copies = [k.stack() for k in kept]
+        for _ in range(4):                                  # dropped results free their rows ...
+            pb.backpropagate(sigs[1], cfg)
+        again = pb.backpropagate(sigs[0], cfg)              # ... and a recycled row holds only the new result
+    rows = [r for k in kept + [again] for r in (k.x, k.y)]
+    for i in range(len(rows)):
+        for j in range(i + 1, len(rows)):
+            assert not np.shares_memory(rows[i], rows[j])
+    for k, c in zip(kept, copies):
+        np.testing.assert_array_equal(k.stack(), c)         # untouched by the later calls
+    np.testing.assert_array_equal(again.stack(), copies[0])
+
+
 @pytest.mark.parametrize("n_total", [1, 5, 1348, 4099, (1 << 17), (1 << 22) + 777])
 def test_dropin_complex128_path_bit_equal(rng, n_total):
     # backpropagate(sig, cfg) on complex128 rows (dbp_backpropagate_c128: host-thread casts,

@@ -161,3 +161,31 @@ def test_gpu_entry_points_fail_loudly_without_a_device():
                           pb.SsfmStepConfig(1))
     with pytest.raises(RuntimeError):
         pb.butterfly_equalize(pb.DualPolSignal(x[0], x[1], 56e9))
+
+
+def test_output_row_arena_never_aliases_live_results():
+    # backprop._RowArena: the complex128 output rows of backpropagate() are recycled only
+    # once nothing refers to them (sigkit.py:56-68 promises the caller its own arrays)
+    arena = backprop._RowArena(16 << 20)
+    n = 1 << 16                                            # 1 MiB rows
+    a, b = arena.take(n), arena.take(n)
+    assert a.dtype == np.complex128 and a.shape == (n,) and not np.shares_memory(a, b)
+    addr = a.__array_interface__["data"][0]
+    part = a[7:99]                                         # a slice keeps the row busy
+    sig = pb.DualPolSignal(b, b, 1.0)                      # so does a signal built on it
+    baddr = b.__array_interface__["data"][0]
+    del a, b
+    c = arena.take(n)
+    assert c.__array_interface__["data"][0] not in (addr, baddr)
+    del part
+    d = arena.take(n)
+    assert d.__array_interface__["data"][0] == addr        # recycled once free
+    assert arena.take(n // 2).size == n // 2               # other lengths get their own rows
+    del sig
+    # the cap bounds what is tracked; rows that do not fit are plain allocations
+    held = [arena.take(n) for _ in range(40)]
+    assert arena.tracked_bytes() <= 16 << 20
+    assert len({h.__array_interface__["data"][0] for h in held}) == 40
+    small = arena.take(16)                                 # heap-sized rows bypass the arena
+    assert small.base is None
+    assert backprop._RowArena(0).take(n).base is None      # DBP_HOST_ARENA_MB=0: disabled
