@@ -6,11 +6,15 @@
 // across the ABI: failures return a negative code and leave a message in a
 // thread-local string (dbp_last_error).
 #include <cuda_runtime.h>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include <algorithm>
 #include <atomic>
 #include <thread>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -909,9 +913,51 @@ int ensure_pinned(dbp_plan* p, size_t bytes) {
   return DBP_OK;
 }
 
+// Host casts of the complex128 drop-in path.  Rows of 2^18 samples and more
+// are written with SSE2 streaming stores: the pinned staging is read next by
+// the copy engine and a result row of that size does not stay in cache, so
+// write-allocating those lines only adds a third to the casts' memory traffic
+// (cvtpd2ps / cvtps2pd round exactly like the scalar casts).
+long long stream_min_len() {   // DBP_HOST_STREAM_MIN: shortest row (samples) cast with streaming stores
+  static const long long v = [] {
+    const char* e = std::getenv("DBP_HOST_STREAM_MIN");
+    return e && *e ? std::atoll(e) : (1LL << 18);
+  }();
+  return v;
+}
+
+inline void narrow_run(const double2* s, float2* d, long long run, bool stream) {
+  long long k = 0;
+#if defined(__SSE2__)
+  if (stream) {
+    for (; k < run && (reinterpret_cast<uintptr_t>(d + k) & 15); ++k) d[k] = make_float2((float)s[k].x, (float)s[k].y);
+    for (; k + 2 <= run; k += 2) {
+      const __m128 a = _mm_cvtpd_ps(_mm_loadu_pd(reinterpret_cast<const double*>(s + k)));
+      const __m128 b = _mm_cvtpd_ps(_mm_loadu_pd(reinterpret_cast<const double*>(s + k + 1)));
+      _mm_stream_ps(reinterpret_cast<float*>(d + k), _mm_movelh_ps(a, b));
+    }
+  }
+#endif
+  for (; k < run; ++k) d[k] = make_float2((float)s[k].x, (float)s[k].y);
+}
+
+inline void widen_run(const float2* s, double2* d, long long lo, long long hi, bool stream) {
+  long long k = lo;
+#if defined(__SSE2__)
+  if (stream && (reinterpret_cast<uintptr_t>(d) & 15) == 0) {
+    for (; k < hi; ++k) {
+      const __m128 v = _mm_castpd_ps(_mm_load_sd(reinterpret_cast<const double*>(s + k)));
+      _mm_stream_pd(reinterpret_cast<double*>(d + k), _mm_cvtps_pd(v));
+    }
+  }
+#endif
+  for (; k < hi; ++k) d[k] = make_double2((double)s[k].x, (double)s[k].y);
+}
+
 // dst[pol][i] = (float2) src[pol][(g0 + i) mod n] for i < len (rows of pitch len), both
 // polarisations in one pass over the host pool
 void narrow_span(dbp::HostPool* pool, const double2* const src[2], int64_t n, int64_t g0, int64_t len, float2* dst) {
+  const bool stream = len >= stream_min_len();
   pool->parallel_for(len, [&](long long lo, long long hi) {
     for (int pol = 0; pol < 2; ++pol) {
       long long i = lo;
@@ -919,23 +965,24 @@ void narrow_span(dbp::HostPool* pool, const double2* const src[2], int64_t n, in
         int64_t g = (g0 + i) % n;
         if (g < 0) g += n;
         const long long run = std::min<long long>(hi - i, n - g);
-        const double2* s = src[pol] + g;
-        float2* d = dst + pol * len + i;
-        for (long long k = 0; k < run; ++k) d[k] = make_float2((float)s[k].x, (float)s[k].y);
+        narrow_run(src[pol] + g, dst + pol * len + i, run, stream);
         i += run;
       }
     }
+#if defined(__SSE2__)
+    if (stream) _mm_sfence();
+#endif
   });
 }
 
 // dst[pol][k] = (double2) src[pol][k] for k < len (src rows of pitch len)
 void widen(dbp::HostPool* pool, const float2* src, int64_t len, double2* const dst[2]) {
+  const bool stream = len >= stream_min_len();
   pool->parallel_for(len, [&](long long lo, long long hi) {
-    for (int pol = 0; pol < 2; ++pol) {
-      const float2* s = src + pol * len;
-      double2* d = dst[pol];
-      for (long long k = lo; k < hi; ++k) d[k] = make_double2((double)s[k].x, (double)s[k].y);
-    }
+    for (int pol = 0; pol < 2; ++pol) widen_run(src + pol * len, dst[pol], lo, hi, stream);
+#if defined(__SSE2__)
+    if (stream) _mm_sfence();
+#endif
   });
 }
 
