@@ -119,10 +119,11 @@ int dbp_run_chunk(dbp_plan* plan, const void* d_in, void* d_out, int64_t n_total
                   void* stream);
 
 /* Host-buffer run: h_in/h_out are [batch][2][n_total] complex64 in host
- * memory (pinned for full PCIe speed, pageable accepted).  Copies in,
- * processes blocks [block_begin, block_end) and copies the kept samples
- * out, pipelined over two streams; returns after completion (the
- * reference's synchronous semantics).                                        */
+ * memory (pinned for full PCIe speed; pageable rows of whole waveforms of
+ * 2^16 samples and more are staged through the plan's pinned buffers by
+ * host threads, same bits).  Copies in, processes blocks [block_begin,
+ * block_end) and copies the kept samples out, pipelined over two streams;
+ * returns after completion (the reference's synchronous semantics).          */
 int dbp_run_host(dbp_plan* plan, const void* h_in, void* h_out, int64_t n_total, int batch,
                  int64_t block_begin, int64_t block_end);
 

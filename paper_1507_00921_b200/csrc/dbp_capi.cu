@@ -96,6 +96,7 @@ namespace dbp_capi_internal {
 int fail(int code, const std::string& msg) { return ::fail(code, msg); }
 void add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_total() { return g_launches.load(); }
+int run_host_staged(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, int batch);
 }  // namespace dbp_capi_internal
 
 struct dbp_plan {
@@ -774,6 +775,10 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
   if (out_hi > n_total) out_hi = n_total;
   const char* src = static_cast<const char*>(h_in);
   char* dst = static_cast<char*>(h_out);
+  if (full_range) {   // pageable rows: through pinned staging on the host pool
+    rc = dbp_capi_internal::run_host_staged(p, h_in, h_out, n_total, batch);
+    if (rc != 1) return rc;
+  }
   // copies that read / write the caller's host buffers may still be queued
   // when a later call fails: drain both staging streams before returning,
   // so the caller can free its buffers on any return code
@@ -879,6 +884,7 @@ int dbp_run_host(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, in
   return DBP_OK;
 }
 
+extern "C++" {
 namespace {
 
 // one host conversion pool for the process (DBP_HOST_THREADS threads, default
@@ -954,9 +960,35 @@ inline void widen_run(const float2* s, double2* d, long long lo, long long hi, b
   for (; k < hi; ++k) d[k] = make_double2((double)s[k].x, (double)s[k].y);
 }
 
+// complex64 rows (a caller's pageable buffers staged through pinned memory): plain copies
+inline void copy_run(const float2* s, float2* d, long long run, bool stream) {
+  long long k = 0;
+#if defined(__SSE2__)
+  if (stream) {
+    for (; k < run && (reinterpret_cast<uintptr_t>(d + k) & 15); ++k) d[k] = s[k];
+    for (; k + 8 <= run; k += 8) {
+      const __m128 a = _mm_loadu_ps(reinterpret_cast<const float*>(s + k));
+      const __m128 b = _mm_loadu_ps(reinterpret_cast<const float*>(s + k + 2));
+      const __m128 c = _mm_loadu_ps(reinterpret_cast<const float*>(s + k + 4));
+      const __m128 e = _mm_loadu_ps(reinterpret_cast<const float*>(s + k + 6));
+      _mm_stream_ps(reinterpret_cast<float*>(d + k), a);
+      _mm_stream_ps(reinterpret_cast<float*>(d + k + 2), b);
+      _mm_stream_ps(reinterpret_cast<float*>(d + k + 4), c);
+      _mm_stream_ps(reinterpret_cast<float*>(d + k + 6), e);
+    }
+  }
+#endif
+  std::memcpy(d + k, s + k, (size_t)(run - k) * sizeof(float2));
+}
+inline void narrow_run(const float2* s, float2* d, long long run, bool stream) { copy_run(s, d, run, stream); }
+inline void widen_run(const float2* s, float2* d, long long lo, long long hi, bool stream) {
+  copy_run(s + lo, d + lo, hi - lo, stream);
+}
+
 // dst[pol][i] = (float2) src[pol][(g0 + i) mod n] for i < len (rows of pitch len), both
 // polarisations in one pass over the host pool
-void narrow_span(dbp::HostPool* pool, const double2* const src[2], int64_t n, int64_t g0, int64_t len, float2* dst) {
+template <typename Elem>
+void narrow_span(dbp::HostPool* pool, const Elem* const src[2], int64_t n, int64_t g0, int64_t len, float2* dst) {
   const bool stream = len >= stream_min_len();
   pool->parallel_for(len, [&](long long lo, long long hi) {
     for (int pol = 0; pol < 2; ++pol) {
@@ -975,8 +1007,9 @@ void narrow_span(dbp::HostPool* pool, const double2* const src[2], int64_t n, in
   });
 }
 
-// dst[pol][k] = (double2) src[pol][k] for k < len (src rows of pitch len)
-void widen(dbp::HostPool* pool, const float2* src, int64_t len, double2* const dst[2]) {
+// dst[pol][k] = (Elem) src[pol][k] for k < len (src rows of pitch len)
+template <typename Elem>
+void widen(dbp::HostPool* pool, const float2* src, int64_t len, Elem* const dst[2]) {
   const bool stream = len >= stream_min_len();
   pool->parallel_for(len, [&](long long lo, long long hi) {
     for (int pol = 0; pol < 2; ++pol) widen_run(src + pol * len, dst[pol], lo, hi, stream);
@@ -986,40 +1019,40 @@ void widen(dbp::HostPool* pool, const float2* src, int64_t len, double2* const d
   });
 }
 
-// samples per polarisation and chunk of the complex128 drop-in pipeline: a
-// quarter of the signal, so that even one configs[0] waveform overlaps its
-// casts with its copies, within [2^16, 2^21] (DBP_C128_CHUNK overrides)
-int64_t c128_chunk_samples(int64_t n_total) {
+// samples per polarisation and chunk of the staged host pipeline: a quarter
+// of the signal, so that even one configs[0] waveform overlaps its casts with
+// its copies, within [2^16, 2^21]; a batch of four items and more fills the
+// pipeline with its other items and takes whole items up to 2^21 samples
+// (DBP_C128_CHUNK overrides)
+int64_t c128_chunk_samples(int64_t n_total, int batch) {
   static const int64_t forced = [] {
     const char* v = std::getenv("DBP_C128_CHUNK");
     return v && *v ? std::atoll(v) : 0LL;
   }();
   if (forced > 0) return forced;
-  return std::min<int64_t>(int64_t(1) << 21, std::max<int64_t>(int64_t(1) << 16, n_total / 4));
+  const int64_t want = batch >= 4 ? n_total : n_total / 4;
+  return std::min<int64_t>(int64_t(1) << 21, std::max<int64_t>(int64_t(1) << 16, want));
 }
 
-}  // namespace
-
-int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* h_out_x, void* h_out_y,
-                           int64_t n_total) {
-  int rc = check_ready(p);
-  if (rc) return rc;
-  if (!h_x || !h_y || !h_out_x || !h_out_y) return fail(DBP_EINVAL, "null host buffer");
-  if (n_total < 1) return fail(DBP_EINVAL, "signal must contain at least one sample");
-  DeviceGuard g(p->device);
-  const double2* in[2] = {static_cast<const double2*>(h_x), static_cast<const double2*>(h_y)};
-  double2* out[2] = {static_cast<double2*>(h_out_x), static_cast<double2*>(h_out_y)};
+// Host rows staged through pinned memory, for `batch` items of two rows each
+// (Elem = double2: the reference's complex128 rows, cast on the host pool;
+// float2: a caller's pageable complex64 rows, copied).  The chunks -- whole
+// items, or block ranges with halos of one item -- run as one pipeline over
+// all items: host copy-in, H2D, kernel, D2H on the chunk's stream (two slots),
+// host copy-out two chunks later.
+template <typename Elem, typename InRow, typename OutRow>
+int staged_pipeline(dbp_plan* p, InRow in_row, OutRow out_row, int64_t n_total, int batch) {
   const int64_t nb = (n_total + p->step - 1) / p->step;
   // chunk: a block range whose halo'd span is c128_chunk_samples() per polarisation
   // (balanced: the nearest whole number of equal chunks)
-  const int64_t per0 = std::max<int64_t>(1, (c128_chunk_samples(n_total) - p->M) / p->step);
+  const int64_t per0 = std::max<int64_t>(1, (c128_chunk_samples(n_total, batch) - p->M) / p->step);
   const int64_t want_chunks = std::max<int64_t>(1, (nb + per0 / 2) / per0);
   const int64_t per_blocks = (nb + want_chunks - 1) / want_chunks;
   const bool single = nb <= per_blocks || per_blocks * p->step + p->M > n_total;
   const int64_t span_cap = single ? n_total : per_blocks * p->step + p->M;
   const int64_t out_cap = single ? n_total : per_blocks * p->step;
   const size_t in_bytes = (size_t)2 * span_cap * sizeof(float2), out_bytes = (size_t)2 * out_cap * sizeof(float2);
-  rc = ensure_staging(p, std::max(in_bytes, out_bytes));
+  int rc = ensure_staging(p, std::max(in_bytes, out_bytes));
   if (rc) return rc;
   rc = ensure_pinned(p, std::max(in_bytes, out_bytes));
   if (rc) return rc;
@@ -1030,15 +1063,16 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
         if (p->streams[s]) cudaStreamSynchronize(p->streams[s]);
     }
   } drain{p};
-  const int64_t n_chunks = single ? 1 : (nb + per_blocks - 1) / per_blocks;
-  // output of chunk k: [olo, ohi) per polarisation
+  const int64_t per_item = single ? 1 : (nb + per_blocks - 1) / per_blocks;
+  const int64_t n_chunks = per_item * batch;
+  // output of chunk k (chunk k % per_item of item k / per_item): [olo, ohi) per polarisation
   auto out_range = [&](int64_t k, int64_t& olo, int64_t& ohi) {
     if (single) {
       olo = 0;
       ohi = n_total;
       return;
     }
-    const int64_t b0 = k * per_blocks, b1 = std::min(nb, b0 + per_blocks);
+    const int64_t b0 = (k % per_item) * per_blocks, b1 = std::min(nb, b0 + per_blocks);
     olo = b0 * p->step;
     ohi = std::min<int64_t>(n_total, b1 * p->step);
   };
@@ -1048,8 +1082,9 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
     int64_t olo, ohi;
     out_range(k, olo, ohi);
     const float2* pin = static_cast<const float2*>(p->h_pin[slot][1]);
-    double2* const dst[2] = {out[0] + olo, out[1] + olo};
-    widen(p->pool, pin, ohi - olo, dst);
+    const int item = (int)(k / per_item);
+    Elem* const dst[2] = {out_row(item, 0) + olo, out_row(item, 1) + olo};
+    widen<Elem>(p->pool, pin, ohi - olo, dst);
     return DBP_OK;
   };
   for (int64_t k = 0; k < n_chunks; ++k) {
@@ -1060,17 +1095,19 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
     float2* pin_out = static_cast<float2*>(p->h_pin[slot][1]);
     char* din = static_cast<char*>(p->d_stage[slot][0]);
     char* dout = static_cast<char*>(p->d_stage[slot][1]);
+    const int item = (int)(k / per_item);
+    const Elem* const in[2] = {in_row(item, 0), in_row(item, 1)};
     int64_t olo, ohi;
     out_range(k, olo, ohi);
     if (single) {
-      narrow_span(p->pool, in, n_total, 0, n_total, pin_in);
+      narrow_span<Elem>(p->pool, in, n_total, 0, n_total, pin_in);
       DBP_CUDA(cudaMemcpyAsync(din, pin_in, 2 * n_total * sizeof(float2), cudaMemcpyHostToDevice, s), "H2D");
       rc = dbp_run(p, din, dout, n_total, 1, 0, nb, s);
       if (rc) return rc;
     } else {
-      const int64_t b0 = k * per_blocks, b1 = std::min(nb, b0 + per_blocks);
+      const int64_t b0 = (k % per_item) * per_blocks, b1 = std::min(nb, b0 + per_blocks);
       const int64_t span = (b1 - b0) * p->step + p->M, g0 = b0 * p->step - p->lead;
-      narrow_span(p->pool, in, n_total, g0, span, pin_in);
+      narrow_span<Elem>(p->pool, in, n_total, g0, span, pin_in);
       DBP_CUDA(cudaMemcpyAsync(din, pin_in, 2 * span * sizeof(float2), cudaMemcpyHostToDevice, s), "H2D");
       rc = dbp_run_chunk(p, din, dout, n_total, 1, b0, b1, span, ohi - olo, s);
       if (rc) return rc;
@@ -1081,6 +1118,54 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
   for (int64_t k = std::max<int64_t>(0, n_chunks - 2); k < n_chunks; ++k)
     if ((rc = finish(k))) return rc;
   return DBP_OK;
+}
+
+// true when a host pointer is ordinary pageable memory (not cudaHostAlloc / cudaHostRegister)
+bool is_pageable(const void* ptr) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+}  // namespace
+
+namespace dbp_capi_internal {
+// dbp_run_host on pageable complex64 buffers (whole items of 2^16 samples and
+// more): cudaMemcpyAsync from pageable memory is a synchronous driver-staged
+// copy, so the rows go through the plan's pinned staging on the host pool
+// instead (DBP_STAGE_PAGEABLE=0: the plain copies).  Returns 1 when the call
+// was not taken.
+int run_host_staged(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total, int batch) {
+  static const bool enabled = [] {
+    const char* v = std::getenv("DBP_STAGE_PAGEABLE");
+    return !(v && *v == '0');
+  }();
+  if (!enabled || n_total < (int64_t(1) << 16)) return 1;
+  if (!is_pageable(h_in) && !is_pageable(h_out)) return 1;
+  const float2* src = static_cast<const float2*>(h_in);
+  float2* dst = static_cast<float2*>(h_out);
+  return staged_pipeline<float2>(
+      p, [&](int item, int pol) { return src + ((int64_t)2 * item + pol) * n_total; },
+      [&](int item, int pol) { return dst + ((int64_t)2 * item + pol) * n_total; }, n_total, batch);
+}
+}  // namespace dbp_capi_internal
+
+}  // extern "C++"
+
+int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* h_out_x, void* h_out_y,
+                           int64_t n_total) {
+  int rc = check_ready(p);
+  if (rc) return rc;
+  if (!h_x || !h_y || !h_out_x || !h_out_y) return fail(DBP_EINVAL, "null host buffer");
+  if (n_total < 1) return fail(DBP_EINVAL, "signal must contain at least one sample");
+  DeviceGuard g(p->device);
+  const double2* in[2] = {static_cast<const double2*>(h_x), static_cast<const double2*>(h_y)};
+  double2* out[2] = {static_cast<double2*>(h_out_x), static_cast<double2*>(h_out_y)};
+  return staged_pipeline<double2>(
+      p, [&](int, int pol) { return in[pol]; }, [&](int, int pol) { return out[pol]; }, n_total, 1);
 }
 
 int dbp_plan_set_coeff_batch(dbp_plan* p, const double* coeffs, int n_sets, int n_coeffs) {

@@ -486,6 +486,33 @@ def test_multi_device_split_bit_equal(rng, batch):
     np.testing.assert_array_equal(out.stack(), one[0])
 
 
+@pytest.mark.parametrize("batch,n_total", [(1, (1 << 16)), (1, (1 << 19) + 5), (5, (1 << 16) + 123), (4, 1 << 18)])
+def test_pageable_host_rows_bit_equal_pinned(rng, batch, n_total):
+    # dbp_run_host on ordinary numpy (pageable) rows goes through pinned staging on the host
+    # pool, whole items or block-range chunks with halos (run_host_staged); on page-locked
+    # buffers it copies directly: same bits either way (spectral.py:100-101, blocks independent)
+    from paper_1507_00921_b200 import _native
+    span = pb.FiberParams(-21.6826, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    x = (0.02 * (rng.normal(size=(batch, 2, n_total)) + 1j * rng.normal(size=(batch, 2, n_total)))).astype(np.complex64)
+    eng = pb.get_engine(cfg, 56e9)
+    got = np.empty_like(x)
+    eng.run_host(x, got)
+    pin_in, pin_out = _native.PinnedBuffer(x.shape), _native.PinnedBuffer(x.shape)
+    try:
+        pin_in.array[...] = x
+        eng.run_host(pin_in.array, pin_out.array)
+        np.testing.assert_array_equal(got, pin_out.array)
+        # mixed: pageable in, pinned out
+        pin_out.array[...] = 0
+        eng.run_host(x, pin_out.array)
+        np.testing.assert_array_equal(got, pin_out.array)
+    finally:
+        pin_in.free()
+        pin_out.free()
+
+
 def test_dropin_results_are_distinct_arrays_across_calls(rng):
     # the recycled output rows (backprop._RowArena) never alias a result the caller still
     # holds, and a recycled row is fully rewritten (spectral.py:145: the output is a new array)

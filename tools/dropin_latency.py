@@ -37,3 +37,15 @@ for lg in (12, 14, 17, 20, 24):
     c = t(lambda: eng.run_host(x64, out64))
     print(f"n=2^{lg}: backpropagate {a:8.1f} us  native c128 (preallocated out) {b:8.1f} us  run_host c64 {c:8.1f} us"
           f"  -> {n / a / 1e3:.3f} GS/s drop-in (dual-pol samples)")
+
+# a batch of pageable complex64 waveforms through backpropagate_batch (configs[3] shape, reduced batch)
+rng = np.random.default_rng(1)
+xb = (0.02 * (rng.normal(size=(32, 2, 1 << 18)) + 1j * rng.normal(size=(32, 2, 1 << 18)))).astype(np.complex64)
+ob = np.empty_like(xb)
+eng = pb.get_engine(cfg, 56e9)
+eng.run_host(xb, ob)
+t0 = time.perf_counter()
+for _ in range(5):
+    eng.run_host(xb, ob)
+sec = (time.perf_counter() - t0) / 5
+print(f"batch 32 x 2^18 pageable complex64 run_host: {sec * 1e3:.2f} ms -> {32 * (1 << 18) / sec / 1e9:.3f} GS/s")
