@@ -123,7 +123,7 @@ def kernel_name(a) -> str:
         # N = 8192 split-step programs: the radix-2-around-4096 kernel (csrc/dbp_r2_kernel.cuh)
         return f"dbp::dbp_r2_kernel<{kernel_prog(a)}, {kernel_twp(a)}>"
     ps = a.algorithm == "ffe" and logn >= 11
-    return f"dbp::dbp_block_kernel<{logn}, {kernel_prog(a)}, {kernel_twp(a)}{', 1' if ps else ''}>"
+    return f"dbp::dbp_block_kernel<{logn}, {kernel_prog(a)}, {kernel_twp(a)}{', 1' if ps else ', 0'}>"
 
 
 def kernel_prog(a) -> int:
