@@ -133,9 +133,12 @@ int dbp_run_host(dbp_plan* plan, const void* h_in, void* h_out, int64_t n_total,
  * h_out_y: complex128 results of the same length.  The whole signal, cyclic
  * framing (spectral.py:122-145).  The complex128 -> complex64 casts (numpy's
  * astype rounding) and back run on host threads (DBP_HOST_THREADS, default
- * min(16, cores)) into pinned staging, pipelined over block-range chunks of
- * ~2^21 samples with halos against the H2D copy, the kernel and the D2H
- * copy.  Synchronous; bitwise equal to dbp_run_host on the complex64 cast.   */
+ * min(16, cores)) into pinned staging, pipelined over block-range chunks
+ * (a quarter of the signal within [2^16, 2^21] samples) with halos against
+ * the H2D copy, the kernel and the D2H copy.  The result rows must not
+ * overlap the input rows or each other (DBP_EINVAL): like the reference
+ * (spectral.py:129) the call never mutates its input.  Synchronous; bitwise
+ * equal to dbp_run_host on the complex64 cast.                               */
 int dbp_backpropagate_c128(dbp_plan* plan, const void* h_x, const void* h_y, void* h_out_x, void* h_out_y,
                            int64_t n_total);
 

@@ -1145,6 +1145,12 @@ int run_host_staged(dbp_plan* p, const void* h_in, void* h_out, int64_t n_total,
   }();
   if (!enabled || n_total < (int64_t(1) << 16)) return 1;
   if (!is_pageable(h_in) && !is_pageable(h_out)) return 1;
+  // in place (or overlapping) buffers keep the plain path, which uploads a whole item before
+  // it writes any of its output: here a later chunk's halo would read rows already rewritten
+  const char* a0 = static_cast<const char*>(h_in);
+  const char* b0 = static_cast<const char*>(h_out);
+  const size_t bytes = (size_t)batch * 2 * n_total * sizeof(float2);
+  if (a0 < b0 + bytes && b0 < a0 + bytes) return 1;
   const float2* src = static_cast<const float2*>(h_in);
   float2* dst = static_cast<float2*>(h_out);
   return staged_pipeline<float2>(
@@ -1164,6 +1170,14 @@ int dbp_backpropagate_c128(dbp_plan* p, const void* h_x, const void* h_y, void* 
   DeviceGuard g(p->device);
   const double2* in[2] = {static_cast<const double2*>(h_x), static_cast<const double2*>(h_y)};
   double2* out[2] = {static_cast<double2*>(h_out_x), static_cast<double2*>(h_out_y)};
+  // the reference never mutates its input (spectral.py:129): a chunk's halo is read after
+  // earlier chunks' results are written, so the result rows must be separate from the input rows
+  for (int i = 0; i < 2; ++i)
+    for (int o = 0; o < 2; ++o)
+      if (in[i] < out[o] + n_total && out[o] < in[i] + n_total)
+        return fail(DBP_EINVAL, "result rows must not overlap the input rows");
+  if (out[0] < out[1] + n_total && out[1] < out[0] + n_total)
+    return fail(DBP_EINVAL, "result rows must not overlap each other");
   return staged_pipeline<double2>(
       p, [&](int, int pol) { return in[pol]; }, [&](int, int pol) { return out[pol]; }, n_total, 1);
 }

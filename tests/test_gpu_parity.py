@@ -513,6 +513,29 @@ def test_pageable_host_rows_bit_equal_pinned(rng, batch, n_total):
         pin_out.free()
 
 
+def test_in_place_host_rows(rng):
+    # dbp_run_host in place (h_out == h_in) keeps the plain whole-item path and its result;
+    # dbp_backpropagate_c128 refuses result rows that overlap its input (spectral.py:129:
+    # the reference never mutates its input)
+    n_total = (1 << 18) + 77
+    span = pb.FiberParams(-21.6826, 1.3, 0.2, 80.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(2048, 700), quiet_link(40, span), num_steps=1,
+                       coeffs=pb.EssfmCoefficients(waveforms.gaussian_coeffs(17)))
+    x = (0.02 * (rng.normal(size=(1, 2, n_total)) + 1j * rng.normal(size=(1, 2, n_total)))).astype(np.complex64)
+    eng = pb.get_engine(cfg, 56e9)
+    want = eng.run_host(x)
+    buf = x.copy()
+    eng.run_host(buf, buf)
+    np.testing.assert_array_equal(buf, want)
+    xs = x[0].astype(np.complex128)
+    other = np.empty(n_total, np.complex128)
+    with eng.native.lock:
+        with pytest.raises(ValueError, match="overlap"):
+            eng.native.backpropagate_c128(xs[0], xs[1], xs[0], other)
+        with pytest.raises(ValueError, match="overlap"):
+            eng.native.backpropagate_c128(xs[0], xs[1], other, other)
+
+
 def test_dropin_results_are_distinct_arrays_across_calls(rng):
     # the recycled output rows (backprop._RowArena) never alias a result the caller still
     # holds, and a recycled row is fully rewritten (spectral.py:145: the output is a new array)
