@@ -76,6 +76,11 @@ VARIANTS = {
     "dittab": ["-DDBP_DIT_TABLED=1"],
     "dittab_all": ["-DDBP_DIT_TABLED=1", "-DDBP_DIT_MAX_STEPS=1000", "-DDBP_DIT_MAX_LOGN=13"],
     "noio": ["-DDBP_EXPERIMENT_NOLOAD=1", "-DDBP_EXPERIMENT_NOSTORE=1"],
+    # last session: ptxas register-usage level (default 5) at the 64-register cap
+    "rul0": ["-Xptxas", "--register-usage-level=0"],
+    "rul3": ["-Xptxas", "--register-usage-level=3"],
+    "rul8": ["-Xptxas", "--register-usage-level=8"],
+    "rul10": ["-Xptxas", "--register-usage-level=10"],
 }
 if __name__ == "__main__":
     names = sys.argv[1:] or list(VARIANTS)
