@@ -486,7 +486,7 @@ def test_multi_device_split_bit_equal(rng, batch):
     np.testing.assert_array_equal(out.stack(), one[0])
 
 
-@pytest.mark.parametrize("batch,n_total", [(1, (1 << 16)), (1, (1 << 19) + 5), (5, (1 << 16) + 123), (4, 1 << 18)])
+@pytest.mark.parametrize("batch,n_total", [(1, (1 << 16)), (1, (1 << 19) + 5), (3, (1 << 18) + 11), (5, (1 << 16) + 123), (4, 1 << 18)])
 def test_pageable_host_rows_bit_equal_pinned(rng, batch, n_total):
     # dbp_run_host on ordinary numpy (pageable) rows goes through pinned staging on the host
     # pool, whole items or block-range chunks with halos (run_host_staged); on page-locked
