@@ -28,6 +28,11 @@ FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-diag-suppress", "177"]
 
 
+# per-unit flags: the N = 2048 FFE polarisation-split kernel gains 1.9% at ptxas register-usage
+# level 8, every other kernel is fastest at the default (profiles/r2/ab_regusage.txt, ab_ffe_unit.txt)
+UNIT_FLAGS = {"dbp_kernel_ffe_ps": ["-Xptxas", "--register-usage-level=8"]}
+
+
 def nvcc() -> str:
     exe = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
     if not Path(exe).exists():
@@ -63,7 +68,8 @@ def build(force: bool = False, verbose: bool = False, extra_flags=None, lib: Pat
     for src in _sources():
         obj = obj_root / (src.stem + ".o")
         if force or _stale(obj, [src, *headers, Path(__file__)]):
-            cmd = [nvcc(), *ARCH, *FLAGS, *extra, *env_flags, "-I", str(CSRC), "-I", str(INCLUDE),
+            cmd = [nvcc(), *ARCH, *FLAGS, *UNIT_FLAGS.get(src.stem, []), *extra, *env_flags,
+                   "-I", str(CSRC), "-I", str(INCLUDE),
                    "-c", str(src), "-o", str(obj)]
             jobs.append((src, obj, cmd))
 

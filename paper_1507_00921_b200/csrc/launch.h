@@ -321,6 +321,9 @@ cudaError_t launch_r2t(const KernelParams& kp0, cudaStream_t stream) {
   return cudaGetLastError();
 }
 
+// launch_polsplit<11> (the FFE program as polarisation-split pairs at N = 2048), dbp_kernel_ffe_ps.cu
+cudaError_t launch_polsplit_ffe_2048(const KernelParams& kp, cudaStream_t stream);
+
 template <int LOGN>
 cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, size_t smem_bytes,
                                      cudaStream_t stream) {
@@ -333,7 +336,12 @@ cudaError_t launch_block_kernel_impl(const KernelParams& kp, long long n_ctas, s
   if constexpr (LOGN == 13) {
     if (polsplit_enabled<LOGN>(kp)) return launch_polsplit<LOGN>(kp, stream);
   } else if constexpr (LOGN >= 10 && LOGN <= 12) {
-    if (polsplit_enabled<LOGN>(kp)) return launch_polsplit<LOGN>(kp, stream);
+    // the N = 2048 FFE pairs are instantiated in their own unit (dbp_kernel_ffe_ps.cu),
+    // which build.py compiles with its own ptxas register-usage level
+    if (polsplit_enabled<LOGN>(kp)) {
+      if constexpr (LOGN == 11) return launch_polsplit_ffe_2048(kp, stream);
+      else return launch_polsplit<LOGN>(kp, stream);
+    }
   }
   if constexpr (LOGN >= 10 && LOGN <= 12) {
     if (kp.program == kFFE && kp.wtw != nullptr && kp.tab_nat != nullptr && warp_ffe_enabled()) return launch_warp_ffe<LOGN - 6>(kp, stream);
