@@ -147,6 +147,7 @@ struct dbp_plan {
   double2* d_work = nullptr;      // ... the FFT's ping-pong partner ...
   double* d_inten = nullptr;      // ... and [block][N] intensities
   long long ws_blocks = 0;
+  cudaEvent_t ws_done = nullptr;  // end of the last launch that used the workspace (any stream)
 };
 
 namespace {
@@ -243,6 +244,13 @@ int launch_general(const dbp_plan* cp, const dbp::KernelParams& kp, cudaStream_t
   }
   dg::Taps taps{};
   for (int i = 0; i <= p->nc && i < dg::kMaxTaps; ++i) taps.c[i] = p->c64[i];
+  // one workspace per plan: calls on different streams (the two slots of the
+  // host pipelines) take turns, each waiting for the previous call's kernels
+  if (!p->ws_done) {
+    DBP_CUDA(cudaEventCreateWithFlags(&p->ws_done, cudaEventDisableTiming), "cudaEventCreate");
+  } else {
+    DBP_CUDA(cudaStreamWaitEvent(s, p->ws_done, 0), "cudaStreamWaitEvent");
+  }
   long long launches = 0;
   for (long long blk0 = 0; blk0 < kp.total_blocks; blk0 += chunk) {
     const long long nblk = std::min(chunk, kp.total_blocks - blk0);
@@ -279,6 +287,7 @@ int launch_general(const dbp_plan* cp, const dbp::KernelParams& kp, cudaStream_t
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(e, "general block-length path launch");
+  DBP_CUDA(cudaEventRecord(p->ws_done, s), "cudaEventRecord");
   g_launches.fetch_add(launches, std::memory_order_relaxed);
   return DBP_OK;
 }
@@ -482,6 +491,7 @@ int dbp_plan_destroy(dbp_plan* p) {
   cudaFree(p->d_ws);
   cudaFree(p->d_work);
   cudaFree(p->d_inten);
+  if (p->ws_done) cudaEventDestroy(p->ws_done);
   delete p;
   return DBP_OK;
 }

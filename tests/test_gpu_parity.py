@@ -735,6 +735,29 @@ def test_general_block_lengths_match_oracle(n_blk, m, alg, arr, steps):
     assert err <= 1e-6, (n_blk, m, alg, arr, err)   # float64 inside: only the complex64 I/O rounding
 
 
+@pytest.mark.parametrize("n_blk,m,n", [(16384, 3000, 4 * 16384 + 2), (32768, 12419, 117994)])
+def test_general_block_lengths_through_the_host_pipelines(n_blk, m, n):
+    # the staged host pipelines run consecutive chunks on two streams; the general path's
+    # kernels share one workspace per plan, so its launches must take turns
+    # (launch_general's ws_done event).  Found by tools/fuzz_parity.py --seed 4242:
+    # garbage at N = 32768, n = 117994 before the event.  Repeated: a race is timing dependent.
+    rng = np.random.default_rng(n)
+    span = pb.FiberParams(-21.68, 1.3, 0.2, 60.0)
+    cfg = pb.DbpConfig("essfm", pb.OverlapPlan(n_blk, m), quiet_link(2, span), num_steps=8,
+                       coeffs=pb.EssfmCoefficients(np.r_[1.0, 0.05 * rng.normal(size=23)]),
+                       arrangement="linear-first")
+    x = (0.02 * (rng.normal(size=(2, 2, n)) + 1j * rng.normal(size=(2, 2, n)))).astype(np.complex64)
+    want = [dbp_port.backpropagate_arrays(x[i].astype(np.complex128), 56e9, port_config(cfg)) for i in range(2)]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        for _ in range(3):
+            got = pb.backpropagate_batch(x, 56e9, cfg)                      # pageable complex64 rows
+            for i in range(2):
+                assert dbp_port.per_block_rel_l2(got[i], want[i], n_blk, m).max() <= 1e-6
+            one = pb.backpropagate(pb.DualPolSignal(x[0, 0], x[0, 1], 56e9), cfg).stack()   # complex128 rows
+            assert dbp_port.per_block_rel_l2(one, want[0], n_blk, m).max() <= 1e-6
+
+
 def test_general_block_length_multi_chunk_and_chunk_mode_in_subprocess():
     # a small workspace budget (DBP_GENERAL_WS_MB) forces many block chunks;
     # the chunk-mode entry (dbp_run_chunk over two halves) must equal the
