@@ -234,16 +234,22 @@ class _RowArena:
         return sys.getrefcount(self._rows[i]) == 2
 
     def take(self, n: int) -> np.ndarray:
-        nbytes = 16 * n
+        """A complex128 row of n samples (the rows of a ``DualPolSignal`` result)."""
+        return self.take_array((n,), np.complex128)
+
+    def take_array(self, shape, dtype) -> np.ndarray:
+        """An uninitialised C-contiguous array; every caller overwrites all of it."""
+        dt = np.dtype(dtype)
+        nbytes = int(np.prod(shape)) * dt.itemsize
         if nbytes < self._MIN_BYTES or 2 * nbytes > self._cap:
-            return np.empty(n, dtype=np.complex128)
+            return np.empty(shape, dtype=dt)
         with self._lock:
-            rows = self._rows
+            rows = self._rows                 # owners: 1-D byte arrays
             for i in range(len(rows)):
-                if rows[i].size == n and self._idle(i):
+                if rows[i].nbytes == nbytes and self._idle(i):
                     row = rows.pop(i)
                     rows.append(row)
-                    return row[:]
+                    return row.view(dt).reshape(shape)
             total = sum(r.nbytes for r in rows)
             i = 0
             while total + nbytes > self._cap and i < len(rows):
@@ -252,10 +258,10 @@ class _RowArena:
                     del rows[i]
                 else:
                     i += 1
-            row = np.empty(n, dtype=np.complex128)
+            row = np.empty(nbytes, dtype=np.uint8)
             if total + nbytes <= self._cap:
                 rows.append(row)
-            return row[:]
+            return row.view(dt).reshape(shape)
 
     def tracked_bytes(self) -> int:
         with self._lock:
@@ -313,7 +319,7 @@ def backpropagate_batch(samples: np.ndarray, sample_rate: float, cfg: DbpConfig,
         raise ValueError("expected (batch, 2, n) samples with n >= 1")
     _warn_short_overlap(cfg, sample_rate, stacklevel=2)
     devs = _resolve_devices(device, devices)
-    out = np.zeros_like(x)
+    out = _OUT_ROWS.take_array(x.shape, np.complex64)   # every sample is overwritten below
     if len(devs) == 1:
         return get_engine(cfg, sample_rate, devs[0]).run_host(x, out)
     b, _, n = x.shape

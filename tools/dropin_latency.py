@@ -49,3 +49,10 @@ for _ in range(5):
     eng.run_host(xb, ob)
 sec = (time.perf_counter() - t0) / 5
 print(f"batch 32 x 2^18 pageable complex64 run_host: {sec * 1e3:.2f} ms -> {32 * (1 << 18) / sec / 1e9:.3f} GS/s")
+pb.backpropagate_batch(xb, 56e9, cfg)
+t0 = time.perf_counter()
+for _ in range(5):
+    res = pb.backpropagate_batch(xb, 56e9, cfg)
+sec = (time.perf_counter() - t0) / 5
+print(f"batch 32 x 2^18 pageable complex64 backpropagate_batch (result allocated by the call): {sec * 1e3:.2f} ms -> "
+      f"{32 * (1 << 18) / sec / 1e9:.3f} GS/s")
