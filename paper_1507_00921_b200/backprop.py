@@ -209,7 +209,8 @@ def get_engine(cfg: DbpConfig, sample_rate: float, device: int = 0) -> DbpEngine
 
 
 class _RowArena:
-    """Recycled complex128 output rows for ``backpropagate``.
+    """Recycled result arrays for ``backpropagate`` (complex128 rows) and
+    ``backpropagate_batch`` (the complex64 batch).
 
     The reference returns freshly allocated rows (sigkit.py:56-68); a fresh
     numpy row of this size is an anonymous mapping whose first write faults
